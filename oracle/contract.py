@@ -1,0 +1,184 @@
+"""Bucket elimination and Eq. (1) slicing (oracle; test infrastructure only).
+
+PAPER.md:361-368 (§4.2): the network is contracted by sequential elimination of
+its indices; the tensor produced by eliminating index i is indexed by the union
+of the index sets of the tensors containing i, minus i.  Buckets are keyed by
+the earliest index in the elimination order.  Each
+bucket is ONE numpy.einsum call (a library primitive serving as one step, in
+complex128); scalars are multiplied into a running accumulator.
+
+PAPER.md:519-524, Eq. (1):  sum_{m_1..m_n} ( sum_{V \\ {m_i}} T^1 ... T^N ).
+Step-dependent slicing: the prefix of the order is
+contracted once with the sliced indices still present, then every slice fixes
+the sliced indices in the remaining tensors and contracts the residual order.
+Slice results are summed in a fixed pairwise tree over the slice id j, bit b of
+j being the value of the b-th sliced label in ascending label order (A13, A14).
+
+`greedy_min_degree` is the oracle's OWN orderer (ties to the
+smallest label), independent of the product planner.
+"""
+from __future__ import annotations
+
+from typing import Dict, Iterable, List, Sequence, Tuple
+
+import numpy as np
+
+from .network import Tensor, fix_indices
+
+
+def _einsum_bucket(ts: Sequence[Tensor], v: int) -> Tensor:
+    union = sorted(set().union(*[set(l) for _, l in ts]) - {v})
+    local = {lab: i for i, lab in enumerate(union + [v])}
+    if len(local) > 52:
+        raise ValueError("bucket too wide for numpy.einsum sublists")
+    args = []
+    for arr, labs in ts:
+        args.append(arr)
+        args.append([local[l] for l in labs])
+    args.append([local[l] for l in union])
+    out = np.einsum(*args, optimize=False)
+    return np.asarray(out, dtype=np.complex128), tuple(union)
+
+
+def partial_eliminate(tensors: Sequence[Tensor], order: Sequence[int]):
+    """Eliminate the indices of `order` (in order); return (remaining tensors, scalar).
+
+    Tensors touching no index of `order` pass through unchanged.
+    """
+    pos = {lab: i for i, lab in enumerate(order)}
+    buckets: Dict[int, List[Tensor]] = {v: [] for v in order}
+    rest: List[Tensor] = []
+    scalar = complex(1.0)
+    for arr, labs in tensors:
+        if len(labs) == 0:
+            scalar *= complex(arr)
+            continue
+        ins = [l for l in labs if l in pos]
+        if ins:
+            buckets[min(ins, key=pos.__getitem__)].append((arr, tuple(labs)))
+        else:
+            rest.append((arr, tuple(labs)))
+    for v in order:
+        ts = buckets[v]
+        if not ts:
+            continue
+        arr, labs = _einsum_bucket(ts, v)
+        if len(labs) == 0:
+            scalar *= complex(arr)
+            continue
+        ins = [l for l in labs if l in pos]
+        if ins:
+            buckets[min(ins, key=pos.__getitem__)].append((arr, labs))
+        else:
+            rest.append((arr, labs))
+    return rest, scalar
+
+
+def bucket_eliminate(tensors: Sequence[Tensor], order: Sequence[int]) -> complex:
+    """Full contraction to a scalar along `order` (must cover every label)."""
+    rest, scalar = partial_eliminate(tensors, order)
+    if rest:
+        missing = sorted(set().union(*[set(l) for _, l in rest]))
+        raise ValueError(f"order misses live labels {missing[:8]}")
+    return scalar
+
+
+def pairwise_sum(vals: Sequence[complex]) -> complex:
+    """Fixed-order pairwise tree over the list index."""
+    vals = list(vals)
+    if not vals:
+        return complex(0.0)
+    while len(vals) > 1:
+        nxt = [vals[i] + vals[i + 1] for i in range(0, len(vals) - 1, 2)]
+        if len(vals) % 2:
+            nxt.append(vals[-1])
+        vals = nxt
+    return vals[0]
+
+
+def slice_assignment(sliced: Sequence[int], j: int) -> Dict[int, int]:
+    s = sorted(sliced)
+    return {lab: (j >> b) & 1 for b, lab in enumerate(s)}
+
+
+def contract_sliced(tensors: Sequence[Tensor], prefix: Sequence[int], sliced: Sequence[int],
+                    residual: Sequence[int], slices: Iterable[int] | None = None,
+                    return_parts: bool = False):
+    """Step-dependent sliced contraction, Eq. (1) with a shared prefix."""
+    rest, pscalar = partial_eliminate(tensors, prefix)
+    k = len(sliced)
+    js = range(1 << k) if slices is None else list(slices)
+    parts = []
+    for j in js:
+        sl = fix_indices(rest, slice_assignment(sliced, j))
+        parts.append(pscalar * bucket_eliminate(sl, residual))
+    total = pairwise_sum(parts)
+    return (total, parts) if return_parts else total
+
+
+# ------------------------------------------------------------------ line graph + own greedy
+def line_graph(tensors: Sequence[Tensor]) -> Dict[int, set]:
+    """Vertices = indices, one clique per tensor."""
+    adj: Dict[int, set] = {}
+    for _, labs in tensors:
+        for a in labs:
+            adj.setdefault(a, set())
+            for b in labs:
+                if a != b:
+                    adj[a].add(b)
+    return adj
+
+
+def eliminate_vertex(adj: Dict[int, set], v: int) -> None:
+    """Remove v and make its neighbourhood a clique."""
+    nb = adj.pop(v)
+    for a in nb:
+        adj[a].discard(v)
+        adj[a].update(nb - {a})
+
+
+def greedy_min_degree(tensors: Sequence[Tensor], exclude: Iterable[int] = ()) -> Tuple[List[int], List[int]]:
+    """Eliminate a lowest-degree vertex, ties -> smallest label."""
+    adj = line_graph(tensors)
+    ex = set(exclude)
+    order, degs = [], []
+    while True:
+        cand = [v for v in adj if v not in ex]
+        if not cand:
+            break
+        v = min(cand, key=lambda x: (len(adj[x]), x))
+        degs.append(len(adj[v]))
+        order.append(v)
+        eliminate_vertex(adj, v)
+    return order, degs
+
+
+def width_of_order(tensors: Sequence[Tensor], order: Sequence[int]) -> List[int]:
+    adj = line_graph(tensors)
+    degs = []
+    for v in order:
+        degs.append(len(adj[v]))
+        eliminate_vertex(adj, v)
+    return degs
+
+
+def contract(tensors: Sequence[Tensor], order: Sequence[int] | None = None) -> complex:
+    """sigma by bucket elimination; own greedy min-degree order unless given."""
+    if order is None:
+        order, _ = greedy_min_degree(tensors)
+    return bucket_eliminate(tensors, order)
+
+
+def brute_force(tensors: Sequence[Tensor]) -> complex:
+    """Sum over all assignments of all labels of the product (the plain definition;
+    PAPER.md:214, 233-234).  Only for <= ~22 labels."""
+    labs = sorted(set().union(*[set(l) for _, l in tensors])) if tensors else []
+    if len(labs) > 52:
+        raise ValueError("too many labels")
+    local = {l: i for i, l in enumerate(labs)}
+    args = []
+    for arr, ls in tensors:
+        args.append(arr)
+        args.append([local[l] for l in ls])
+    args.append([])
+    return complex(np.einsum(*args, optimize=False))
