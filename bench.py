@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: sliced single-amplitude contraction of the paper's 210-qubit QAOA circuit (C5a).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C5a]
+
+One STEP = one whole-job contraction sigma = <0^N|U(gamma, beta)|0^N> for a fresh (gamma, beta)
+draw: leaf materialization, the shared prefix, this rank's block of the 2^k slices (Eq. 1), the
+NCCL all-reduce of the per-slice partials (N > 1) -- every row of SURVEY.md §8(a) a6-a11.  The
+plan (a1-a5: instance, network, ordering, step-dependent slicing, lowering) depends only on the
+graph and is reused across parameters; its build time is reported
+separately in config.plan_s.
+
+value = contractions per second of the whole job (strong scaling: the total work -- one
+amplitude -- is fixed, the slices are split across ranks).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from tn_inputs import WORKLOADS, qaoa_angles, random_regular_graph  # noqa: E402
+
+MAX_WIDTH = {"C4a": 30, "C4b": 30, "C5a": 32, "C5b": 32, "C2": 62}
+K_RANGE = {"C4a": (8, 12), "C4b": (8, 12), "C5a": (3, 12), "C5b": (3, 14), "C2": (0, 0)}
+METRIC = "sliced single-amplitude contraction throughput (QAOA MaxCut, 3-regular)"
+
+
+def build_workload_plan(name: str = "C5a", seed: int = 0):
+    """Instance + plan for a named workload (reading A11 for k and the orderer)."""
+    import paper_2012_02430_b200 as T
+
+    w = WORKLOADS[name]
+    g = random_regular_graph(w.n, 3, seed)
+    ga, be = qaoa_angles(w.p, seed)
+    t0 = time.perf_counter()
+    kmin, kmax = K_RANGE.get(name, (0, 12))
+    plan, tried = T.select_sliced_plan(g, w.p, MAX_WIDTH.get(name, 32), k_min=kmin, k_max=kmax)
+    plan_s = time.perf_counter() - t0
+    meta = {"plan_s": plan_s, "tried": tried}
+    return plan, g, ga, be, meta
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle sample
+def oracle_sample(plan, g, ga, be, budget_s: float = 15.0, max_width: int = 22):
+    """Time the oracle (as it stands) on a bounded sample of the same contraction and scale it
+    to contractions/s.  The sample: the shared prefix, then slice 0 of the plan with the plan's
+    residual order as data, further sub-sliced (Eq. 1, exact) on the m indices that appear in the
+    most of the widest intermediates, until the width is <= max_width; as many sub-slices as fit
+    in `budget_s` are contracted; cost = prefix time + mean sub-slice time x 2^(k+m)."""
+    from oracle import contract, network
+
+    pre, sl, res, _ = plan.schedule()
+    t0 = time.perf_counter()
+    tens = network.qaoa_amplitude_network(g.n, g.edges, ga, be)
+    rest, _ = contract.partial_eliminate(tens, pre)
+    t_prefix = time.perf_counter() - t0
+    rest0 = network.fix_indices(rest, contract.slice_assignment(sl, 0))
+    extra = []
+    while True:
+        fixed = network.fix_indices(rest0, {l: 0 for l in extra})
+        order = [l for l in res if l not in extra]
+        adj = contract.line_graph(fixed)
+        steps = []
+        for v in order:
+            if v in adj:
+                steps.append((len(adj[v]), set(adj[v])))
+                contract.eliminate_vertex(adj, v)
+        w = max((d for d, _ in steps), default=0)
+        if w <= max_width:
+            break
+        cnt = {}
+        for d, nb in steps:
+            if d >= w - 1:
+                for u in nb:
+                    cnt[u] = cnt.get(u, 0) + 2.0 ** d
+        extra.append(max(cnt, key=lambda u: (cnt[u], -u)))
+    m = len(extra)
+    times = []
+    t_start = time.perf_counter()
+    j = 0
+    while (time.perf_counter() - t_start) < budget_s and j < (1 << m):
+        a = {l: (j >> b) & 1 for b, l in enumerate(sorted(extra))}
+        t1 = time.perf_counter()
+        contract.bucket_eliminate(network.fix_indices(rest0, a), order)
+        times.append(time.perf_counter() - t1)
+        j += 1
+    k = len(sl)
+    est = t_prefix + statistics.mean(times) * (2 ** (k + m))
+    return {"value": 1.0 / est, "unit": "contractions/s", "cores": 1, "kind": "oracle",
+            "sample": (f"prefix ({len(pre)} steps) + {len(times)} of 2^{m} sub-slices of slice 0 of 2^{k} "
+                       f"(plan residual order as data, width {w}, complex128 numpy.einsum per bucket, "
+                       f"1 thread), scaled x 2^{k + m}; est. {est:.3g} s per contraction"),
+            "sample_s": time.perf_counter() - t0}
+
+
+# ---------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5a")
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-budget", type=float, default=15.0)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return main_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2012_02430_b200 as T
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = T.TN_C64 if args.dtype == "c64" else T.TN_C128
+    plan, g, ga0, be0, meta = build_workload_plan(args.workload)
+    info = plan.info
+    n = plan.n_slices
+    from paper_2012_02430_b200.scheduler import slice_block
+    begin, end = slice_block(n, rank, world)
+    w = WORKLOADS[args.workload]
+    params = [qaoa_angles(w.p, 1000 + s) for s in range(args.warmup + args.steps)]
+    stream = torch.cuda.current_stream()
+    dev = torch.device("cuda", local)
+    partials = torch.zeros(2 * n, dtype=torch.float64, device=dev)
+    ws = plan.workspace(dtype, dev)
+
+    def step(ga, be):
+        partials.zero_()
+        if end > begin:
+            plan.contract_sliced(ga, be, begin, end, partials, dtype=dtype)
+        if world > 1:
+            dist.all_reduce(partials)
+
+    for s in range(args.warmup):
+        step(*params[s])
+    torch.cuda.synchronize()
+    plan.profile_read()                      # reset counters
+    plan.profile(True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.steps):
+        step(*params[args.warmup + s])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    plan.profile(False)
+    prof = plan.profile_read()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = 1000.0 / ms_step
+
+    # ---- e2e through the public API: host params in, host result out (D2H + host sum inside)
+    e2e_ms = []
+    for s in range(max(1, min(args.steps, 3))):
+        ga, be = params[s]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        partials.zero_()
+        if end > begin:
+            plan.contract_sliced(ga, be, begin, end, partials, dtype=dtype)
+        if world > 1:
+            dist.all_reduce(partials)
+        host = partials.cpu()
+        sigma = plan.sum_partials(host.tolist())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = 1000.0 / float(te.item())
+
+    # ---- roofline of the dominant kernel (standalone bucket-step launches, k_bucket)
+    peak, peak_src = load_peaks()
+    kb_ms = prof["ms"]
+    kb_bytes = prof["bytes"]
+    achieved = (kb_bytes / (kb_ms / 1e3)) / 1e9 if kb_ms > 0 else 0.0
+    gpu_launches = prof["all_launches"]
+    algo_bytes_step = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("bytes_per_algorithmic_byte")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "contractions/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 complex)" if dtype == T.TN_C64 else "c128 (fp64 complex)",
+        "data": "synthetic: seeded random 3-regular graph + U(0,pi) angles (tn_inputs)",
+        "config": {
+            "workload": f"{args.workload}: QAOA MaxCut p={w.p}, N={w.n} ({len(g.edges)} edges), single amplitude",
+            "n_qubits": w.n, "p": w.p, "seed": 0,
+            "plan": {"orderer": plan.orderer,
+                     "k": info["k"], "n_slices": n, "slice_step": info["slice_step"],
+                     "width": info["width"], "unsliced_width": info["unsliced_width"],
+                     "steps_per_slice": info["steps_per_slice"], "prefix_steps": info["prefix_steps"],
+                     "workspace_GB": info["workspace_bytes"][dtype] / 1e9},
+            "plan_s": meta["plan_s"],
+            "parallelism": f"slices x{world} (contiguous blocks, 1 NCCL all-reduce)",
+            "l2": "no flush needed: per-slice intermediates up to 2^%d x %d B >> 126 MB L2" % (
+                info["width"], 8 if dtype == T.TN_C64 else 16),
+            "algorithmic_GB_per_step": algo_bytes_step / 1e9,
+            "step_GBps_algorithmic": algo_bytes_step / (ms_step / 1e3) / 1e9,
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "kernel": "k_bucket (standalone bucket steps)", "peak_source": peak_src,
+                     "kernel_share_of_step": (kb_ms / args.steps) / ms_step if ms_step else None,
+                     "launches": prof["launches"]},
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "contractions/s",
+                "h2d_bytes_per_step": 2 * w.p * 8, "d2h_bytes_per_step": 16 * n},
+        "gpu_launches": gpu_launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = oracle_sample(plan, g, ga0, be0, budget_s=args.oracle_budget)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # never let the baseline break the bench line
+            line["cpu_baseline"] = {"value": None, "unit": "contractions/s", "cores": 1, "kind": "oracle",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_reference(args, rank, world):
+    """--impl reference: the oracle (as it stands) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import paper_2012_02430_b200 as T  # planning only (host code) to fix the same schedule
+
+    w = WORKLOADS[args.workload]
+    plan, g, ga, be, meta = build_workload_plan(args.workload)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps are no-ops
+    vals, samples = [], []
+    budget = max(3.0, min(args.oracle_budget, 150.0 / max(1, args.steps)))
+    for s in range(args.steps):
+        cb = oracle_sample(plan, g, ga, be, budget_s=budget)
+        vals.append(cb["value"])
+        samples.append(cb["sample"])
+    v = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "contractions/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128 (fp64 complex, numpy)", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: QAOA MaxCut p={w.p}, N={w.n}", "plan_k": plan.info["k"]},
+            "cpu_baseline": {"value": v, "unit": "contractions/s", "cores": 1, "kind": "oracle",
+                             "sample": samples[0]},
+            "e2e": {"value": v, "unit": "contractions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

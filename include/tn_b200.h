@@ -1,0 +1,157 @@
+/*
+ * tn_b200.h -- C ABI of the B200-native sliced bucket-elimination contractor
+ * for QAOA MaxCut tensor networks (arXiv:2012.02430, "Tensor Network Quantum
+ * Simulator With Step-Dependent Parallelization").
+ *
+ * Citations are PAPER.md line numbers (+ section / equation) of the paper text
+ * in the reference bundle.  The library is libtnb200.so; every entry point is
+ * extern "C", takes plain pointers and sizes, never throws, and returns a
+ * tn_status (0 = OK, < 0 = error; tn_last_error() has a thread-local message).
+ *
+ * Memory ownership: the caller owns every buffer passed in (host arrays,
+ * device workspace, result arrays) and the CUDA stream.  A tn_plan owns its
+ * host tables and, lazily, one small device copy of its step tables per
+ * device (freed by tn_plan_free).  The library never calls cudaMalloc for
+ * tensors: all intermediates live in the caller's workspace (`ws`).
+ * "Device" pointers below are CUDA global-memory pointers on the current
+ * device; "host" pointers are ordinary CPU memory.
+ */
+#ifndef TN_B200_H
+#define TN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tn_plan tn_plan; /* opaque, immutable after load, shareable across threads */
+
+typedef enum { TN_C64 = 0, TN_C128 = 1 } tn_dtype; /* complex64 / complex128 storage + arithmetic */
+
+typedef enum {
+  TN_OK = 0,
+  TN_E_INVAL = -1,    /* bad argument: p mismatch, begin > end, short workspace, null pointer */
+  TN_E_PLAN = -2,     /* malformed / version-mismatched plan, order misses a live label,
+                         n exceeds the live vertex count */
+  TN_E_TOO_WIDE = -3, /* contraction width above opts->max_width or device memory */
+  TN_E_NOMEM = -4,    /* host allocation failed */
+  TN_E_CUDA = -5,     /* a CUDA runtime call or kernel launch failed (message has the CUDA error) */
+  TN_E_DTYPE = -6     /* unsupported dtype */
+} tn_status;
+
+typedef enum { TN_KIND_AMPLITUDE = 0, TN_KIND_ENERGY = 1 } tn_kind;
+typedef enum { TN_ORDER_MIN_FILL = 0, TN_ORDER_MIN_DEGREE = 1 } tn_orderer;
+
+/* Planner options (§5.1 ordering; §5.3 step-dependent slicing). */
+typedef struct {
+  int32_t kind;           /* tn_kind */
+  int32_t orderer;        /* tn_orderer: greedy min-fill, or min-degree ("contracts the lowest-degree
+                             vertex"). Ties: min-fill -> lower degree -> smaller label;
+                             min-degree -> smaller label. */
+  int32_t n_sliced;       /* n of §5.3: number of sliced indices (0 = no slicing). Amplitude only. */
+  int32_t r;              /* r of §5.3: indices sliced per round (r == n: one slice step s; the
+                             paper's 210-qubit run). 0 means r = n. */
+  int32_t max_width;      /* > 0: fail with TN_E_TOO_WIDE if the contraction width exceeds it */
+  int32_t small_log2;     /* steps whose output has <= small_log2 indices run in the batched
+                             interpreter kernel; < 0 selects the default (12) */
+  int32_t reserved[4];    /* must be 0 */
+} tn_build_opts;
+
+typedef struct {
+  int32_t kind, n_qubits, p, n_edges;
+  int32_t width;          /* contraction width c = max_i N_{G_i}(v_i) over executed steps */
+  int32_t unsliced_width; /* width of the planner's full greedy order before slicing */
+  int32_t k;              /* number of sliced indices; 2^k slices (Eq. 1) */
+  int32_t slice_step;     /* s: length of the shared, unsliced prefix */
+  int32_t n_programs;     /* 1 (amplitude) or E = #edges (energy: one light cone per edge) */
+  int32_t n_labels;       /* live indices of the (first) network */
+  uint64_t n_slices;      /* 2^k */
+  uint64_t prefix_steps;  /* bucket steps run once per call (before slicing) */
+  uint64_t steps_per_slice;
+  uint64_t launches_prefix;    /* kernel launches of the prefix */
+  uint64_t launches_per_slice; /* kernel launches per slice (incl. the per-slice finalize) */
+  size_t workspace_bytes[2];   /* per tn_dtype: bytes of device workspace needed by every call */
+  double pred_bytes_per_slice[2]; /* algorithmic bytes of one slice: sum over steps of
+                                     (inputs read once + output written once) x sizeof(dtype) */
+  double pred_bytes_prefix[2];
+  double pred_bytes_big_per_slice[2]; /* the part of pred_bytes_per_slice in standalone launches */
+  uint64_t big_launches_per_slice;    /* standalone bucket-kernel launches per slice */
+} tn_plan_info_t;
+
+/* ---------------------------------------------------------------- planning (host only) */
+/* Build a plan for the QAOA MaxCut instance (graph, depth p).  edges: host int32[2*n_edges]
+ * (pairs i<j or j<i, 0-based).  kind AMPLITUDE: the single amplitude sigma = <0^N|U|0^N>
+ * (§5) as ONE network with live indices w(q,l) = l*N+q, l < p;
+ * kind ENERGY: one reverse-light-cone <Z_u Z_v> network per edge.
+ * Output: *buf (host, library-allocated; release with tn_buffer_free), *len bytes.
+ * The plan does not depend on (gamma, beta): it is reused across parameters. */
+tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int32_t* edges, int32_t p,
+                        const tn_build_opts* opts, void** buf, size_t* len);
+void tn_buffer_free(void* buf);
+
+/* Parse + validate a plan buffer (host).  Caller owns *out; free with tn_plan_free. */
+tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out);
+void tn_plan_free(tn_plan* plan);
+tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* out);
+
+/* The schedule as data (amplitude plans): host arrays sized by tn_plan_info:
+ * prefix[slice_step] labels, sliced[k] labels (ascending: bit b of slice id j is the value of
+ * sliced[b], reading A13), residual[n_labels - slice_step - k] labels, degrees[n_labels - k]
+ * (N_{G_i}(v_i) of the executed steps).  Any pointer may be NULL. */
+tn_status tn_plan_schedule(const tn_plan* plan, int32_t* prefix, int32_t* sliced, int32_t* residual,
+                           int32_t* degrees);
+
+/* ---------------------------------------------------------------- contraction (device) */
+/* Unsliced amplitude (sliced plans: all 2^k slices summed locally).  gamma, beta: host double[p].
+ * ws: device buffer of >= workspace_bytes[dtype] bytes (e.g. torch.empty).  stream: cudaStream_t
+ * (NULL = legacy default stream).  out: host double[2] = {Re sigma, Im sigma}, 2^{-N/2} applied in
+ * FP64 (reading A15).  Synchronous with respect to `stream` on return. */
+tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma, const double* beta,
+                      int32_t p, void* ws, size_t ws_bytes, void* stream, double out[2]);
+
+/* Slices [begin, end) of a sliced plan, Eq. (1): runs the shared prefix once,
+ * then every slice; writes the complex128 result of slice j into device double
+ * partials_dev[2j], partials_dev[2j+1] (2^{-N/2} applied) and leaves other entries untouched.
+ * Asynchronous on `stream`.  The caller zero-fills, all-reduces (torch.distributed / NCCL) and
+ * sums with tn_sum_partials. */
+tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, const double* gamma,
+                             const double* beta, int32_t p, uint64_t begin, uint64_t end, void* ws,
+                             size_t ws_bytes, void* stream, double* partials_dev);
+
+/* Fixed-order pairwise sum over j of partials_host[2j..2j+1], j < n_slices (host; bit-identical
+ * for any partition of the slices across GPUs). out: host double[2]. */
+tn_status tn_sum_partials(const tn_plan* plan, const double* partials_host, double out[2]);
+
+/* Energy plan: all E light-cone networks contracted in ONE batched launch.  zz: host double[E]
+ * (Re <Z_u Z_v> per edge in the graph's edge order), zz_imag_max: host double (max |Im|, ~0),
+ * energy: host double = sum_e (1 - zz[e]) / 2 (reading A3).  Synchronous on return. */
+tn_status tn_energy(const tn_plan* plan, tn_dtype dtype, const double* gamma, const double* beta,
+                    int32_t p, void* ws, size_t ws_bytes, void* stream, double* zz,
+                    double* zz_imag_max, double* energy);
+
+/* One bucket step -- "elimination of vertex (index) v" (§4.2) -- on caller
+ * tensors:  out[o] = sum_{x in {0,1}} prod_t in_t[ins(pext(o, out_mask[t]), pv[t], x)],
+ * where pext gathers the output bits selected by out_mask[t] (in order) and ins inserts the summed
+ * bit x at bit position pv[t] of input t.  Input t has popcount(out_mask[t]) + 1 bits.
+ * in_dev: host array of n_in device pointers; out_dev: device pointer of 2^out_rank elements.
+ * 1 <= n_in <= 8, 0 <= out_rank <= 40.  Asynchronous on `stream`. */
+tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* const* in_dev,
+                       const uint64_t* out_mask, const int32_t* pv, void* out_dev, int32_t out_rank,
+                       void* stream);
+
+/* Per-step device timing for the next calls on this plan (CUDA events on the launching stream).
+ * enable != 0 turns it on.  tn_profile_read returns, for standalone bucket-kernel launches since
+ * the last read: count, total milliseconds and total algorithmic bytes (host outputs). */
+tn_status tn_profile_enable(tn_plan* plan, int32_t enable);
+tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms, double* total_bytes,
+                          uint64_t* all_launches);
+
+const char* tn_last_error(void);
+int32_t tn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TN_B200_H */

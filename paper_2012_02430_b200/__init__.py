@@ -1,0 +1,132 @@
+"""B200-native sliced bucket-elimination contractor for QAOA MaxCut tensor networks
+(arXiv:2012.02430, "Tensor Network Quantum Simulator With Step-Dependent Parallelization").
+
+Layers:
+  include/tn_b200.h + csrc/     the C-ABI library libtnb200.so (planner, executor, sm_100a kernels)
+  _binding.py                   ctypes marshalling, C names
+  this module                   Plan (handle + workspace), plan selection (reading A11)
+  scheduler.py                  slice partition over torch.distributed ranks + one all-reduce
+
+PyTorch supplies device memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _binding as B
+from ._binding import (TN_C64, TN_C128, TN_KIND_AMPLITUDE, TN_KIND_ENERGY, TN_ORDER_MIN_DEGREE,
+                       TN_ORDER_MIN_FILL, TnError)
+
+__all__ = ["Plan", "TN_C64", "TN_C128", "TN_KIND_AMPLITUDE", "TN_KIND_ENERGY", "TN_ORDER_MIN_FILL",
+           "TN_ORDER_MIN_DEGREE", "TnError", "build_plan", "select_sliced_plan"]
+
+ORDERERS = {"min-fill": TN_ORDER_MIN_FILL, "min-degree": TN_ORDER_MIN_DEGREE}
+
+
+class Plan:
+    """A loaded plan (tn_plan_load) plus cached device workspaces (torch.empty)."""
+
+    def __init__(self, buf: bytes):
+        self.buf = buf
+        self.handle = B.tn_plan_load(buf)
+        self.info = B.tn_plan_info(self.handle)
+        self._ws: Dict[Tuple[int, str], object] = {}
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            B.tn_plan_free(h)
+            self.handle = None
+
+    # ------------------------------------------------------------ properties
+    @property
+    def n_slices(self) -> int:
+        return int(self.info["n_slices"])
+
+    @property
+    def width(self) -> int:
+        return int(self.info["width"])
+
+    def schedule(self):
+        """(prefix, sliced, residual, degrees) label lists (tn_plan_schedule)."""
+        return B.tn_plan_schedule(self.handle)
+
+    def workspace_bytes(self, dtype: int) -> int:
+        return int(self.info["workspace_bytes"][dtype])
+
+    def workspace(self, dtype: int, device=None):
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        key = (dtype, str(dev))
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = torch.empty(self.workspace_bytes(dtype), dtype=torch.uint8, device=dev)
+            self._ws[key] = ws
+        return ws
+
+    def release_workspaces(self):
+        self._ws.clear()
+
+    # ------------------------------------------------------------ calls
+    def _stream(self, stream):
+        import torch
+
+        s = torch.cuda.current_stream() if stream is None else stream
+        return s.cuda_stream
+
+    def contract(self, gammas, betas, dtype: int = TN_C64, stream=None) -> complex:
+        ws = self.workspace(dtype)
+        return B.tn_contract(self.handle, dtype, gammas, betas, ws.data_ptr(), ws.numel(), self._stream(stream))
+
+    def contract_sliced(self, gammas, betas, begin: int, end: int, partials, dtype: int = TN_C64,
+                        stream=None) -> None:
+        ws = self.workspace(dtype)
+        B.tn_contract_sliced(self.handle, dtype, gammas, betas, begin, end, ws.data_ptr(), ws.numel(),
+                             self._stream(stream), partials.data_ptr())
+
+    def sum_partials(self, partials_host) -> complex:
+        return B.tn_sum_partials(self.handle, partials_host)
+
+    def energy(self, gammas, betas, dtype: int = TN_C64, stream=None):
+        ws = self.workspace(dtype)
+        return B.tn_energy(self.handle, dtype, gammas, betas, ws.data_ptr(), ws.numel(), self._stream(stream))
+
+    def profile(self, enable: bool = True):
+        B.tn_profile_enable(self.handle, enable)
+
+    def profile_read(self):
+        return B.tn_profile_read(self.handle)
+
+
+def build_plan(graph, p: int, kind: str = "amplitude", orderer: str = "min-fill", n_sliced: int = 0,
+               r: int = 0, max_width: int = 0, small_log2: int = -1) -> Plan:
+    """Plan for a tn_inputs.Graph (or any object with .n and .edges)."""
+    k = TN_KIND_AMPLITUDE if kind == "amplitude" else TN_KIND_ENERGY
+    buf = B.tn_plan_build(graph.n, graph.edges, p, kind=k, orderer=ORDERERS[orderer], n_sliced=n_sliced,
+                          r=r, max_width=max_width, small_log2=small_log2)
+    plan = Plan(buf)
+    plan.orderer = orderer
+    return plan
+
+
+def select_sliced_plan(graph, p: int, max_width: int, k_min: int = 0, k_max: int = 12,
+                       orderers: Sequence[str] = ("min-fill", "min-degree"), r: int = 0,
+                       small_log2: int = -1) -> Tuple[Plan, List[dict]]:
+    """Reading A11: the smallest k in [k_min, k_max] whose width <= max_width; among the
+    orderers at that k, the plan with fewer predicted bytes (ties -> min-degree)."""
+    tried: List[dict] = []
+    for k in range(k_min, k_max + 1):
+        cands = []
+        for o in orderers:
+            pl = build_plan(graph, p, "amplitude", o, n_sliced=k, r=r, small_log2=small_log2)
+            total = pl.info["pred_bytes_per_slice"][0] * pl.n_slices + pl.info["pred_bytes_prefix"][0]
+            tried.append({"k": k, "orderer": o, "width": pl.width, "pred_bytes_c64": total,
+                          "unsliced_width": pl.info["unsliced_width"], "slice_step": pl.info["slice_step"]})
+            if pl.width <= max_width:
+                cands.append((total, 0 if o == "min-degree" else 1, pl))
+        if cands:
+            cands.sort(key=lambda c: (c[0], c[1]))
+            return cands[0][2], tried
+    raise TnError(-3, f"no plan with width <= {max_width} for k <= {k_max}")

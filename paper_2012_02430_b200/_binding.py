@@ -1,0 +1,198 @@
+"""Thin ctypes binding of libtnb200.so (include/tn_b200.h) -- argument marshalling only.
+
+The function names are the C names.  Every numeric step runs in the library's CUDA
+kernels; there is no Python or CPU fallback: importing this module without the built
+library raises ImportError (build it with `python -m paper_2012_02430_b200.build`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtnb200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2012_02430_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+TN_C64, TN_C128 = 0, 1
+TN_KIND_AMPLITUDE, TN_KIND_ENERGY = 0, 1
+TN_ORDER_MIN_FILL, TN_ORDER_MIN_DEGREE = 0, 1
+STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4: "TN_E_NOMEM",
+          -5: "TN_E_CUDA", -6: "TN_E_DTYPE"}
+
+SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_plan_load", "tn_plan_free", "tn_plan_info",
+           "tn_plan_schedule", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy",
+           "tn_eliminate", "tn_profile_enable", "tn_profile_read", "tn_last_error", "tn_version"]
+
+
+class TnError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{where}: {self.name}: {last_error()}")
+
+
+class tn_build_opts(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("orderer", C.c_int32), ("n_sliced", C.c_int32), ("r", C.c_int32),
+                ("max_width", C.c_int32), ("small_log2", C.c_int32), ("reserved", C.c_int32 * 4)]
+
+
+class tn_plan_info_t(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_qubits", C.c_int32), ("p", C.c_int32), ("n_edges", C.c_int32),
+                ("width", C.c_int32), ("unsliced_width", C.c_int32), ("k", C.c_int32),
+                ("slice_step", C.c_int32), ("n_programs", C.c_int32), ("n_labels", C.c_int32),
+                ("n_slices", C.c_uint64), ("prefix_steps", C.c_uint64), ("steps_per_slice", C.c_uint64),
+                ("launches_prefix", C.c_uint64), ("launches_per_slice", C.c_uint64),
+                ("workspace_bytes", C.c_size_t * 2), ("pred_bytes_per_slice", C.c_double * 2),
+                ("pred_bytes_prefix", C.c_double * 2), ("pred_bytes_big_per_slice", C.c_double * 2),
+                ("big_launches_per_slice", C.c_uint64)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if hasattr(v, "__len__") else v
+        return d
+
+
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_lib.tn_plan_build.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                               C.POINTER(tn_build_opts), C.POINTER(_P), C.POINTER(C.c_size_t)]
+_lib.tn_buffer_free.argtypes = [_P]
+_lib.tn_buffer_free.restype = None
+_lib.tn_plan_load.argtypes = [_P, C.c_size_t, C.POINTER(_P)]
+_lib.tn_plan_free.argtypes = [_P]
+_lib.tn_plan_free.restype = None
+_lib.tn_plan_info.argtypes = [_P, C.POINTER(tn_plan_info_t)]
+_I32P = C.POINTER(C.c_int32)
+_lib.tn_plan_schedule.argtypes = [_P, _I32P, _I32P, _I32P, _I32P]
+_lib.tn_contract.argtypes = [_P, C.c_int, _D, _D, C.c_int32, _P, C.c_size_t, _P, _D]
+_lib.tn_contract_sliced.argtypes = [_P, C.c_int, _D, _D, C.c_int32, C.c_uint64, C.c_uint64, _P,
+                                    C.c_size_t, _P, _P]
+_lib.tn_sum_partials.argtypes = [_P, _D, _D]
+_lib.tn_energy.argtypes = [_P, C.c_int, _D, _D, C.c_int32, _P, C.c_size_t, _P, _D, _D, _D]
+_lib.tn_eliminate.argtypes = [C.c_int, C.c_int32, C.POINTER(_P), C.POINTER(C.c_uint64), _I32P, _P,
+                              C.c_int32, _P]
+_lib.tn_profile_enable.argtypes = [_P, C.c_int32]
+_lib.tn_profile_read.argtypes = [_P, C.POINTER(C.c_uint64), _D, _D, C.POINTER(C.c_uint64)]
+_lib.tn_last_error.restype = C.c_char_p
+_lib.tn_version.restype = C.c_int32
+for _n in SYMBOLS:
+    if _n not in ("tn_buffer_free", "tn_plan_free", "tn_last_error", "tn_version"):
+        getattr(_lib, _n).restype = C.c_int
+
+
+def last_error() -> str:
+    return (_lib.tn_last_error() or b"").decode()
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise TnError(st, where)
+
+
+def _dbl(xs):
+    return (C.c_double * len(xs))(*[float(x) for x in xs])
+
+
+# ---------------------------------------------------------------- 1:1 wrappers
+def tn_version() -> int:
+    return int(_lib.tn_version())
+
+
+def tn_plan_build(n_qubits: int, edges, p: int, kind: int = TN_KIND_AMPLITUDE,
+                  orderer: int = TN_ORDER_MIN_FILL, n_sliced: int = 0, r: int = 0,
+                  max_width: int = 0, small_log2: int = -1) -> bytes:
+    flat = []
+    for e in edges:
+        flat.extend((int(e[0]), int(e[1])))
+    arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    opts = tn_build_opts(kind, orderer, n_sliced, r, max_width, small_log2)
+    buf, ln = _P(), C.c_size_t()
+    _check(_lib.tn_plan_build(n_qubits, len(flat) // 2, arr, p, C.byref(opts), C.byref(buf), C.byref(ln)),
+           "tn_plan_build")
+    try:
+        return C.string_at(buf, ln.value)
+    finally:
+        _lib.tn_buffer_free(buf)
+
+
+def tn_plan_load(buf: bytes) -> int:
+    h = _P()
+    _check(_lib.tn_plan_load(buf, len(buf), C.byref(h)), "tn_plan_load")
+    return h.value
+
+
+def tn_plan_free(h: int) -> None:
+    _lib.tn_plan_free(h)
+
+
+def tn_plan_info(h: int) -> dict:
+    info = tn_plan_info_t()
+    _check(_lib.tn_plan_info(h, C.byref(info)), "tn_plan_info")
+    return info.as_dict()
+
+
+def tn_plan_schedule(h: int):
+    info = tn_plan_info(h)
+    s, k, L = info["slice_step"], info["k"], info["n_labels"]
+    pre = (C.c_int32 * max(1, s))()
+    sl = (C.c_int32 * max(1, k))()
+    res = (C.c_int32 * max(1, L - s - k))()
+    nd = info["prefix_steps"] + info["steps_per_slice"]
+    deg = (C.c_int32 * max(1, nd))()
+    _check(_lib.tn_plan_schedule(h, pre, sl, res, deg), "tn_plan_schedule")
+    return list(pre)[:s], list(sl)[:k], list(res)[:L - s - k], list(deg)[:nd]
+
+
+def tn_contract(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, stream: int) -> complex:
+    out = (C.c_double * 2)()
+    _check(_lib.tn_contract(h, dtype, _dbl(gammas), _dbl(betas), len(gammas), ws_ptr, ws_bytes,
+                            stream, out), "tn_contract")
+    return complex(out[0], out[1])
+
+
+def tn_contract_sliced(h: int, dtype: int, gammas, betas, begin: int, end: int, ws_ptr: int,
+                       ws_bytes: int, stream: int, partials_ptr: int) -> None:
+    _check(_lib.tn_contract_sliced(h, dtype, _dbl(gammas), _dbl(betas), len(gammas), begin, end,
+                                   ws_ptr, ws_bytes, stream, partials_ptr), "tn_contract_sliced")
+
+
+def tn_sum_partials(h: int, partials) -> complex:
+    """partials: flat float64 sequence [re0, im0, re1, im1, ...] (host)."""
+    arr = _dbl(list(partials))
+    out = (C.c_double * 2)()
+    _check(_lib.tn_sum_partials(h, arr, out), "tn_sum_partials")
+    return complex(out[0], out[1])
+
+
+def tn_energy(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, stream: int):
+    E = tn_plan_info(h)["n_programs"]
+    zz = (C.c_double * E)()
+    im, en = C.c_double(), C.c_double()
+    _check(_lib.tn_energy(h, dtype, _dbl(gammas), _dbl(betas), len(gammas), ws_ptr, ws_bytes, stream,
+                          zz, C.byref(im), C.byref(en)), "tn_energy")
+    return list(zz), im.value, en.value
+
+
+def tn_eliminate(dtype: int, in_ptrs, out_masks, pvs, out_ptr: int, out_rank: int, stream: int) -> None:
+    n = len(in_ptrs)
+    ins = (_P * n)(*in_ptrs)
+    masks = (C.c_uint64 * n)(*out_masks)
+    pv = (C.c_int32 * n)(*pvs)
+    _check(_lib.tn_eliminate(dtype, n, ins, masks, pv, out_ptr, out_rank, stream), "tn_eliminate")
+
+
+def tn_profile_enable(h: int, enable: bool) -> None:
+    _check(_lib.tn_profile_enable(h, 1 if enable else 0), "tn_profile_enable")
+
+
+def tn_profile_read(h: int):
+    n, alln = C.c_uint64(), C.c_uint64()
+    ms, by = C.c_double(), C.c_double()
+    _check(_lib.tn_profile_read(h, C.byref(n), C.byref(ms), C.byref(by), C.byref(alln)), "tn_profile_read")
+    return {"launches": n.value, "ms": ms.value, "bytes": by.value, "all_launches": alln.value}

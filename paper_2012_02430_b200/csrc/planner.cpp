@@ -1,0 +1,705 @@
+// planner.cpp -- host planner: QAOA network builder, bitset line graph, greedy min-fill /
+// min-degree orderers, step-dependent slicing and lowering to a bucket program.
+//
+//   PAPER.md:199-235, 350-359  circuit -> tensor expression -> line graph (indices = vertices,
+//                              tensors = cliques, diagonal gates share one index per wire)
+//   PAPER.md:361-368           elimination of vertex i (neighbourhood becomes a clique)
+//   PAPER.md:384-401           contraction width c = max_i N_{G_i}(v_i)
+//   PAPER.md:459-463           greedy ordering (lowest degree first)
+//   PAPER.md:509-527, Eq. (1)  slicing n indices -> 2^n independent networks
+//   PAPER.md:545-567           step-dependent slicing (Fig. slice_algo)
+#include "planner.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+
+#include "../../include/tn_b200.h"
+
+namespace tnb {
+
+// ============================================================== network builders
+namespace {
+
+struct NetBuilder {
+  Network net;
+  std::map<std::vector<int>, int> index;
+  int n_plus = 0;
+  void add(std::vector<int> labels, Factor f) {
+    std::sort(labels.begin(), labels.end());
+    if (std::adjacent_find(labels.begin(), labels.end()) != labels.end())
+      throw std::runtime_error("tensor with repeated index");
+    if (f.code == LC_PLUS) n_plus++;
+    auto it = index.find(labels);
+    if (it == index.end()) {
+      index.emplace(labels, (int)net.tensors.size());
+      net.tensors.push_back(NetTensor{labels, {f}});
+    } else {
+      auto& t = net.tensors[it->second];
+      if ((int)t.factors.size() >= kMaxFactors) throw std::runtime_error("too many merged factors");
+      t.factors.push_back(f);
+    }
+  }
+};
+
+void check_edges(int n, const std::vector<int>& edges) {
+  std::vector<std::pair<int, int>> seen;
+  for (size_t e = 0; e + 1 < edges.size(); e += 2) {
+    int a = edges[e], b = edges[e + 1];
+    if (a < 0 || b < 0 || a >= n || b >= n || a == b) throw std::invalid_argument("bad edge");
+    seen.emplace_back(std::min(a, b), std::max(a, b));
+  }
+  std::sort(seen.begin(), seen.end());
+  if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
+    throw std::invalid_argument("duplicate edge");
+}
+
+}  // namespace
+
+Network build_amplitude_network(int n, const std::vector<int>& edges, int p) {
+  check_edges(n, edges);
+  NetBuilder b;
+  auto w = [n](int q, int l) { return l * n + q; };
+  for (int q = 0; q < n; ++q) b.add({w(q, 0)}, {LC_PLUS, 0, 0});
+  for (int l = 1; l <= p; ++l) {
+    for (size_t e = 0; e + 1 < edges.size(); e += 2)
+      b.add({w(edges[e], l - 1), w(edges[e + 1], l - 1)}, {LC_ZZ, (uint8_t)(l - 1), 0});
+    for (int q = 0; q < n; ++q) {
+      if (l < p)
+        b.add({w(q, l - 1), w(q, l)}, {LC_RX, (uint8_t)(l - 1), 0});
+      else  // output wire fixed to 0: <0| e^{-i b X} is a vector on w(q, p-1)
+        b.add({w(q, p - 1)}, {LC_RXROW0, (uint8_t)(l - 1), 0});
+    }
+  }
+  b.net.n_labels = n * p;
+  b.net.log2_scale = -0.5 * b.n_plus;
+  return b.net;
+}
+
+Network build_cone_network(int n, const std::vector<int>& edges, int p, int u, int v) {
+  check_edges(n, edges);
+  // reverse light cone (reading A17): L_p = {u, v}; E_l = edges touching L_l;
+  // L_{l-1} = L_l U endpoints(E_l); m_q = max{l : q in L_l}
+  std::vector<std::vector<char>> L(p + 1, std::vector<char>(n, 0));
+  std::vector<std::vector<int>> E(p + 1);
+  L[p][u] = L[p][v] = 1;
+  for (int l = p; l >= 1; --l) {
+    L[l - 1] = L[l];
+    for (size_t e = 0; e + 1 < edges.size(); e += 2) {
+      int a = edges[e], c = edges[e + 1];
+      if (L[l][a] || L[l][c]) {
+        E[l].push_back((int)e);
+        L[l - 1][a] = L[l - 1][c] = 1;
+      }
+    }
+  }
+  std::vector<int> m(n, -1);
+  for (int q = 0; q < n; ++q)
+    for (int l = 0; l <= p; ++l)
+      if (L[l][q]) m[q] = l;
+  // labels: per cone qubit ascending: ket levels 0..m-1, shared top t, bra levels 0..m-1
+  std::vector<std::vector<int>> kl(n), bl(n);
+  int next = 0;
+  for (int q = 0; q < n; ++q) {
+    if (m[q] < 0) continue;
+    kl[q].resize(m[q] + 1);
+    bl[q].resize(m[q] + 1);
+    for (int a = 0; a < m[q]; ++a) kl[q][a] = next++;
+    int t = next++;
+    kl[q][m[q]] = bl[q][m[q]] = t;
+    for (int a = 0; a < m[q]; ++a) bl[q][a] = next++;
+  }
+  NetBuilder b;
+  for (int q = 0; q < n; ++q) {
+    if (m[q] < 0) continue;
+    b.add({kl[q][0]}, {LC_PLUS, 0, 0});
+    b.add({bl[q][0]}, {LC_PLUS, 0, 1});
+  }
+  for (int l = 1; l <= p; ++l) {
+    for (int e : E[l]) {
+      int a = edges[e], c = edges[e + 1];
+      b.add({kl[a][l - 1], kl[c][l - 1]}, {LC_ZZ, (uint8_t)(l - 1), 0});
+      b.add({bl[a][l - 1], bl[c][l - 1]}, {LC_ZZ, (uint8_t)(l - 1), 1});
+    }
+    for (int q = 0; q < n; ++q) {
+      if (m[q] >= l) {
+        b.add({kl[q][l - 1], kl[q][l]}, {LC_RX, (uint8_t)(l - 1), 0});
+        b.add({bl[q][l - 1], bl[q][l]}, {LC_RX, (uint8_t)(l - 1), 1});
+      }
+    }
+  }
+  b.add({kl[u][m[u]]}, {LC_ZOBS, 0, 0});
+  b.add({kl[v][m[v]]}, {LC_ZOBS, 0, 0});
+  b.net.n_labels = next;
+  b.net.log2_scale = -0.5 * b.n_plus;
+  b.net.edge_u = u;
+  b.net.edge_v = v;
+  return b.net;
+}
+
+// ============================================================== bitset line graph
+static inline int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+BitGraph::BitGraph(int n) : n_(n), W_((n + 63) / 64), n_alive_(n) {
+  adj_.assign((size_t)n * W_, 0);
+  alive_.assign(n, 1);
+  deg_.assign(n, 0);
+}
+
+BitGraph BitGraph::from_network(const Network& net) {
+  BitGraph g(net.n_labels);
+  for (const auto& t : net.tensors)
+    for (size_t i = 0; i < t.labels.size(); ++i)
+      for (size_t j = i + 1; j < t.labels.size(); ++j) g.add_edge(t.labels[i], t.labels[j]);
+  return g;
+}
+
+void BitGraph::add_edge(int a, int b) {
+  if (a == b || adjacent(a, b)) return;
+  rowm(a)[b >> 6] |= 1ull << (b & 63);
+  rowm(b)[a >> 6] |= 1ull << (a & 63);
+  deg_[a]++;
+  deg_[b]++;
+}
+
+std::vector<int> BitGraph::neighbours(int v) const {
+  std::vector<int> out;
+  const uint64_t* r = row(v);
+  for (int w = 0; w < W_; ++w) {
+    uint64_t x = r[w];
+    while (x) {
+      int b = __builtin_ctzll(x);
+      out.push_back(w * 64 + b);
+      x &= x - 1;
+    }
+  }
+  return out;
+}
+
+void BitGraph::eliminate(int v) {
+  std::vector<int> nb = neighbours(v);
+  const uint64_t* rv = row(v);
+  for (int a : nb) {
+    uint64_t* ra = rowm(a);
+    ra[v >> 6] &= ~(1ull << (v & 63));
+    int d = 0;
+    for (int w = 0; w < W_; ++w) {
+      ra[w] |= rv[w];
+      if (w == (a >> 6)) ra[w] &= ~(1ull << (a & 63));
+      if (w == (v >> 6)) ra[w] &= ~(1ull << (v & 63));
+      d += popc(ra[w]);
+    }
+    deg_[a] = d;
+  }
+  std::fill(rowm(v), rowm(v) + W_, 0ull);
+  deg_[v] = 0;
+  alive_[v] = 0;
+  n_alive_--;
+}
+
+void BitGraph::remove(int v) {
+  for (int a : neighbours(v)) {
+    rowm(a)[v >> 6] &= ~(1ull << (v & 63));
+    deg_[a]--;
+  }
+  std::fill(rowm(v), rowm(v) + W_, 0ull);
+  deg_[v] = 0;
+  alive_[v] = 0;
+  n_alive_--;
+}
+
+int64_t BitGraph::fill_in(int v) const {
+  const uint64_t* rv = row(v);
+  int64_t missing = 0;
+  for (int a : neighbours(v)) {
+    const uint64_t* ra = row(a);
+    int c = 0;
+    for (int w = 0; w < W_; ++w) c += popc(rv[w] & ~ra[w]);
+    missing += c - 1;  // a itself is in N(v) but not in N(a)
+  }
+  return missing / 2;
+}
+
+// ============================================================== greedy orderers
+Ordering greedy_order(BitGraph g, int orderer) {
+  const int n = g.size();
+  Ordering o;
+  std::vector<int64_t> fill(n, 0);
+  const bool minfill = orderer == TN_ORDER_MIN_FILL;
+  if (minfill)
+    for (int v = 0; v < n; ++v)
+      if (g.alive(v)) fill[v] = g.fill_in(v);
+  std::vector<char> dirty(n, 0);
+  while (g.n_alive() > 0) {
+    int best = -1;
+    for (int v = 0; v < n; ++v) {
+      if (!g.alive(v)) continue;
+      if (best < 0) { best = v; continue; }
+      if (minfill) {
+        if (fill[v] < fill[best] || (fill[v] == fill[best] && g.degree(v) < g.degree(best))) best = v;
+      } else if (g.degree(v) < g.degree(best)) {
+        best = v;
+      }
+    }
+    const int d = g.degree(best);
+    o.order.push_back(best);
+    o.degrees.push_back(d);
+    o.width = std::max(o.width, d);
+    o.cost += std::ldexp(1.0, d);
+    if (!minfill) {
+      g.eliminate(best);
+      continue;
+    }
+    std::vector<int> nb = g.neighbours(best);
+    g.eliminate(best);
+    // fill values change only within distance 2 of the eliminated vertex
+    std::vector<int> touched;
+    for (int a : nb) {
+      if (!dirty[a]) { dirty[a] = 1; touched.push_back(a); }
+      for (int c : g.neighbours(a))
+        if (!dirty[c]) { dirty[c] = 1; touched.push_back(c); }
+    }
+    for (int a : touched) {
+      fill[a] = g.fill_in(a);
+      dirty[a] = 0;
+    }
+  }
+  return o;
+}
+
+// ============================================================== step-dependent slicing
+Schedule slice_search(const BitGraph& g0, int n, int r, int orderer) {
+  Schedule sch;
+  Ordering full0 = greedy_order(g0, orderer);
+  sch.unsliced_width = full0.width;
+  if (n <= 0) {
+    sch.residual = full0.order;
+    sch.width = full0.width;
+    sch.cost = full0.cost;
+    return sch;
+  }
+  if (r <= 0 || r > n) r = n;
+  if (n > g0.n_alive()) throw std::invalid_argument("n exceeds the live vertex count");
+  BitGraph g = g0;
+  int prefix_width = 0;
+  double prefix_cost = 0.0;
+  int n_done = 0;
+  bool first_round = true;
+  std::vector<int> phaseB_prefix;
+  while (n_done < n) {
+    const int rr = std::min(r, n - n_done);
+    Ordering full = first_round ? full0 : greedy_order(g, orderer);
+    int peak = 0;
+    for (size_t i = 0; i < full.degrees.size(); ++i)
+      if (full.degrees[i] > full.degrees[peak]) peak = (int)i;
+    // candidate steps s in [0, peak] (reading A8)
+    BitGraph gs = g;
+    int pmax = prefix_width;
+    double pcost = 0.0;
+    int best_s = -1, best_w = 1 << 30;
+    double best_cost = 0.0;
+    std::vector<int> best_S;
+    BitGraph best_g;
+    for (int s = 0; s <= peak && s <= (int)full.order.size(); ++s) {
+      if (s > 0) {
+        pmax = std::max(pmax, full.degrees[s - 1]);
+        pcost += std::ldexp(1.0, full.degrees[s - 1]) * std::ldexp(1.0, n_done);
+        gs.eliminate(full.order[s - 1]);
+      }
+      if (gs.n_alive() < rr) break;
+      // the rr vertices with the most neighbours in G_s, ties -> smaller label (reading A9)
+      std::vector<int> cand;
+      for (int v = 0; v < gs.size(); ++v)
+        if (gs.alive(v)) cand.push_back(v);
+      std::stable_sort(cand.begin(), cand.end(),
+                       [&](int a, int b) { return gs.degree(a) > gs.degree(b); });
+      std::vector<int> S(cand.begin(), cand.begin() + rr);
+      BitGraph gr = gs;
+      for (int v : S) gr.remove(v);
+      Ordering res = greedy_order(gr, orderer);
+      const int w = std::max(pmax, res.width);
+      const double cost = prefix_cost + pcost + std::ldexp(res.cost, n_done + rr);
+      // best: smaller width, then fewer predicted operations, then smaller s (reading A10)
+      if (w < best_w || (w == best_w && cost < best_cost)) {
+        best_w = w;
+        best_cost = cost;
+        best_s = s;
+        best_S = S;
+        best_g = gr;
+      }
+    }
+    if (best_s < 0) throw std::invalid_argument("n exceeds the live vertex count");
+    std::vector<int> pre(full.order.begin(), full.order.begin() + best_s);
+    for (int i = 0; i < best_s; ++i) {
+      prefix_width = std::max(prefix_width, full.degrees[i]);
+      prefix_cost += std::ldexp(1.0, full.degrees[i]) * std::ldexp(1.0, n_done);
+    }
+    if (first_round)
+      sch.prefix = pre;
+    else
+      phaseB_prefix.insert(phaseB_prefix.end(), pre.begin(), pre.end());
+    sch.sliced.insert(sch.sliced.end(), best_S.begin(), best_S.end());
+    g = best_g;
+    n_done += rr;
+    first_round = false;
+  }
+  Ordering res = greedy_order(g, orderer);
+  sch.residual = phaseB_prefix;
+  sch.residual.insert(sch.residual.end(), res.order.begin(), res.order.end());
+  std::sort(sch.sliced.begin(), sch.sliced.end());
+  sch.width = std::max(prefix_width, res.width);
+  sch.cost = prefix_cost + std::ldexp(res.cost, n);
+  return sch;
+}
+
+// ============================================================== lowering
+namespace {
+
+struct Sym {
+  std::vector<int> idx;   // layout order: ascending key = most significant first
+  int leaf = -1;
+  int birth = 0;          // time of production (0 = materialization)
+  int death = -1;         // last use
+  bool persistent = false;
+  bool scalar_ref = false;
+  uint64_t off = 0;
+  uint64_t size = 0;      // allocated elements (aligned)
+  bool phaseB_born = false;
+};
+
+uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Arena {
+  std::map<uint64_t, uint64_t> holes;  // off -> size
+  uint64_t top = 0;
+  uint64_t alloc(uint64_t need) {
+    for (auto it = holes.begin(); it != holes.end(); ++it) {
+      if (it->second >= need) {
+        uint64_t off = it->first, sz = it->second;
+        holes.erase(it);
+        if (sz > need) holes[off + need] = sz - need;
+        return off;
+      }
+    }
+    // extend at the top, absorbing a trailing hole
+    if (!holes.empty()) {
+      auto last = std::prev(holes.end());
+      if (last->first + last->second == top) {
+        uint64_t off = last->first;
+        holes.erase(last);
+        top = off + need;
+        return off;
+      }
+    }
+    uint64_t off = top;
+    top += need;
+    return off;
+  }
+  void release(uint64_t off, uint64_t sz) {
+    if (sz == 0) return;
+    auto it = holes.emplace(off, sz).first;
+    auto nx = std::next(it);
+    if (nx != holes.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      holes.erase(nx);
+    }
+    if (it != holes.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        holes.erase(it);
+      }
+    }
+  }
+};
+
+}  // namespace
+
+LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, std::string* err) {
+  LoweredProgram out;
+  const int NL = net.n_labels;
+  const int k = (int)sch.sliced.size();
+  std::vector<int64_t> key(NL, INT64_MIN);
+  std::vector<int> slice_bit(NL, -1);
+  for (int b = 0; b < k; ++b) {
+    key[sch.sliced[b]] = -1 - b;
+    slice_bit[sch.sliced[b]] = b;
+  }
+  const int sA = (int)sch.prefix.size();
+  for (int i = 0; i < sA; ++i) key[sch.prefix[i]] = i;
+  for (size_t i = 0; i < sch.residual.size(); ++i) key[sch.residual[i]] = sA + (int64_t)i;
+  for (int l = 0; l < NL; ++l)
+    if (key[l] == INT64_MIN) {
+      *err = "order misses live label " + std::to_string(l);
+      return out;
+    }
+  const int total_pos = sA + (int)sch.residual.size();
+  auto by_key = [&](int a, int b) { return key[a] < key[b]; };
+
+  std::vector<Sym> syms;
+  for (size_t t = 0; t < net.tensors.size(); ++t) {
+    Sym s;
+    s.idx = net.tensors[t].labels;
+    std::sort(s.idx.begin(), s.idx.end(), by_key);
+    s.leaf = (int)t;
+    syms.push_back(s);
+  }
+  auto home = [&](const Sym& s) -> int64_t {  // min key over non-sliced indices, -1 if none
+    for (int l : s.idx)
+      if (slice_bit[l] < 0) return key[l];
+    return -1;
+  };
+  std::vector<std::vector<int>> bucket(total_pos);
+  std::vector<int> scalars;
+  auto route = [&](int id) {
+    int64_t h = home(syms[id]);
+    if (h < 0) {
+      syms[id].scalar_ref = true;
+      scalars.push_back(id);
+    } else {
+      bucket[h].push_back(id);
+    }
+  };
+  for (size_t i = 0; i < syms.size(); ++i) route((int)i);
+
+  struct PendingStep {
+    StepRec rec;
+    std::vector<int> ins;
+    int outsym;
+  };
+  std::vector<PendingStep> pend;
+  for (int pos = 0; pos < total_pos; ++pos) {
+    const int v = pos < sA ? sch.prefix[pos] : sch.residual[pos - sA];
+    const bool phaseB = pos >= sA;
+    std::vector<int> ins = bucket[pos];
+    if (ins.empty()) continue;  // an index of no tensor (cannot happen for connected networks)
+    if ((int)ins.size() > kMaxIn) {
+      *err = "bucket with more than 8 tensors at label " + std::to_string(v);
+      return out;
+    }
+    const int t_now = (int)pend.size() + 1;
+    Sym o;
+    for (int id : ins)
+      for (int l : syms[id].idx)
+        if (l != v && !(phaseB && slice_bit[l] >= 0)) o.idx.push_back(l);  // phase B: sliced fixed
+    std::sort(o.idx.begin(), o.idx.end(), by_key);
+    o.idx.erase(std::unique(o.idx.begin(), o.idx.end()), o.idx.end());
+    o.birth = t_now;
+    o.phaseB_born = phaseB;
+    // bits of the output in this phase (phase B: sliced indices are fixed, not bits)
+    std::vector<int> obits;
+    for (int l : o.idx)
+      if (!(phaseB && slice_bit[l] >= 0)) obits.push_back(l);
+    if (phaseB && obits.size() != o.idx.size()) {
+      *err = "internal: phase-B output holds a sliced index";
+      return out;
+    }
+    const int R = (int)obits.size();
+    if (R > 62) {
+      *err = "output rank above 62";
+      return out;
+    }
+    StepRec rec;
+    std::memset(&rec, 0, sizeof(rec));
+    rec.out_rank = R;
+    rec.n_in = (int)ins.size();
+    rec.phase = phaseB ? 1 : 0;
+    rec.label = v;
+    rec.degree = R;
+    // largest input first (in-place candidate)
+    std::stable_sort(ins.begin(), ins.end(),
+                     [&](int a, int b) { return syms[a].idx.size() > syms[b].idx.size(); });
+    for (size_t t = 0; t < ins.size(); ++t) {
+      const Sym& s = syms[ins[t]];
+      std::vector<int> bits;
+      uint32_t smask = 0;
+      for (int l : s.idx) {
+        if (phaseB && slice_bit[l] >= 0)
+          smask |= 1u << slice_bit[l];
+        else
+          bits.push_back(l);
+      }
+      InRec& in = rec.in[t];
+      in.rank = (uint32_t)bits.size();
+      in.slice_mask = smask;
+      uint64_t mask = 0;
+      int pv = -1;
+      for (size_t i = 0; i < bits.size(); ++i) {
+        const int pos_in = (int)bits.size() - 1 - (int)i;
+        if (bits[i] == v) {
+          pv = pos_in;
+          continue;
+        }
+        auto it = std::find(obits.begin(), obits.end(), bits[i]);
+        const int pos_out = R - 1 - (int)(it - obits.begin());
+        mask |= 1ull << pos_out;
+      }
+      in.out_mask = mask;
+      in.pv = (uint32_t)pv;
+      // monotone check: the non-v bits of the input must be the selected output bits in order
+      if (pv < 0 || popc(mask) + 1 != (int)bits.size()) {
+        *err = "internal: bad embedding";
+        return out;
+      }
+      in.flags = (in.rank + 2 >= (uint32_t)R && R >= 16) ? 1u : 0u;
+    }
+    // in-place: in[0] is an intermediate of this phase holding every output bit with v on top
+    {
+      const Sym& s0 = syms[ins[0]];
+      const InRec& i0 = rec.in[0];
+      const uint64_t full = R == 64 ? ~0ull : ((1ull << R) - 1);
+      const bool same_phase_interm = s0.leaf < 0 && s0.phaseB_born == phaseB;
+      rec.inplace = (same_phase_interm && i0.slice_mask == 0 && i0.rank == (uint32_t)R + 1 &&
+                     i0.out_mask == full && i0.pv == (uint32_t)R && s0.idx.size() == (size_t)R + 1)
+                        ? 1
+                        : 0;
+    }
+    for (int id : ins) syms[id].death = t_now;
+    const int oid = (int)syms.size();
+    syms.push_back(o);
+    pend.push_back(PendingStep{rec, ins, oid});
+    route(oid);
+  }
+  for (size_t i = 0; i < syms.size(); ++i) {
+    if (syms[i].death < 0 && !syms[i].scalar_ref) {
+      *err = "internal: dangling tensor";
+      return out;
+    }
+  }
+  const int nsteps = (int)pend.size();
+  const int T_end = nsteps + 1;
+  int nA = 0;
+  for (auto& ps : pend)
+    if (ps.rec.phase == 0) nA++;
+  // lifetimes: tensors used in phase B but born before it persist across slices
+  for (auto& s : syms) {
+    if (s.scalar_ref) s.death = T_end;
+    const bool usedB = s.death > nA;
+    if (usedB && !s.phaseB_born) {
+      s.persistent = true;
+      s.death = T_end + 1;
+    }
+    s.size = align_up(1ull << s.idx.size());
+  }
+  // ---- arena: interval allocation in time order; leaves at t = 0
+  Arena ar;
+  for (auto& s : syms)
+    if (s.leaf >= 0) s.off = ar.alloc(s.size);
+  // free dead leaves / tensors at step t after allocating the step's output
+  std::vector<std::vector<int>> dies(T_end + 2);
+  for (size_t i = 0; i < syms.size(); ++i)
+    if (syms[i].death <= T_end) dies[syms[i].death].push_back((int)i);
+  for (int si = 0; si < nsteps; ++si) {
+    const int t = si + 1;
+    PendingStep& ps = pend[si];
+    Sym& o = syms[ps.outsym];
+    if (ps.rec.inplace) {
+      Sym& a = syms[ps.ins[0]];
+      o.off = a.off;
+      ar.release(a.off + o.size, a.size - o.size);
+      a.size = 0;  // its lower part now belongs to the output
+    } else {
+      o.off = ar.alloc(o.size);
+    }
+    for (int id : dies[t]) {
+      if (syms[id].persistent) continue;
+      ar.release(syms[id].off, syms[id].size);
+      syms[id].size = 0;
+    }
+  }
+  out.arena_elems = ar.top;
+  uint64_t pers = 0;
+  for (auto& s : syms)
+    if (s.persistent) pers = std::max(pers, s.off + align_up(1ull << s.idx.size()));
+  out.persistent_elems = pers;
+
+  // ---- records
+  for (size_t t = 0; t < net.tensors.size(); ++t) {
+    LeafRec lr;
+    std::memset(&lr, 0, sizeof(lr));
+    lr.off = syms[t].off;
+    lr.rank = (int32_t)net.tensors[t].labels.size();
+    lr.nfact = (int32_t)net.tensors[t].factors.size();
+    for (int f = 0; f < lr.nfact; ++f) {
+      lr.code[f] = net.tensors[t].factors[f].code;
+      lr.layer[f] = net.tensors[t].factors[f].layer;
+      lr.conj[f] = net.tensors[t].factors[f].conj;
+    }
+    out.leaves.push_back(lr);
+  }
+  for (int si = 0; si < nsteps; ++si) {
+    PendingStep& ps = pend[si];
+    ps.rec.out_off = syms[ps.outsym].off;
+    for (int t = 0; t < ps.rec.n_in; ++t) ps.rec.in[t].off = syms[ps.ins[t]].off;
+    const Sym& o = syms[ps.outsym];
+    ps.rec.degree = (int)o.idx.size();
+    out.degrees.push_back(ps.rec.degree);
+    out.width = std::max(out.width, ps.rec.degree);
+    out.steps.push_back(ps.rec);
+  }
+  for (int id : scalars) {
+    ScalarRec sr;
+    std::memset(&sr, 0, sizeof(sr));
+    sr.off = syms[id].off;
+    uint32_t m = 0;
+    for (int l : syms[id].idx) m |= 1u << slice_bit[l];
+    sr.slice_mask = m;
+    out.scalars.push_back(sr);
+  }
+  // ---- ops: runs of small steps go to the interpreter, the rest are standalone launches
+  for (int phase = 0; phase < 2; ++phase) {
+    int i = 0;
+    while (i < nsteps) {
+      if (out.steps[i].phase != phase) { ++i; continue; }
+      const StepRec& st = out.steps[i];
+      double elems = std::ldexp(1.0, st.out_rank);
+      for (int t = 0; t < st.n_in; ++t) elems += std::ldexp(1.0, (int)st.in[t].rank);
+      if (phase == 0) out.elems_prefix += elems; else out.elems_slice += elems;
+      if (st.out_rank > small_log2 && st.out_rank >= 1) {
+        out.ops.push_back(OpRec{OP_BIG, i, i + 1, phase});
+        if (phase == 1) { out.elems_big_slice += elems; out.big_launches_slice++; }
+        ++i;
+        continue;
+      }
+      int j = i;
+      while (j < nsteps && out.steps[j].phase == phase && out.steps[j].out_rank <= small_log2) {
+        if (j > i) {
+          const StepRec& s2 = out.steps[j];
+          double e2 = std::ldexp(1.0, s2.out_rank);
+          for (int t = 0; t < s2.n_in; ++t) e2 += std::ldexp(1.0, (int)s2.in[t].rank);
+          if (phase == 0) out.elems_prefix += e2; else out.elems_slice += e2;
+        }
+        ++j;
+      }
+      out.ops.push_back(OpRec{OP_RUN, i, j, phase});
+      i = j;
+    }
+  }
+  for (auto& op : out.ops) (op.phase == 0 ? out.launches_prefix : out.launches_slice)++;
+  out.launches_slice += 1;  // per-slice finalize
+  ProgramRec& pr = out.prog;
+  std::memset(&pr, 0, sizeof(pr));
+  pr.stepA_begin = 0;
+  pr.stepA_end = nA;
+  pr.stepB_begin = nA;
+  pr.stepB_end = nsteps;
+  int oa = 0;
+  while (oa < (int)out.ops.size() && out.ops[oa].phase == 0) ++oa;
+  pr.opA_begin = 0;
+  pr.opA_end = oa;
+  pr.opB_begin = oa;
+  pr.opB_end = (int)out.ops.size();
+  pr.scal_begin = 0;
+  pr.scal_end = (int)out.scalars.size();
+  pr.edge_u = net.edge_u;
+  pr.edge_v = net.edge_v;
+  pr.log2_scale = net.log2_scale;
+  pr.arena_begin = 0;
+  pr.arena_end = out.arena_elems;
+  (void)T_end;
+  return out;
+}
+
+}  // namespace tnb

@@ -1,0 +1,100 @@
+// planner.h -- host-side planner internals (network builder, line graph, orderers,
+// step-dependent slicing, lowering).  Product code; the oracle shares none of it.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "plan_format.h"
+
+namespace tnb {
+
+struct Factor {
+  uint8_t code, layer, conj;
+};
+
+struct NetTensor {
+  std::vector<int> labels;       // sorted ascending, distinct
+  std::vector<Factor> factors;   // elementwise product of gate tensors on `labels`
+};
+
+struct Network {
+  int n_labels = 0;
+  std::vector<NetTensor> tensors;
+  double log2_scale = 0.0;       // -(#|+> factors)/2
+  int edge_u = -1, edge_v = -1;
+};
+
+// PAPER.md:199-235 (§4.1) + Fig. 1 with the CNOT-Z-CNOT gadget fused into a
+// diagonal ZZ(gamma): live indices w(q,l) = l*N + q, l = 0..p-1 (reading A6).
+Network build_amplitude_network(int n, const std::vector<int>& edges, int p);
+// <psi|Z_u Z_v|psi> restricted to the reverse light cone of edge (u, v).
+Network build_cone_network(int n, const std::vector<int>& edges, int p, int u, int v);
+
+// ---------------------------------------------------------------- line graph
+class BitGraph {
+ public:
+  BitGraph() = default;
+  explicit BitGraph(int n);
+  static BitGraph from_network(const Network& net);
+  int size() const { return n_; }
+  bool alive(int v) const { return alive_[v] != 0; }
+  int degree(int v) const { return deg_[v]; }
+  int n_alive() const { return n_alive_; }
+  void add_edge(int a, int b);
+  // elimination of vertex v: remove it and make its neighbourhood a clique
+  void eliminate(int v);
+  // slicing: remove v and its edges, no fill-in
+  void remove(int v);
+  bool adjacent(int a, int b) const { return (row(a)[b >> 6] >> (b & 63)) & 1; }
+  const uint64_t* row(int v) const { return &adj_[(size_t)v * W_]; }
+  int words() const { return W_; }
+  int64_t fill_in(int v) const;  // non-adjacent neighbour pairs of v
+  std::vector<int> neighbours(int v) const;
+
+ private:
+  uint64_t* rowm(int v) { return &adj_[(size_t)v * W_]; }
+  int n_ = 0, W_ = 0, n_alive_ = 0;
+  std::vector<uint64_t> adj_;
+  std::vector<uint8_t> alive_;
+  std::vector<int> deg_;
+};
+
+struct Ordering {
+  std::vector<int> order;
+  std::vector<int> degrees;   // N_{G_i}(v_i)
+  int width = 0;              // max degree
+  double cost = 0.0;          // sum_i 2^{degree_i} ("C ~ 2^c")
+};
+
+// greedy orderers: orderer = TN_ORDER_MIN_FILL / TN_ORDER_MIN_DEGREE
+Ordering greedy_order(BitGraph g, int orderer);
+
+struct Schedule {
+  std::vector<int> prefix;    // phase A order (first slicing round's prefix, s indices)
+  std::vector<int> sliced;    // ascending labels; bit b of a slice id <-> sliced[b]
+  std::vector<int> residual;  // phase B order (later rounds' prefixes + final residual)
+  int width = 0, unsliced_width = 0;
+  double cost = 0.0;
+};
+
+// step-dependent slicing (Fig. slice_algo): n indices in rounds of r
+Schedule slice_search(const BitGraph& g0, int n, int r, int orderer);
+
+struct LoweredProgram {
+  std::vector<LeafRec> leaves;
+  std::vector<StepRec> steps;
+  std::vector<ScalarRec> scalars;
+  std::vector<OpRec> ops;
+  ProgramRec prog{};
+  uint64_t arena_elems = 0, persistent_elems = 0;
+  double elems_slice = 0, elems_prefix = 0, elems_big_slice = 0;
+  uint64_t big_launches_slice = 0, launches_prefix = 0, launches_slice = 0;
+  int width = 0;
+  std::vector<int> degrees;   // executed step degrees (phase A then phase B)
+};
+
+LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, std::string* err);
+
+}  // namespace tnb

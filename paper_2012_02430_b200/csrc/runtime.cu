@@ -1,0 +1,707 @@
+// runtime.cu -- the C ABI of libtnb200.so (include/tn_b200.h): plan build / load / info, the
+// step-program executor and the kernel launches.  Every step of the contraction runs in the
+// kernels of kernels.cuh; the host only sequences launches on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tn_b200.h"
+#include "kernels.cuh"
+#include "plan_format.h"
+#include "planner.h"
+
+using namespace tnb;
+
+// ============================================================== errors
+static thread_local std::string g_err;
+static tn_status fail(tn_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(TN_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+// ============================================================== plan object
+struct DevTables {
+  StepRec* steps = nullptr;
+  LeafRec* leaves = nullptr;
+  ScalarRec* scalars = nullptr;
+  ProgramRec* progs = nullptr;
+};
+
+struct ProfRec {
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+struct tn_plan {
+  PlanHeader h{};
+  std::vector<ProgramRec> progs;
+  std::vector<LeafRec> leaves;
+  std::vector<StepRec> steps;
+  std::vector<OpRec> ops;
+  std::vector<ScalarRec> scalars;
+  std::vector<int32_t> prefix, sliced, residual, degrees;
+  std::mutex mu;
+  std::map<int, DevTables> dev;
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  uint64_t all_launches = 0;
+  ~tn_plan() {
+    for (auto& kv : dev) {
+      cudaSetDevice(kv.first);
+      cudaFree(kv.second.steps);
+      cudaFree(kv.second.leaves);
+      cudaFree(kv.second.scalars);
+      cudaFree(kv.second.progs);
+    }
+    for (auto& p : prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
+};
+
+// ============================================================== serialization
+namespace {
+
+template <typename T>
+void put(std::vector<uint8_t>& buf, const T* p, size_t n) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(p);
+  buf.insert(buf.end(), b, b + n * sizeof(T));
+}
+
+template <typename T>
+bool get(const uint8_t*& cur, const uint8_t* end, std::vector<T>& v, int64_t n) {
+  if (n < 0) return false;
+  const size_t bytes = (size_t)n * sizeof(T);
+  if ((size_t)(end - cur) < bytes) return false;
+  v.resize((size_t)n);
+  if (bytes) std::memcpy(v.data(), cur, bytes);
+  cur += bytes;
+  return true;
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t ws_bytes_for(const PlanHeader& h, int dtype) {
+  const size_t es = dtype == TN_C64 ? 8 : 16;
+  const uint64_t nsl = 1ull << h.k;
+  const uint64_t nres = std::max<uint64_t>(nsl, (uint64_t)h.n_programs);
+  return align256(h.arena_elems * es) + align256(16 * nres) + 256;
+}
+
+}  // namespace
+
+// ============================================================== C ABI: planning
+extern "C" tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int32_t* edges,
+                                   int32_t p, const tn_build_opts* opts, void** buf, size_t* len) {
+  if (!opts || !buf || !len || (n_edges > 0 && !edges) || n_qubits <= 0 || n_edges < 0)
+    return fail(TN_E_INVAL, "tn_plan_build: null or negative argument");
+  if (p < 1 || p > kMaxP) return fail(TN_E_INVAL, "tn_plan_build: p out of range [1, 16]");
+  if (opts->orderer != TN_ORDER_MIN_FILL && opts->orderer != TN_ORDER_MIN_DEGREE)
+    return fail(TN_E_INVAL, "tn_plan_build: unknown orderer");
+  if (opts->kind != TN_KIND_AMPLITUDE && opts->kind != TN_KIND_ENERGY)
+    return fail(TN_E_INVAL, "tn_plan_build: unknown kind");
+  if (opts->n_sliced < 0 || opts->n_sliced > 30 || opts->r < 0)
+    return fail(TN_E_INVAL, "tn_plan_build: n_sliced must be in [0, 30], r >= 0");
+  if (opts->kind == TN_KIND_ENERGY && opts->n_sliced != 0)
+    return fail(TN_E_INVAL, "tn_plan_build: energy plans are unsliced");
+  const int small_log2 = opts->small_log2 < 0 ? 12 : opts->small_log2;
+  try {
+    std::vector<int> ev(edges, edges + 2 * (size_t)n_edges);
+    std::vector<Network> nets;
+    if (opts->kind == TN_KIND_AMPLITUDE) {
+      nets.push_back(build_amplitude_network(n_qubits, ev, p));
+    } else {
+      for (int e = 0; e < n_edges; ++e)
+        nets.push_back(build_cone_network(n_qubits, ev, p, ev[2 * e], ev[2 * e + 1]));
+    }
+    PlanHeader h;
+    std::memset(&h, 0, sizeof(h));
+    h.magic = kPlanMagic;
+    h.version = kPlanVersion;
+    h.kind = opts->kind;
+    h.n_qubits = n_qubits;
+    h.p = p;
+    h.n_edges = n_edges;
+    h.orderer = opts->orderer;
+    h.small_log2 = small_log2;
+    h.n_labels = nets.empty() ? 0 : nets[0].n_labels;
+    std::vector<ProgramRec> progs;
+    std::vector<LeafRec> leaves;
+    std::vector<StepRec> steps;
+    std::vector<OpRec> ops;
+    std::vector<ScalarRec> scal;
+    Schedule sch0;
+    std::vector<int> degrees0;
+    uint64_t arena = 0;
+    for (size_t ni = 0; ni < nets.size(); ++ni) {
+      const Network& net = nets[ni];
+      BitGraph g = BitGraph::from_network(net);
+      Schedule sch = slice_search(g, opts->n_sliced, opts->r, opts->orderer);
+      if (opts->max_width > 0 && sch.width > opts->max_width) {
+        return fail(TN_E_TOO_WIDE, "contraction width " + std::to_string(sch.width) +
+                                       " exceeds max_width " + std::to_string(opts->max_width));
+      }
+      std::string err;
+      LoweredProgram lp = lower(net, sch, small_log2, &err);
+      if (!err.empty()) return fail(TN_E_PLAN, "lowering: " + err);
+      if (opts->max_width > 0 && lp.width > opts->max_width)
+        return fail(TN_E_TOO_WIDE, "contraction width " + std::to_string(lp.width));
+      const int32_t leaf0 = (int32_t)leaves.size(), step0 = (int32_t)steps.size();
+      const int32_t op0 = (int32_t)ops.size(), sc0 = (int32_t)scal.size();
+      for (auto l : lp.leaves) { l.off += arena; leaves.push_back(l); }
+      for (auto s : lp.steps) {
+        s.out_off += arena;
+        for (int t = 0; t < s.n_in; ++t) s.in[t].off += arena;
+        steps.push_back(s);
+      }
+      for (auto o : lp.ops) { o.begin += step0; o.end += step0; ops.push_back(o); }
+      for (auto s : lp.scalars) { s.off += arena; s.program = (int32_t)ni; scal.push_back(s); }
+      ProgramRec pr = lp.prog;
+      pr.stepA_begin += step0; pr.stepA_end += step0;
+      pr.stepB_begin += step0; pr.stepB_end += step0;
+      pr.opA_begin += op0; pr.opA_end += op0;
+      pr.opB_begin += op0; pr.opB_end += op0;
+      pr.scal_begin += sc0; pr.scal_end += sc0;
+      pr.arena_begin = arena;
+      pr.arena_end = arena + lp.arena_elems;
+      progs.push_back(pr);
+      (void)leaf0;
+      arena += lp.arena_elems;
+      h.width = std::max(h.width, lp.width);
+      h.unsliced_width = std::max(h.unsliced_width, sch.unsliced_width);
+      if (ni == 0) {
+        sch0 = sch;
+        degrees0 = lp.degrees;
+        h.k = (int32_t)sch.sliced.size();
+        h.r = opts->r == 0 ? h.k : opts->r;
+        h.slice_step = (int32_t)sch.prefix.size();
+        h.persistent_elems = lp.persistent_elems;
+      }
+      h.pred_elems_slice += lp.elems_slice;
+      h.pred_elems_prefix += lp.elems_prefix;
+      h.pred_elems_big_slice += lp.elems_big_slice;
+      h.big_launches_slice += lp.big_launches_slice;
+      h.launches_prefix += lp.launches_prefix;
+      h.launches_slice += lp.launches_slice;
+    }
+    h.arena_elems = arena;
+    h.n_programs = (int32_t)progs.size();
+    h.n_leaves = (int32_t)leaves.size();
+    h.n_steps = (int32_t)steps.size();
+    h.n_ops = (int32_t)ops.size();
+    h.n_scalars = (int32_t)scal.size();
+    h.n_prefix = (int32_t)sch0.prefix.size();
+    h.n_residual = (int32_t)sch0.residual.size();
+    h.n_degrees = (int32_t)degrees0.size();
+    std::vector<uint8_t> out;
+    put(out, &h, 1);
+    put(out, progs.data(), progs.size());
+    put(out, leaves.data(), leaves.size());
+    put(out, steps.data(), steps.size());
+    put(out, ops.data(), ops.size());
+    put(out, scal.data(), scal.size());
+    put(out, sch0.prefix.data(), sch0.prefix.size());
+    put(out, sch0.sliced.data(), sch0.sliced.size());
+    put(out, sch0.residual.data(), sch0.residual.size());
+    put(out, degrees0.data(), degrees0.size());
+    void* mem = std::malloc(out.size());
+    if (!mem) return fail(TN_E_NOMEM, "tn_plan_build: out of host memory");
+    std::memcpy(mem, out.data(), out.size());
+    *buf = mem;
+    *len = out.size();
+    return TN_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(TN_E_PLAN, std::string("tn_plan_build: ") + e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(TN_E_NOMEM, "tn_plan_build: out of host memory");
+  } catch (const std::exception& e) {
+    return fail(TN_E_PLAN, std::string("tn_plan_build: ") + e.what());
+  }
+}
+
+extern "C" void tn_buffer_free(void* buf) { std::free(buf); }
+
+// ============================================================== C ABI: load / info
+extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
+  if (!buf || !out) return fail(TN_E_INVAL, "tn_plan_load: null argument");
+  *out = nullptr;
+  const uint8_t* cur = static_cast<const uint8_t*>(buf);
+  const uint8_t* end = cur + len;
+  if (len < sizeof(PlanHeader)) return fail(TN_E_PLAN, "tn_plan_load: buffer too short");
+  std::unique_ptr<tn_plan> pl(new (std::nothrow) tn_plan());
+  if (!pl) return fail(TN_E_NOMEM, "tn_plan_load: out of host memory");
+  std::memcpy(&pl->h, cur, sizeof(PlanHeader));
+  cur += sizeof(PlanHeader);
+  const PlanHeader& h = pl->h;
+  if (h.magic != kPlanMagic || h.version != kPlanVersion)
+    return fail(TN_E_PLAN, "tn_plan_load: bad magic or version");
+  if (h.k < 0 || h.k > 30 || h.p < 1 || h.p > kMaxP || h.n_programs < 1)
+    return fail(TN_E_PLAN, "tn_plan_load: bad header");
+  if (!get(cur, end, pl->progs, h.n_programs) || !get(cur, end, pl->leaves, h.n_leaves) ||
+      !get(cur, end, pl->steps, h.n_steps) || !get(cur, end, pl->ops, h.n_ops) ||
+      !get(cur, end, pl->scalars, h.n_scalars) || !get(cur, end, pl->prefix, h.n_prefix) ||
+      !get(cur, end, pl->sliced, h.k) || !get(cur, end, pl->residual, h.n_residual) ||
+      !get(cur, end, pl->degrees, h.n_degrees))
+    return fail(TN_E_PLAN, "tn_plan_load: truncated buffer");
+  if (cur != end) return fail(TN_E_PLAN, "tn_plan_load: trailing bytes");
+  // validation: every access stays inside the arena
+  const uint64_t A = h.arena_elems;
+  for (const auto& l : pl->leaves)
+    if (l.rank < 0 || l.rank > 2 || l.nfact < 1 || l.nfact > kMaxFactors || l.off + 4 > A + kAlign)
+      return fail(TN_E_PLAN, "tn_plan_load: bad leaf record");
+  for (const auto& s : pl->steps) {
+    if (s.n_in < 1 || s.n_in > kMaxIn || s.out_rank < 0 || s.out_rank > 62)
+      return fail(TN_E_PLAN, "tn_plan_load: bad step record");
+    if (s.out_off + (1ull << s.out_rank) > A) return fail(TN_E_PLAN, "tn_plan_load: step output out of arena");
+    for (int t = 0; t < s.n_in; ++t) {
+      const InRec& in = s.in[t];
+      const int full = (int)in.rank + __builtin_popcount(in.slice_mask);
+      if (in.rank < 1 || full > 62 || in.pv >= in.rank ||
+          __builtin_popcountll(in.out_mask) + 1 != (int)in.rank ||
+          (s.out_rank < 64 && (in.out_mask >> s.out_rank) != 0) ||
+          (in.slice_mask >> h.k) != 0 || in.off + (1ull << full) > A)
+        return fail(TN_E_PLAN, "tn_plan_load: bad step input record");
+    }
+  }
+  for (const auto& o : pl->ops)
+    if (o.begin < 0 || o.end > h.n_steps || o.begin >= o.end || (o.type != OP_BIG && o.type != OP_RUN) ||
+        (o.type == OP_BIG && pl->steps[o.begin].out_rank < 1))
+      return fail(TN_E_PLAN, "tn_plan_load: bad op record");
+  for (const auto& s : pl->scalars)
+    if ((s.slice_mask >> h.k) != 0 || s.off + (1ull << __builtin_popcount(s.slice_mask)) > A)
+      return fail(TN_E_PLAN, "tn_plan_load: bad scalar record");
+  for (const auto& pr : pl->progs)
+    if (pr.stepB_begin < 0 || pr.stepB_end > h.n_steps || pr.scal_begin < 0 || pr.scal_end > h.n_scalars ||
+        pr.opA_begin < 0 || pr.opB_end > h.n_ops)
+      return fail(TN_E_PLAN, "tn_plan_load: bad program record");
+  *out = pl.release();
+  return TN_OK;
+}
+
+extern "C" void tn_plan_free(tn_plan* plan) { delete plan; }
+
+extern "C" tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* o) {
+  if (!plan || !o) return fail(TN_E_INVAL, "tn_plan_info: null argument");
+  const PlanHeader& h = plan->h;
+  std::memset(o, 0, sizeof(*o));
+  o->kind = h.kind;
+  o->n_qubits = h.n_qubits;
+  o->p = h.p;
+  o->n_edges = h.n_edges;
+  o->width = h.width;
+  o->unsliced_width = h.unsliced_width;
+  o->k = h.k;
+  o->slice_step = h.slice_step;
+  o->n_programs = h.n_programs;
+  o->n_labels = h.n_labels;
+  o->n_slices = 1ull << h.k;
+  uint64_t nA = 0, nB = 0;
+  for (const auto& s : plan->steps) (s.phase == 0 ? nA : nB)++;
+  o->prefix_steps = nA;
+  o->steps_per_slice = nB;
+  o->launches_prefix = h.launches_prefix;
+  o->launches_per_slice = h.launches_slice;
+  for (int d = 0; d < 2; ++d) {
+    const double es = d == 0 ? 8.0 : 16.0;
+    o->workspace_bytes[d] = ws_bytes_for(h, d);
+    o->pred_bytes_per_slice[d] = h.pred_elems_slice * es;
+    o->pred_bytes_prefix[d] = h.pred_elems_prefix * es;
+    o->pred_bytes_big_per_slice[d] = h.pred_elems_big_slice * es;
+  }
+  o->big_launches_per_slice = h.big_launches_slice;
+  return TN_OK;
+}
+
+extern "C" tn_status tn_plan_schedule(const tn_plan* plan, int32_t* prefix, int32_t* sliced,
+                                      int32_t* residual, int32_t* degrees) {
+  if (!plan) return fail(TN_E_INVAL, "tn_plan_schedule: null plan");
+  if (prefix) std::copy(plan->prefix.begin(), plan->prefix.end(), prefix);
+  if (sliced) std::copy(plan->sliced.begin(), plan->sliced.end(), sliced);
+  if (residual) std::copy(plan->residual.begin(), plan->residual.end(), residual);
+  if (degrees) std::copy(plan->degrees.begin(), plan->degrees.end(), degrees);
+  return TN_OK;
+}
+
+extern "C" tn_status tn_sum_partials(const tn_plan* plan, const double* partials, double out[2]) {
+  if (!plan || !partials || !out) return fail(TN_E_INVAL, "tn_sum_partials: null argument");
+  const uint64_t n = 1ull << plan->h.k;
+  std::vector<double> buf(partials, partials + 2 * n);
+  uint64_t m = n;
+  while (m > 1) {
+    uint64_t hh = 0;
+    for (uint64_t i = 0; i + 1 < m; i += 2, ++hh) {
+      buf[2 * hh] = buf[2 * i] + buf[2 * (i + 1)];
+      buf[2 * hh + 1] = buf[2 * i + 1] + buf[2 * (i + 1) + 1];
+    }
+    if (m & 1) {
+      buf[2 * hh] = buf[2 * (m - 1)];
+      buf[2 * hh + 1] = buf[2 * (m - 1) + 1];
+      ++hh;
+    }
+    m = hh;
+  }
+  out[0] = buf[0];
+  out[1] = buf[1];
+  return TN_OK;
+}
+
+// ============================================================== executor
+namespace {
+
+tn_status ensure_dev(tn_plan* pl, DevTables** out) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(pl->mu);
+  auto it = pl->dev.find(dev);
+  if (it == pl->dev.end()) {
+    DevTables t;
+    auto up = [](void** dst, const void* src, size_t bytes) -> cudaError_t {
+      cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+      if (e != cudaSuccess) return e;
+      return bytes ? cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    CU(up((void**)&t.steps, pl->steps.data(), pl->steps.size() * sizeof(StepRec)));
+    CU(up((void**)&t.leaves, pl->leaves.data(), pl->leaves.size() * sizeof(LeafRec)));
+    CU(up((void**)&t.scalars, pl->scalars.data(), pl->scalars.size() * sizeof(ScalarRec)));
+    CU(up((void**)&t.progs, pl->progs.data(), pl->progs.size() * sizeof(ProgramRec)));
+    it = pl->dev.emplace(dev, t).first;
+  }
+  *out = &it->second;
+  return TN_OK;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+uint64_t host_pext(uint64_t x, uint64_t m) {
+  uint64_t r = 0;
+  int k = 0;
+  while (m) {
+    const uint64_t b = m & (~m + 1);
+    if (x & b) r |= 1ull << k;
+    ++k;
+    m ^= b;
+  }
+  return r;
+}
+
+template <typename T, int NIN>
+void launch_bucket_n(const BigArgs& a, cudaStream_t st) {
+  constexpr int VEC = VecT<T>::n;
+  constexpr uint64_t TILE = (uint64_t)kBucketThreads * VEC * kBucketIters;
+  const uint64_t n_out = 1ull << a.out_rank;
+  const uint64_t tiles = (n_out + TILE - 1) / TILE;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, cap);
+  k_bucket<T, NIN><<<grid, kBucketThreads, 0, st>>>(a);
+}
+
+template <typename T>
+void launch_bucket(const BigArgs& a, cudaStream_t st) {
+  switch (a.n_in) {
+    case 1: launch_bucket_n<T, 1>(a, st); break;
+    case 2: launch_bucket_n<T, 2>(a, st); break;
+    case 3: launch_bucket_n<T, 3>(a, st); break;
+    case 4: launch_bucket_n<T, 4>(a, st); break;
+    case 5: launch_bucket_n<T, 5>(a, st); break;
+    case 6: launch_bucket_n<T, 6>(a, st); break;
+    case 7: launch_bucket_n<T, 7>(a, st); break;
+    default: launch_bucket_n<T, 8>(a, st); break;
+  }
+}
+
+cudaEvent_t pool_event(tn_plan* pl) {
+  if (!pl->ev_pool.empty()) {
+    cudaEvent_t e = pl->ev_pool.back();
+    pl->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <typename T>
+tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, uint64_t j,
+                  cudaStream_t st) {
+  for (int oi = op_b; oi < op_e; ++oi) {
+    const OpRec& op = pl->ops[oi];
+    if (op.type == OP_BIG) {
+      const StepRec& s = pl->steps[op.begin];
+      BigArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.out = ws + s.out_off;
+      a.out_rank = s.out_rank;
+      a.n_in = s.n_in;
+      double bytes = std::ldexp((double)sizeof(T), s.out_rank);
+      for (int t = 0; t < s.n_in; ++t) {
+        const InRec& in = s.in[t];
+        const uint64_t soff = in.slice_mask ? (host_pext(j, in.slice_mask) << in.rank) : 0;
+        a.in[t] = ws + in.off + soff;
+        a.out_mask[t] = in.out_mask;
+        a.pv[t] = in.pv;
+        a.flags[t] = in.flags | ((t == 0 && s.inplace) ? 1u : 0u);
+        bytes += std::ldexp((double)sizeof(T), (int)in.rank);
+      }
+      ProfRec pr{};
+      if (pl->profiling) {
+        pr.a = pool_event(pl);
+        pr.b = pool_event(pl);
+        pr.bytes = bytes;
+        cudaEventRecord(pr.a, st);
+      }
+      launch_bucket<T>(a, st);
+      if (pl->profiling) {
+        cudaEventRecord(pr.b, st);
+        pl->prof.push_back(pr);
+      }
+    } else {
+      k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
+                                                  dt.scalars, nullptr, 0);
+    }
+    pl->all_launches++;
+  }
+  CU(cudaGetLastError());
+  return TN_OK;
+}
+
+template <typename T>
+tn_status materialize(tn_plan* pl, const DevTables& dt, const double* gamma, const double* beta,
+                      int p, T* ws, cudaStream_t st) {
+  Angles ang;
+  std::memset(&ang, 0, sizeof(ang));
+  for (int l = 0; l < p; ++l) {
+    ang.gamma[l] = gamma[l];
+    ang.beta[l] = beta[l];
+  }
+  ang.p = p;
+  const int n = (int)pl->leaves.size() * 4;
+  if (n > 0) k_materialize<T><<<(n + 255) / 256, 256, 0, st>>>(dt.leaves, (int)pl->leaves.size(), ang, ws);
+  pl->all_launches++;
+  CU(cudaGetLastError());
+  return TN_OK;
+}
+
+tn_status check_call(const tn_plan* plan, int dtype, const double* gamma, const double* beta,
+                     int p, void* ws, size_t ws_bytes) {
+  if (!plan || !gamma || !beta || !ws) return fail(TN_E_INVAL, "null argument");
+  if (dtype != TN_C64 && dtype != TN_C128) return fail(TN_E_DTYPE, "unsupported dtype");
+  if (p != plan->h.p) return fail(TN_E_INVAL, "p does not match the plan");
+  if (ws_bytes < ws_bytes_for(plan->h, dtype)) return fail(TN_E_INVAL, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(TN_E_INVAL, "workspace must be 256-byte aligned");
+  return TN_OK;
+}
+
+template <typename T>
+tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int p, uint64_t begin,
+                      uint64_t end, void* wsv, cudaStream_t st, double* partials_dev) {
+  DevTables* dt = nullptr;
+  tn_status s = ensure_dev(pl, &dt);
+  if (s != TN_OK) return s;
+  T* ws = static_cast<T*>(wsv);
+  if ((s = materialize<T>(pl, *dt, gamma, beta, p, ws, st)) != TN_OK) return s;
+  const ProgramRec& pr = pl->progs[0];
+  if ((s = run_ops<T>(pl, *dt, pr.opA_begin, pr.opA_end, ws, 0, st)) != TN_OK) return s;
+  for (uint64_t j = begin; j < end; ++j) {
+    if ((s = run_ops<T>(pl, *dt, pr.opB_begin, pr.opB_end, ws, j, st)) != TN_OK) return s;
+    k_finalize<T><<<1, 32, 0, st>>>(dt->scalars, pr.scal_begin, pr.scal_end, ws, j, pr.log2_scale,
+                                   partials_dev + 2 * j);
+    pl->all_launches++;
+  }
+  CU(cudaGetLastError());
+  return TN_OK;
+}
+
+double* scratch_ptr(const tn_plan* pl, int dtype, void* ws) {
+  const size_t es = dtype == TN_C64 ? 8 : 16;
+  return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + align256(pl->h.arena_elems * es));
+}
+
+}  // namespace
+
+// ============================================================== C ABI: contraction
+extern "C" tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, const double* gamma,
+                                        const double* beta, int32_t p, uint64_t begin, uint64_t end,
+                                        void* ws, size_t ws_bytes, void* stream,
+                                        double* partials_dev) {
+  tn_status s = check_call(plan, dtype, gamma, beta, p, ws, ws_bytes);
+  if (s != TN_OK) return s;
+  if (plan->h.kind != TN_KIND_AMPLITUDE) return fail(TN_E_INVAL, "not an amplitude plan");
+  if (!partials_dev) return fail(TN_E_INVAL, "null partials");
+  if (begin > end || end > (1ull << plan->h.k)) return fail(TN_E_INVAL, "bad slice range");
+  tn_plan* pl = const_cast<tn_plan*>(plan);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return dtype == TN_C64 ? sliced_impl<float2>(pl, gamma, beta, p, begin, end, ws, st, partials_dev)
+                         : sliced_impl<double2>(pl, gamma, beta, p, begin, end, ws, st, partials_dev);
+}
+
+extern "C" tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma,
+                                 const double* beta, int32_t p, void* ws, size_t ws_bytes,
+                                 void* stream, double out[2]) {
+  tn_status s = check_call(plan, dtype, gamma, beta, p, ws, ws_bytes);
+  if (s != TN_OK) return s;
+  if (!out) return fail(TN_E_INVAL, "null out");
+  if (plan->h.kind != TN_KIND_AMPLITUDE) return fail(TN_E_INVAL, "not an amplitude plan");
+  const uint64_t n = 1ull << plan->h.k;
+  double* scratch = scratch_ptr(plan, dtype, ws);
+  s = tn_contract_sliced(plan, dtype, gamma, beta, p, 0, n, ws, ws_bytes, stream, scratch);
+  if (s != TN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // scratch: 2*max(n, E) doubles of partials, then the pairwise result in the trailing pad
+  double* res = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(scratch) + align256(16 * std::max<uint64_t>(n, plan->h.n_programs)));
+  k_pairwise<<<1, 32, 0, st>>>(scratch, n, res);
+  const_cast<tn_plan*>(plan)->all_launches++;
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(out, res, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return TN_OK;
+}
+
+extern "C" tn_status tn_energy(const tn_plan* plan, tn_dtype dtype, const double* gamma,
+                               const double* beta, int32_t p, void* ws, size_t ws_bytes,
+                               void* stream, double* zz, double* zz_imag_max, double* energy) {
+  tn_status s = check_call(plan, dtype, gamma, beta, p, ws, ws_bytes);
+  if (s != TN_OK) return s;
+  if (plan->h.kind != TN_KIND_ENERGY) return fail(TN_E_INVAL, "not an energy plan");
+  if (!zz) return fail(TN_E_INVAL, "null zz");
+  tn_plan* pl = const_cast<tn_plan*>(plan);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DevTables* dt = nullptr;
+  if ((s = ensure_dev(pl, &dt)) != TN_OK) return s;
+  double* scratch = scratch_ptr(plan, dtype, ws);
+  const int E = plan->h.n_programs;
+  if (dtype == TN_C64) {
+    float2* w = static_cast<float2*>(ws);
+    if ((s = materialize<float2>(pl, *dt, gamma, beta, p, w, st)) != TN_OK) return s;
+    k_program<float2><<<E, kProgramThreads, 0, st>>>(dt->steps, 0, 0, w, 0, dt->progs, dt->scalars,
+                                                     reinterpret_cast<double2*>(scratch), 1);
+  } else {
+    double2* w = static_cast<double2*>(ws);
+    if ((s = materialize<double2>(pl, *dt, gamma, beta, p, w, st)) != TN_OK) return s;
+    k_program<double2><<<E, kProgramThreads, 0, st>>>(dt->steps, 0, 0, w, 0, dt->progs, dt->scalars,
+                                                      reinterpret_cast<double2*>(scratch), 1);
+  }
+  pl->all_launches++;
+  CU(cudaGetLastError());
+  std::vector<double> h(2 * (size_t)E);
+  CU(cudaMemcpyAsync(h.data(), scratch, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  double im = 0.0, en = 0.0;
+  for (int e = 0; e < E; ++e) {
+    zz[e] = h[2 * e];
+    im = std::max(im, std::fabs(h[2 * e + 1]));
+    en += (1.0 - h[2 * e]) / 2.0;
+  }
+  if (zz_imag_max) *zz_imag_max = im;
+  if (energy) *energy = en;
+  return TN_OK;
+}
+
+extern "C" tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* const* in_dev,
+                                  const uint64_t* out_mask, const int32_t* pv, void* out_dev,
+                                  int32_t out_rank, void* stream) {
+  if (n_in < 1 || n_in > kMaxIn || !in_dev || !out_mask || !pv || !out_dev)
+    return fail(TN_E_INVAL, "tn_eliminate: bad argument");
+  if (out_rank < 0 || out_rank > 40) return fail(TN_E_INVAL, "tn_eliminate: out_rank out of range");
+  if (dtype != TN_C64 && dtype != TN_C128) return fail(TN_E_DTYPE, "unsupported dtype");
+  BigArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.out = out_dev;
+  a.out_rank = out_rank;
+  a.n_in = n_in;
+  for (int t = 0; t < n_in; ++t) {
+    if (!in_dev[t] || pv[t] < 0 || pv[t] > 62) return fail(TN_E_INVAL, "tn_eliminate: bad input");
+    if (out_rank < 64 && (out_mask[t] >> out_rank) != 0) return fail(TN_E_INVAL, "tn_eliminate: mask beyond out_rank");
+    if (pv[t] > __builtin_popcountll(out_mask[t])) return fail(TN_E_INVAL, "tn_eliminate: pv beyond input rank");
+    a.in[t] = in_dev[t];
+    a.out_mask[t] = out_mask[t];
+    a.pv[t] = (uint32_t)pv[t];
+    a.flags[t] = 0;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (out_rank == 0) {
+    // a scalar output: route through the interpreter-style path of the standalone kernel is
+    // not possible (VEC pairs); use a one-step program in a temporary device record
+    StepRec rec;
+    std::memset(&rec, 0, sizeof(rec));
+    rec.out_rank = 0;
+    rec.n_in = n_in;
+    StepRec* d = nullptr;
+    CU(cudaMallocAsync((void**)&d, sizeof(StepRec), st));
+    // offsets relative to a null base: encode absolute element addresses
+    const size_t es = dtype == TN_C64 ? 8 : 16;
+    rec.out_off = reinterpret_cast<uintptr_t>(out_dev) / es;
+    for (int t = 0; t < n_in; ++t) {
+      rec.in[t].off = reinterpret_cast<uintptr_t>(in_dev[t]) / es;
+      rec.in[t].out_mask = 0;
+      rec.in[t].rank = 1;
+      rec.in[t].pv = 0;
+    }
+    CU(cudaMemcpyAsync(d, &rec, sizeof(rec), cudaMemcpyHostToDevice, st));
+    if (dtype == TN_C64)
+      k_program<float2><<<1, 32, 0, st>>>(d, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0);
+    else
+      k_program<double2><<<1, 32, 0, st>>>(d, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0);
+    CU(cudaFreeAsync(d, st));
+    CU(cudaGetLastError());
+    return TN_OK;
+  }
+  if (dtype == TN_C64) launch_bucket<float2>(a, st); else launch_bucket<double2>(a, st);
+  CU(cudaGetLastError());
+  return TN_OK;
+}
+
+extern "C" tn_status tn_profile_enable(tn_plan* plan, int32_t enable) {
+  if (!plan) return fail(TN_E_INVAL, "null plan");
+  plan->profiling = enable != 0;
+  return TN_OK;
+}
+
+extern "C" tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms,
+                                     double* total_bytes, uint64_t* all_launches) {
+  if (!plan) return fail(TN_E_INVAL, "null plan");
+  double ms = 0.0, bytes = 0.0;
+  for (auto& p : plan->prof) {
+    CU(cudaEventSynchronize(p.b));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, p.a, p.b));
+    ms += t;
+    bytes += p.bytes;
+    plan->ev_pool.push_back(p.a);
+    plan->ev_pool.push_back(p.b);
+  }
+  if (launches) *launches = plan->prof.size();
+  if (total_ms) *total_ms = ms;
+  if (total_bytes) *total_bytes = bytes;
+  if (all_launches) *all_launches = plan->all_launches;
+  plan->prof.clear();
+  plan->all_launches = 0;
+  return TN_OK;
+}
+
+extern "C" const char* tn_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t tn_version(void) { return (int32_t)kPlanVersion; }

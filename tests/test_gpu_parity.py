@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative error <= 1e-10 for complex128 and <= 1e-4 for
+complex64, relative to |oracle value| (amplitudes) or absolute on <Z_u Z_v> in [-1, 1].
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # the -m gpu suite runs on a B200 only
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2012_02430_b200 as T  # noqa: E402
+from paper_2012_02430_b200 import _binding as B  # noqa: E402
+from paper_2012_02430_b200.scheduler import run_sliced  # noqa: E402
+from oracle import closed_forms as cf  # noqa: E402
+from oracle import contract, energy, network  # noqa: E402
+from oracle import statevector as sv  # noqa: E402
+from tn_inputs import qaoa_angles, random_regular_graph  # noqa: E402
+
+TOL = {T.TN_C64: 1e-4, T.TN_C128: 1e-10}
+DT = {T.TN_C64: torch.complex64, T.TN_C128: torch.complex128}
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+# ------------------------------------------------------------------ one bucket step (tn_eliminate)
+def _random_step(rng, out_rank, n_in):
+    masks, pvs, shapes = [], [], []
+    for t in range(n_in):
+        m = 0
+        for b in range(out_rank):
+            if rng.random() < 0.6:
+                m |= 1 << b
+        if t == 0 and out_rank > 0:
+            m = (1 << out_rank) - 1          # one input holds every output bit (reduce-like)
+        r_in = bin(m).count("1") + 1
+        masks.append(m)
+        pvs.append(int(rng.integers(0, r_in)))
+        shapes.append(r_in)
+    return masks, pvs, shapes
+
+
+def _oracle_step(arrays, masks, pvs, out_rank):
+    # labels: output bit b -> label b ; summed index -> label 100.  Input axes are most
+    # significant first: input bit position q -> axis (rank-1-q).
+    ts = []
+    for a, m, pv in zip(arrays, masks, pvs):
+        bits = [b for b in range(out_rank) if (m >> b) & 1]   # input positions 0.. (skipping pv)
+        pos_labels = []
+        it = iter(bits)
+        for q in range(len(bits) + 1):
+            pos_labels.append(100 if q == pv else next(it))
+        labs = tuple(reversed(pos_labels))                      # axis 0 = most significant
+        ts.append((a.reshape((2,) * len(labs)) if labs else a, labs))
+    arr, labs = contract._einsum_bucket(ts, 100)
+    # oracle output axes are ascending labels = ascending output bit; flatten most-significant first
+    want = tuple(reversed(range(out_rank)))
+    if labs:
+        arr = np.transpose(arr, [labs.index(l) for l in want])
+    return arr.reshape(-1)
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+@pytest.mark.parametrize("out_rank,n_in", [(0, 1), (0, 3), (1, 2), (2, 3), (5, 1), (9, 2), (12, 4),
+                                           (13, 3), (14, 8), (17, 2), (18, 5), (21, 3)])
+def test_eliminate_vs_oracle(dtype, out_rank, n_in):
+    rng = np.random.default_rng(out_rank * 31 + n_in * 7 + dtype)
+    masks, pvs, shapes = _random_step(rng, out_rank, n_in)
+    arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+    dev = [torch.tensor(a, dtype=DT[dtype], device="cuda") for a in arrays]
+    out = torch.empty(2 ** out_rank, dtype=DT[dtype], device="cuda")
+    B.tn_eliminate(dtype, [d.data_ptr() for d in dev], masks, pvs, out.data_ptr(), out_rank,
+                   torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.complex128)
+    ref = _oracle_step(arrays, masks, pvs, out_rank)
+    scale = np.max(np.abs(ref)) + 1e-30
+    assert np.max(np.abs(got - ref)) / scale < TOL[dtype] * 0.1
+
+
+# ------------------------------------------------------------------ amplitudes, small/medium
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+@pytest.mark.parametrize("n,p,k,orderer", [(12, 1, 0, "min-fill"), (14, 2, 0, "min-degree"),
+                                           (16, 3, 2, "min-fill"), (20, 2, 3, "min-degree"),
+                                           (24, 1, 4, "min-fill"), (30, 2, 2, "min-fill")])
+def test_amplitude_vs_oracle(dtype, n, p, k, orderer):
+    g = random_regular_graph(n, 3, n + p)
+    ga, be = qaoa_angles(p, n)
+    plan = T.build_plan(g, p, "amplitude", orderer, n_sliced=k, small_log2=4)
+    got = plan.contract(ga, be, dtype=dtype)
+    ref = contract.contract(network.qaoa_amplitude_network(n, g.edges, ga, be))
+    assert rel(got, ref) < TOL[dtype]
+    if n <= 16:
+        assert rel(got, sv.amplitude(sv.qaoa_state(n, g.edges, ga, be))) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+def test_interpreter_only_and_big_only_agree(dtype):
+    n, p = 22, 2
+    g = random_regular_graph(n, 3, 5)
+    ga, be = qaoa_angles(p, 5)
+    ref = contract.contract(network.qaoa_amplitude_network(n, g.edges, ga, be))
+    for small in (0, 3, 30):   # 0: every step standalone; 30: everything in the interpreter
+        plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=2, small_log2=small)
+        assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
+
+
+def test_slice_partials_vs_oracle_per_slice():
+    """Every per-slice partial of a sliced plan vs the oracle's slice (plan schedule as data)."""
+    n, p, k = 40, 1, 3
+    g = random_regular_graph(n, 3, 40)
+    ga, be = qaoa_angles(p, 40)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=k)
+    pre, sl, res, _ = plan.schedule()
+    tens = network.qaoa_amplitude_network(n, g.edges, ga, be)
+    tot, parts = contract.contract_sliced(tens, pre, sl, res, return_parts=True)
+    partials = torch.zeros(2 * plan.n_slices, dtype=torch.float64, device="cuda")
+    plan.contract_sliced(ga, be, 0, plan.n_slices, partials, dtype=T.TN_C128)
+    torch.cuda.synchronize()
+    h = partials.cpu().numpy()
+    for j in range(plan.n_slices):
+        assert abs(complex(h[2 * j], h[2 * j + 1]) - parts[j]) <= 1e-10 * abs(tot)
+    assert rel(plan.sum_partials(h.tolist()), tot) < 1e-10
+
+
+def test_partition_is_bit_identical():
+    n, p = 30, 1
+    g = random_regular_graph(n, 3, 9)
+    ga, be = qaoa_angles(p, 9)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=4)
+    full = torch.zeros(2 * plan.n_slices, dtype=torch.float64, device="cuda")
+    plan.contract_sliced(ga, be, 0, plan.n_slices, full, dtype=T.TN_C64)
+    parts = torch.zeros_like(full)
+    cuts = [0, 3, 8, 9, 16]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        plan.contract_sliced(ga, be, a, b, parts, dtype=T.TN_C64)
+    torch.cuda.synchronize()
+    assert torch.equal(full, parts)
+    s1 = plan.sum_partials(full.cpu().tolist())
+    s2, _ = run_sliced(plan, ga, be, dtype=T.TN_C64)
+    assert s1 == s2
+
+
+# ------------------------------------------------------------------ energy (C1, C3)
+@pytest.mark.parametrize("dtype", [T.TN_C128, T.TN_C64])
+def test_energy_c1_vs_statevector(dtype):
+    n, p = 16, 1
+    g = random_regular_graph(n, 3, 0)
+    ga, be = qaoa_angles(p, 0)
+    plan = T.build_plan(g, p, "energy", "min-fill")
+    zz, im, E = plan.energy(ga, be, dtype=dtype)
+    psi = sv.qaoa_state(n, g.edges, ga, be)
+    for (u, v), z in zip(g.edges, zz):
+        assert abs(z - sv.zz_expectation(psi, u, v)) < TOL[dtype]
+        assert abs(z - cf.wang_p1_zz(g.edges, u, v, ga[0], be[0])) < TOL[dtype]
+    assert abs(E - sv.maxcut_energy(psi, g.edges)) < TOL[dtype] * len(g.edges)
+    assert im < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C128, T.TN_C64])
+@pytest.mark.parametrize("n,p", [(16, 2), (16, 3), (100, 3)])
+def test_energy_vs_oracle(dtype, n, p):
+    g = random_regular_graph(n, 3, 0)
+    ga, be = qaoa_angles(p, 0)
+    plan = T.build_plan(g, p, "energy", "min-fill")
+    zz, im, E = plan.energy(ga, be, dtype=dtype)
+    Eref, zref = energy.maxcut_energy(n, g.edges, ga, be)
+    assert max(abs(a - b.real) for a, b in zip(zz, zref)) < TOL[dtype]
+    assert abs(E - Eref) < TOL[dtype] * len(g.edges)
+    assert 0.0 <= E <= len(g.edges)
+
+
+# ------------------------------------------------------------------ full-scale closed forms
+def _bench_plan():
+    import bench
+    return bench.build_workload_plan("C5a")
+
+
+@pytest.mark.parametrize("which", ["gamma0", "beta0", "gammapi"])
+def test_c5a_full_scale_closed_forms(which):
+    """C5a (N=210, p=1) at the bench's plan and dtype vs closed forms that hold at any N."""
+    plan, g, ga, be, meta = _bench_plan()
+    n = g.n
+    if which == "gamma0":
+        ga, ref = [0.0], cf.amp_gamma0(n, be)
+    elif which == "beta0":
+        be, ref = [0.0], cf.amp_beta0(n)
+    else:
+        ga, ref = [math.pi], cf.amp_gamma_pi(n, be)
+    got, _ = run_sliced(plan, ga, be, dtype=T.TN_C64)
+    assert rel(got, ref) < 1e-4

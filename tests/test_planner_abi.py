@@ -1,0 +1,158 @@
+"""Host-side tests (-m "not gpu"): the C-ABI library loads and exports every symbol of
+include/tn_b200.h; the planner's schedules are valid, deterministic and replay to the widths
+an independent implementation (the oracle's line graph) computes; error paths."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2012_02430_b200 as T
+from paper_2012_02430_b200 import _binding as B
+from oracle import contract, network
+from tn_inputs import qaoa_angles, random_regular_graph
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tn_b200.h")).read()
+    decl = set(re.findall(r"^(?:tn_status|void|const char\*|int32_t)\s+(tn_[a-z_]+)\(", hdr, re.M))
+    assert decl == set(B.SYMBOLS), decl ^ set(B.SYMBOLS)
+    lib = ctypes.CDLL(B.LIB_PATH)
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert B.tn_version() >= 1
+
+
+def _replay(tensors, prefix, sliced, residual):
+    """Degrees of the executed steps by an independent replay (oracle line graph)."""
+    adj = contract.line_graph(tensors)
+    degs = []
+    for v in prefix:
+        degs.append(len(adj[v]))
+        contract.eliminate_vertex(adj, v)
+    for v in sliced:                       # slicing removes the vertex
+        for a in adj.pop(v, set()):
+            adj[a].discard(v)
+    for v in residual:
+        degs.append(len(adj[v]))
+        contract.eliminate_vertex(adj, v)
+    return degs
+
+
+@pytest.mark.parametrize("n,p,k,orderer", [(20, 1, 0, "min-degree"), (30, 2, 3, "min-fill"),
+                                           (40, 1, 4, "min-degree"), (24, 3, 2, "min-fill"),
+                                           (100, 1, 6, "min-fill")])
+def test_schedule_partition_and_width_replay(n, p, k, orderer):
+    g = random_regular_graph(n, 3, n)
+    ga, be = qaoa_angles(p, n)
+    plan = T.build_plan(g, p, "amplitude", orderer, n_sliced=k)
+    pre, sl, res, degs = plan.schedule()
+    assert len(sl) == k == plan.info["k"] and sl == sorted(sl)
+    labels = set(range(n * p))
+    assert set(pre) | set(sl) | set(res) == labels
+    assert len(pre) + len(sl) + len(res) == len(labels)
+    tens = network.qaoa_amplitude_network(n, g.edges, ga, be)
+    assert set(network.live_labels(tens)) == labels          # label rule l*N+q (reading A6)
+    rep = _replay(tens, pre, sl, res)
+    assert rep == degs
+    assert max(degs) == plan.width
+    assert plan.info["slice_step"] == len(pre)
+
+
+def test_min_degree_matches_independent_greedy():
+    # the planner's unsliced min-degree order == the oracle's own greedy (same tie rule)
+    for n, p in ((16, 1), (20, 2), (30, 3)):
+        g = random_regular_graph(n, 3, 3)
+        ga, be = qaoa_angles(p, 3)
+        plan = T.build_plan(g, p, "amplitude", "min-degree")
+        _, _, res, degs = plan.schedule()
+        order, odeg = contract.greedy_min_degree(network.qaoa_amplitude_network(n, g.edges, ga, be))
+        assert res == order and degs == odeg
+
+
+def test_plan_deterministic_and_reloadable():
+    g = random_regular_graph(60, 3, 2)
+    b1 = B.tn_plan_build(g.n, g.edges, 2, n_sliced=3)
+    b2 = B.tn_plan_build(g.n, g.edges, 2, n_sliced=3)
+    assert b1 == b2
+    h = B.tn_plan_load(b1)
+    assert B.tn_plan_info(h)["k"] == 3
+    B.tn_plan_free(h)
+
+
+def test_slicing_reduces_width_paper_section_5_3():
+    # PAPER.md:569 "n=1 already provides contraction width reduction by 3" (reported; we
+    # assert a reduction by >= 1 and monotone non-increase in n on this instance)
+    g = random_regular_graph(100, 3, 0)
+    widths = []
+    for k in range(0, 5):
+        widths.append(T.build_plan(g, 1, "amplitude", "min-degree", n_sliced=k).width)
+    assert widths[1] <= widths[0] - 1
+    assert all(b <= a for a, b in zip(widths, widths[1:]))
+
+
+def test_literal_p3_n210_is_rejected():
+    # p=3 at N=210 has width ~127 -> TN_E_TOO_WIDE, never a silent attempt
+    g = random_regular_graph(210, 3, 0)
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_build(g.n, g.edges, 3, n_sliced=0, max_width=32)
+    assert ei.value.name == "TN_E_TOO_WIDE"
+    assert "width" in str(ei.value)
+
+
+def test_error_paths():
+    g = random_regular_graph(10, 3, 0)
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_build(10, g.edges, 0)
+    assert ei.value.name == "TN_E_INVAL"
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_build(10, [(0, 0)] + list(g.edges[1:]), 1)
+    assert ei.value.name == "TN_E_PLAN"
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_build(10, list(g.edges) + [g.edges[0]], 1)
+    assert ei.value.name == "TN_E_PLAN"
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_build(10, g.edges, 1, n_sliced=99)
+    assert ei.value.name == "TN_E_INVAL"
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_build(10, g.edges, 1, orderer=7)
+    assert ei.value.name == "TN_E_INVAL"
+    buf = bytearray(B.tn_plan_build(10, g.edges, 1))
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_load(bytes(buf[:40]))
+    assert ei.value.name == "TN_E_PLAN"
+    buf[0] ^= 0xFF
+    with pytest.raises(B.TnError) as ei:
+        B.tn_plan_load(bytes(buf))
+    assert ei.value.name == "TN_E_PLAN"
+
+
+def test_sum_partials_fixed_tree_matches_oracle():
+    g = random_regular_graph(40, 3, 1)
+    plan = T.build_plan(g, 1, "amplitude", "min-fill", n_sliced=5)
+    rng = np.random.default_rng(0)
+    vals = rng.normal(size=2 * plan.n_slices) * np.exp(rng.uniform(-30, 30, size=2 * plan.n_slices))
+    got = plan.sum_partials(vals.tolist())
+    ref = contract.pairwise_sum([complex(vals[2 * j], vals[2 * j + 1]) for j in range(plan.n_slices)])
+    assert got == ref   # bit-identical: same fixed pairwise tree
+
+
+def test_energy_plan_shape():
+    g = random_regular_graph(100, 3, 0)
+    plan = T.build_plan(g, 3, "energy", "min-fill")
+    assert plan.info["n_programs"] == len(g.edges) == 150
+    assert plan.info["k"] == 0
+    assert 7 <= plan.width <= 16            # cone widths 7-13 (instance-dependent)
+
+
+def test_workspace_and_bytes_model():
+    g = random_regular_graph(56, 3, 0)
+    plan = T.build_plan(g, 2, "amplitude", "min-fill")
+    info = plan.info
+    assert info["workspace_bytes"][0] >= 8 * 2 ** plan.width
+    assert info["workspace_bytes"][1] >= 16 * 2 ** plan.width
+    assert math.isclose(info["pred_bytes_per_slice"][1], 2 * info["pred_bytes_per_slice"][0])
