@@ -103,6 +103,23 @@ tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* out);
 tn_status tn_plan_schedule(const tn_plan* plan, int32_t* prefix, int32_t* sliced, int32_t* residual,
                            int32_t* degrees);
 
+/* Per-step description of the lowered bucket program (Fig. contract_cost: the
+ * cost of every elimination step).  out: host array of cap records; *n = number of steps. */
+typedef struct {
+  int32_t phase;          /* 0: shared prefix (run once), 1: per slice */
+  int32_t label;          /* eliminated index */
+  int32_t out_rank;       /* bits of the output in this phase */
+  int32_t degree;         /* N_{G_i}(v_i): indices of the output incl. sliced ones in phase 0 */
+  int32_t n_in;
+  int32_t inplace;        /* output aliases the first input's lower half */
+  int32_t standalone;     /* 1: own k_bucket launch; 0: inside an interpreter run */
+  int32_t in_rank[8];     /* bits of each input read per slice */
+  uint64_t in_out_mask[8];
+  int32_t in_pv[8];
+  double bytes_c64;       /* algorithmic bytes (inputs + output) at complex64 */
+} tn_step_info_t;
+tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int64_t cap, int64_t* n);
+
 /* ---------------------------------------------------------------- contraction (device) */
 /* Unsliced amplitude (sliced plans: all 2^k slices summed locally).  gamma, beta: host double[p].
  * ws: device buffer of >= workspace_bytes[dtype] bytes (e.g. torch.empty).  stream: cudaStream_t

@@ -52,6 +52,10 @@ class Plan:
         """(prefix, sliced, residual, degrees) label lists (tn_plan_schedule)."""
         return B.tn_plan_schedule(self.handle)
 
+    def steps(self):
+        """Per-step records (tn_plan_steps): the Fig. contract_cost profile of the plan."""
+        return B.tn_plan_steps(self.handle)
+
     def workspace_bytes(self, dtype: int) -> int:
         return int(self.info["workspace_bytes"][dtype])
 

@@ -24,7 +24,7 @@ STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4
           -5: "TN_E_CUDA", -6: "TN_E_DTYPE"}
 
 SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_plan_load", "tn_plan_free", "tn_plan_info",
-           "tn_plan_schedule", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy",
+           "tn_plan_schedule", "tn_plan_steps", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy",
            "tn_eliminate", "tn_profile_enable", "tn_profile_read", "tn_last_error", "tn_version"]
 
 
@@ -58,6 +58,13 @@ class tn_plan_info_t(C.Structure):
         return d
 
 
+class tn_step_info_t(C.Structure):
+    _fields_ = [("phase", C.c_int32), ("label", C.c_int32), ("out_rank", C.c_int32), ("degree", C.c_int32),
+                ("n_in", C.c_int32), ("inplace", C.c_int32), ("standalone", C.c_int32),
+                ("in_rank", C.c_int32 * 8), ("in_out_mask", C.c_uint64 * 8), ("in_pv", C.c_int32 * 8),
+                ("bytes_c64", C.c_double)]
+
+
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _lib.tn_plan_build.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
@@ -70,6 +77,7 @@ _lib.tn_plan_free.restype = None
 _lib.tn_plan_info.argtypes = [_P, C.POINTER(tn_plan_info_t)]
 _I32P = C.POINTER(C.c_int32)
 _lib.tn_plan_schedule.argtypes = [_P, _I32P, _I32P, _I32P, _I32P]
+_lib.tn_plan_steps.argtypes = [_P, C.POINTER(tn_step_info_t), C.c_int64, C.POINTER(C.c_int64)]
 _lib.tn_contract.argtypes = [_P, C.c_int, _D, _D, C.c_int32, _P, C.c_size_t, _P, _D]
 _lib.tn_contract_sliced.argtypes = [_P, C.c_int, _D, _D, C.c_int32, C.c_uint64, C.c_uint64, _P,
                                     C.c_size_t, _P, _P]
@@ -147,6 +155,22 @@ def tn_plan_schedule(h: int):
     deg = (C.c_int32 * max(1, nd))()
     _check(_lib.tn_plan_schedule(h, pre, sl, res, deg), "tn_plan_schedule")
     return list(pre)[:s], list(sl)[:k], list(res)[:L - s - k], list(deg)[:nd]
+
+
+def tn_plan_steps(h: int):
+    n = C.c_int64()
+    _check(_lib.tn_plan_steps(h, None, 0, C.byref(n)), "tn_plan_steps")
+    arr = (tn_step_info_t * max(1, n.value))()
+    _check(_lib.tn_plan_steps(h, arr, n.value, C.byref(n)), "tn_plan_steps")
+    out = []
+    for i in range(n.value):
+        s = arr[i]
+        k = s.n_in
+        out.append({"phase": s.phase, "label": s.label, "out_rank": s.out_rank, "degree": s.degree,
+                    "n_in": k, "inplace": s.inplace, "standalone": s.standalone,
+                    "in_rank": list(s.in_rank)[:k], "in_out_mask": list(s.in_out_mask)[:k],
+                    "in_pv": list(s.in_pv)[:k], "bytes_c64": s.bytes_c64})
+    return out
 
 
 def tn_contract(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, stream: int) -> complex:

@@ -338,6 +338,35 @@ extern "C" tn_status tn_plan_schedule(const tn_plan* plan, int32_t* prefix, int3
   return TN_OK;
 }
 
+extern "C" tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int64_t cap, int64_t* n) {
+  if (!plan || !n) return fail(TN_E_INVAL, "tn_plan_steps: null argument");
+  *n = (int64_t)plan->steps.size();
+  std::vector<char> big(plan->steps.size(), 0);
+  for (const auto& op : plan->ops)
+    if (op.type == OP_BIG) big[op.begin] = 1;
+  for (int64_t i = 0; out && i < cap && i < *n; ++i) {
+    const StepRec& s = plan->steps[i];
+    tn_step_info_t& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    o.phase = s.phase;
+    o.label = s.label;
+    o.out_rank = s.out_rank;
+    o.degree = s.degree;
+    o.n_in = s.n_in;
+    o.inplace = s.inplace;
+    o.standalone = big[i];
+    double el = std::ldexp(1.0, s.out_rank);
+    for (int t = 0; t < s.n_in; ++t) {
+      o.in_rank[t] = (int32_t)s.in[t].rank;
+      o.in_out_mask[t] = s.in[t].out_mask;
+      o.in_pv[t] = (int32_t)s.in[t].pv;
+      el += std::ldexp(1.0, (int)s.in[t].rank);
+    }
+    o.bytes_c64 = 8.0 * el;
+  }
+  return TN_OK;
+}
+
 extern "C" tn_status tn_sum_partials(const tn_plan* plan, const double* partials, double out[2]) {
   if (!plan || !partials || !out) return fail(TN_E_INVAL, "tn_sum_partials: null argument");
   const uint64_t n = 1ull << plan->h.k;
@@ -640,7 +669,8 @@ extern "C" tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* cons
     a.in[t] = in_dev[t];
     a.out_mask[t] = out_mask[t];
     a.pv[t] = (uint32_t)pv[t];
-    a.flags[t] = 0;
+    const int r_in = __builtin_popcountll(out_mask[t]) + 1;
+    a.flags[t] = (r_in + 2 >= out_rank && out_rank >= 16) ? 1u : 0u;  // as the lowering
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (out_rank == 0) {
