@@ -274,11 +274,12 @@ def main():
     achieved = (kb_bytes / (kb_ms / 1e3)) / 1e9 if kb_ms > 0 else 0.0
     gpu_launches = prof["all_launches"]
     algo_bytes_step = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
-    traffic = None
+    traffic, traffic_ratio = None, None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and prof["launches"]:
         try:
-            traffic = json.load(open(tr_path)).get("bytes_per_algorithmic_byte")
+            traffic_ratio = json.load(open(tr_path)).get("bytes_per_algorithmic_byte")
+            traffic = traffic_ratio * kb_bytes / prof["launches"]   # DRAM bytes per launch
         except Exception:
             traffic = None
 
@@ -312,6 +313,8 @@ def main():
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "traffic_per_algorithmic_byte": traffic_ratio,
+                     "algorithmic_bytes_per_launch": kb_bytes / prof["launches"] if prof["launches"] else None,
                      "kernel": "k_bucket (standalone bucket steps)", "peak_source": peak_src,
                      "kernel_share_of_step": (kb_ms / args.steps) / ms_step if ms_step else None,
                      "launches": prof["launches"]},

@@ -112,7 +112,8 @@ typedef struct {
   int32_t degree;         /* N_{G_i}(v_i): indices of the output incl. sliced ones in phase 0 */
   int32_t n_in;
   int32_t inplace;        /* output aliases the first input's lower half */
-  int32_t standalone;     /* 1: own k_bucket launch; 0: inside an interpreter run */
+  int32_t standalone;     /* 1: own k_bucket launch; 2: part of a fused reduce chain (k_chain);
+                             0: inside an interpreter run */
   int32_t in_rank[8];     /* bits of each input read per slice */
   uint64_t in_out_mask[8];
   int32_t in_pv[8];

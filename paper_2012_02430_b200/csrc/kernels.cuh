@@ -138,66 +138,122 @@ __device__ __forceinline__ float4 ld_in4(const float4* p, bool stream) {
 constexpr int kBucketThreads = 256;
 constexpr int kBucketIters = 8;
 
-template <typename T, int NIN>
+template <typename T> struct TileBits;
+template <> struct TileBits<float2> { static constexpr int v = 12; };   // 256 thr x 2 elem x 8 it
+template <> struct TileBits<double2> { static constexpr int v = 11; };  // 256 thr x 1 elem x 8 it
+
+// Input access modes (uniform per launch):
+//   CONST: F_t has no bit inside a tile -> the two values (x = 0, 1) are loaded once per tile and
+//          pre-multiplied into the tile constants C0, C1
+//   VEC:   the input holds the output's bit 0 at its bit 0 -> 16-byte vector loads (c64)
+//   BCAST: the input lacks output bit 0 -> one load serves both elements of a pair (c64)
+//   PAIR:  output bit 0 sits elsewhere in the input -> two scalar loads (c64)
+enum : uint32_t { M_CONST = 0, M_VEC = 1, M_BCAST = 2, M_PAIR = 3 };
+
+// OffT = uint32_t when every input has <= 32 bits (element offsets < 2^32), else uint64_t.
+template <typename T, int NIN, typename OffT>
 __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
   constexpr int VEC = VecT<T>::n;
-  constexpr int STRIDE = kBucketThreads * VEC;           // elements per iteration of a CTA
-  constexpr int TILE = STRIDE * kBucketIters;            // elements per tile
+  constexpr int TB = TileBits<T>::v;
+  constexpr int STRIDE = kBucketThreads * VEC;
+  constexpr uint64_t TILE = 1ull << TB;
+  constexpr int NB = 64 - TB;
   const uint64_t n_out = 1ull << a.out_rank;
-  const uint64_t n_tiles = (n_out + TILE - 1) / TILE;
+  const uint64_t n_tiles = (n_out + TILE - 1) >> TB;
   const uint32_t tid = threadIdx.x;
 
-  __shared__ uint64_t kofs[NIN][kBucketIters];
+  __shared__ OffT kofs[NIN][kBucketIters];
+  __shared__ OffT fbit[NIN][NB];
+  __shared__ OffT fcum[NIN][NB + 1];
   if (tid < NIN * kBucketIters) {
     const int t = tid / kBucketIters, kk = tid % kBucketIters;
-    kofs[t][kk] = fmap((uint64_t)kk * STRIDE, a.out_mask[t], a.pv[t]);
+    kofs[t][kk] = (OffT)fmap((uint64_t)kk * STRIDE, a.out_mask[t], a.pv[t]);
   }
-  uint64_t thr[NIN], S[NIN], step1[NIN];
-  const T* in[NIN];
+  for (int i = tid; i < NIN * NB; i += kBucketThreads) {
+    const int t = i / NB, b = i % NB;
+    fbit[t][b] = (OffT)fmap(1ull << (TB + b), a.out_mask[t], a.pv[t]);
+  }
+  __syncthreads();
+  if (tid < NIN) {
+    OffT c = 0;
+    fcum[tid][0] = 0;
+    for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+  }
+  // this CTA's contiguous range of tiles
+  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+
+  OffT thr[NIN], S[NIN], cur[NIN];
+  uint32_t mode[NIN];
   bool strm[NIN];
+  const T* in[NIN];
+  const uint64_t inner = TILE - 1;
 #pragma unroll
   for (int t = 0; t < NIN; ++t) {
     in[t] = static_cast<const T*>(a.in[t]);
-    thr[t] = fmap((uint64_t)tid * VEC, a.out_mask[t], a.pv[t]);
-    S[t] = 1ull << a.pv[t];
-    step1[t] = fmap(1, a.out_mask[t], a.pv[t]);   // offset of the next output element (VEC = 2)
+    thr[t] = (OffT)fmap((uint64_t)tid * VEC, a.out_mask[t], a.pv[t]);
+    S[t] = (OffT)1 << a.pv[t];
+    const uint64_t s1 = fmap(1, a.out_mask[t], a.pv[t]);
+    mode[t] = ((a.out_mask[t] & inner) == 0) ? M_CONST
+              : (VEC == 1 || s1 == 1)        ? M_VEC
+              : (s1 == 0)                    ? M_BCAST
+                                             : M_PAIR;
     strm[t] = (a.flags[t] & 1u) != 0;
+    cur[t] = (OffT)fmap(t0 << TB, a.out_mask[t], a.pv[t]);
   }
+  OffT s1v[NIN];
+#pragma unroll
+  for (int t = 0; t < NIN; ++t) s1v[t] = (OffT)fmap(1, a.out_mask[t], a.pv[t]);
   T* out = static_cast<T*>(a.out);
   __syncthreads();
 
-  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const uint64_t base = tile * TILE;
-    uint64_t tb[NIN];
+  for (uint64_t tile = t0; tile < t1; ++tile) {
+    const uint64_t base = tile << TB;
+    // tile constants: product of the CONST inputs for x = 0 and x = 1
+    T C0 = cfrom<T>(1.0, 0.0), C1 = cfrom<T>(1.0, 0.0);
+    bool has_c = false;
 #pragma unroll
-    for (int t = 0; t < NIN; ++t) tb[t] = fmap(base, a.out_mask[t], a.pv[t]) + thr[t];
+    for (int t = 0; t < NIN; ++t) {
+      if (mode[t] == M_CONST) {
+        const T c0 = __ldg(in[t] + cur[t]);
+        const T c1 = __ldg(in[t] + cur[t] + S[t]);
+        if (!has_c) { C0 = c0; C1 = c1; has_c = true; }
+        else { C0 = cmul(C0, c0); C1 = cmul(C1, c1); }
+      }
+    }
 #pragma unroll 2
     for (int kk = 0; kk < kBucketIters; ++kk) {
       const uint64_t o = base + (uint64_t)kk * STRIDE + (uint64_t)tid * VEC;
       if (o >= n_out) break;
       if constexpr (VEC == 2) {
         float2 p0[2], p1[2];
+        bool first = !has_c;
+        p0[0] = p0[1] = reinterpret_cast<const float2&>(C0);
+        p1[0] = p1[1] = reinterpret_cast<const float2&>(C1);
 #pragma unroll
         for (int t = 0; t < NIN; ++t) {
-          const uint64_t off = tb[t] + kofs[t][kk];
+          if (mode[t] == M_CONST) continue;
+          const OffT off = cur[t] + thr[t] + kofs[t][kk];
           const float2* pt = reinterpret_cast<const float2*>(in[t]);
           float2 x0[2], x1[2];
-          if (step1[t] == 1) {
+          if (mode[t] == M_VEC) {
             const float4 u0 = ld_in4(reinterpret_cast<const float4*>(pt + off), strm[t]);
             const float4 u1 = ld_in4(reinterpret_cast<const float4*>(pt + off + S[t]), strm[t]);
             x0[0] = make_float2(u0.x, u0.y); x0[1] = make_float2(u0.z, u0.w);
             x1[0] = make_float2(u1.x, u1.y); x1[1] = make_float2(u1.z, u1.w);
-          } else if (step1[t] == 0) {
+          } else if (mode[t] == M_BCAST) {
             x0[0] = x0[1] = ld_in(pt + off, strm[t]);
             x1[0] = x1[1] = ld_in(pt + off + S[t], strm[t]);
           } else {
             x0[0] = ld_in(pt + off, strm[t]);
-            x0[1] = ld_in(pt + off + step1[t], strm[t]);
+            x0[1] = ld_in(pt + off + s1v[t], strm[t]);
             x1[0] = ld_in(pt + off + S[t], strm[t]);
-            x1[1] = ld_in(pt + off + step1[t] + S[t], strm[t]);
+            x1[1] = ld_in(pt + off + s1v[t] + S[t], strm[t]);
           }
-          if (t == 0) {
+          if (first) {
             p0[0] = x0[0]; p0[1] = x0[1]; p1[0] = x1[0]; p1[1] = x1[1];
+            first = false;
           } else {
             p0[0] = cmul(p0[0], x0[0]); p0[1] = cmul(p0[1], x0[1]);
             p1[0] = cmul(p1[0], x1[0]); p1[1] = cmul(p1[1], x1[1]);
@@ -206,17 +262,76 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
         const float2 r0 = cadd(p0[0], p1[0]), r1 = cadd(p0[1], p1[1]);
         __stcs(reinterpret_cast<float4*>(out + o), make_float4(r0.x, r0.y, r1.x, r1.y));
       } else {
-        T p0, p1;
+        T p0 = C0, p1 = C1;
+        bool first = !has_c;
 #pragma unroll
         for (int t = 0; t < NIN; ++t) {
-          const uint64_t off = tb[t] + kofs[t][kk];
+          if (mode[t] == M_CONST) continue;
+          const OffT off = cur[t] + thr[t] + kofs[t][kk];
           const T x0 = ld_in(in[t] + off, strm[t]);
           const T x1 = ld_in(in[t] + off + S[t], strm[t]);
-          if (t == 0) { p0 = x0; p1 = x1; }
+          if (first) { p0 = x0; p1 = x1; first = false; }
           else { p0 = cmul(p0, x0); p1 = cmul(p1, x1); }
         }
         __stcs(out + o, cadd(p0, p1));
       }
+    }
+    // next tile: tile -> tile + 1 clears the r trailing ones and sets bit r
+    const int r = __ffsll((long long)~tile) - 1;
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) cur[t] = cur[t] + fbit[t][r] - fcum[t][r];
+  }
+}
+
+// ------------------------------------------------------------------ fused reduce chain
+// m consecutive reduce steps eliminate the top m bits of A; the weights of step i are rank-1 on
+// its summed index.  Re-associated (exact): out[o] = sum_x W[x] A[o + x n_out], W[x] =
+// prod_i w_i[bit_{m-1-i}(x)].  A is read once (streaming), out written once; may alias A.
+struct ChainArgs {
+  void* out;
+  const void* A;
+  const void* w[kMaxChain][kMaxChainW];
+  int32_t nw[kMaxChain];
+  int32_t m;
+  int32_t out_rank;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBucketThreads) k_chain(const ChainArgs a) {
+  constexpr int VEC = VecT<T>::n;
+  __shared__ T W[1 << kMaxChain];
+  const int nx = 1 << a.m;
+  for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+    T acc = cfrom<T>(1.0, 0.0);
+    for (int i = 0; i < a.m; ++i) {
+      const int b = (x >> (a.m - 1 - i)) & 1;
+      for (int k = 0; k < a.nw[i]; ++k) acc = cmul(acc, static_cast<const T*>(a.w[i][k])[b]);
+    }
+    W[x] = acc;
+  }
+  __syncthreads();
+  const uint64_t n_out = 1ull << a.out_rank;
+  const T* A = static_cast<const T*>(a.A);
+  T* out = static_cast<T*>(a.out);
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * VEC;
+  for (uint64_t o = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC; o < n_out; o += step) {
+    if constexpr (VEC == 2) {
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int x = 0; x < nx; ++x) {
+        const float4 u = __ldcs(reinterpret_cast<const float4*>(A + o + (uint64_t)x * n_out));
+        const float2 w = reinterpret_cast<const float2&>(W[x]);
+        acc0.x = fmaf(w.x, u.x, fmaf(-w.y, u.y, acc0.x));
+        acc0.y = fmaf(w.x, u.y, fmaf(w.y, u.x, acc0.y));
+        acc1.x = fmaf(w.x, u.z, fmaf(-w.y, u.w, acc1.x));
+        acc1.y = fmaf(w.x, u.w, fmaf(w.y, u.z, acc1.y));
+      }
+      __stcs(reinterpret_cast<float4*>(out + o), make_float4(acc0.x, acc0.y, acc1.x, acc1.y));
+    } else {
+      T acc = cfrom<T>(0.0, 0.0);
+#pragma unroll 4
+      for (int x = 0; x < nx; ++x) acc = cadd(acc, cmul(W[x], __ldcs(A + o + (uint64_t)x * n_out)));
+      __stcs(out + o, acc);
     }
   }
 }

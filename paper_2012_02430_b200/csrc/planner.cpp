@@ -677,6 +677,60 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       i = j;
     }
   }
+  // ---- fusion of reduce chains (phase B): step i is a chain head if its first input holds
+  // every output bit with the summed bit on top and its other inputs are rank-1 weights on the
+  // summed index; step i+1 extends the chain if it is the in-place reduce of step i's output.
+  {
+    auto is_reduce = [&](const StepRec& st) {
+      if (st.out_rank < 1 || st.n_in - 1 > kMaxChainW) return false;
+      const uint64_t full = (1ull << st.out_rank) - 1;
+      if (st.in[0].out_mask != full || st.in[0].pv != (uint32_t)st.out_rank ||
+          st.in[0].rank != (uint32_t)st.out_rank + 1)
+        return false;
+      for (int t = 1; t < st.n_in; ++t)
+        if (st.in[t].out_mask != 0 || st.in[t].rank != 1) return false;
+      return true;
+    };
+    std::vector<OpRec> fused;
+    for (size_t oi = 0; oi < out.ops.size(); ++oi) {
+      const OpRec& op = out.ops[oi];
+      if (op.phase != 1 || op.type != OP_BIG || !is_reduce(out.steps[op.begin])) {
+        fused.push_back(op);
+        continue;
+      }
+      size_t oj = oi + 1;
+      int end = op.begin + 1;
+      while (oj < out.ops.size() && (end - op.begin) < kMaxChain) {
+        const OpRec& nx = out.ops[oj];
+        if (nx.phase != 1 || nx.type != OP_BIG || nx.begin != end) break;
+        const StepRec& st = out.steps[nx.begin];
+        const StepRec& pv = out.steps[end - 1];
+        if (!st.inplace || !is_reduce(st) || st.in[0].off != pv.out_off || st.out_rank < 1) break;
+        ++end;
+        ++oj;
+      }
+      if (end - op.begin >= 2) {
+        const int m = end - op.begin;
+        const StepRec& h = out.steps[op.begin];
+        double unf = 0.0;
+        for (int k = op.begin; k < end; ++k) {
+          const StepRec& sk = out.steps[k];
+          unf += std::ldexp(1.0, sk.out_rank);
+          for (int t = 0; t < sk.n_in; ++t) unf += std::ldexp(1.0, (int)sk.in[t].rank);
+        }
+        double fz = std::ldexp(1.0, (int)h.in[0].rank) + std::ldexp(1.0, (int)h.in[0].rank - m);
+        for (int k = op.begin; k < end; ++k) fz += 2.0 * (out.steps[k].n_in - 1);
+        out.elems_slice += fz - unf;
+        out.elems_big_slice += fz - unf;
+        out.big_launches_slice -= (uint64_t)(m - 1);
+        fused.push_back(OpRec{OP_CHAIN, op.begin, end, 1});
+        oi = oj - 1;
+      } else {
+        fused.push_back(op);
+      }
+    }
+    out.ops.swap(fused);
+  }
   for (auto& op : out.ops) (op.phase == 0 ? out.launches_prefix : out.launches_slice)++;
   out.launches_slice += 1;  // per-slice finalize
   ProgramRec& pr = out.prog;

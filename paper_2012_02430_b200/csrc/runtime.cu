@@ -280,7 +280,9 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
     }
   }
   for (const auto& o : pl->ops)
-    if (o.begin < 0 || o.end > h.n_steps || o.begin >= o.end || (o.type != OP_BIG && o.type != OP_RUN) ||
+    if (o.begin < 0 || o.end > h.n_steps || o.begin >= o.end ||
+        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN) ||
+        (o.type == OP_CHAIN && (o.end - o.begin > kMaxChain || pl->steps[o.end - 1].out_rank < 1)) ||
         (o.type == OP_BIG && pl->steps[o.begin].out_rank < 1))
       return fail(TN_E_PLAN, "tn_plan_load: bad op record");
   for (const auto& s : pl->scalars)
@@ -343,7 +345,8 @@ extern "C" tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int
   *n = (int64_t)plan->steps.size();
   std::vector<char> big(plan->steps.size(), 0);
   for (const auto& op : plan->ops)
-    if (op.type == OP_BIG) big[op.begin] = 1;
+    if (op.type == OP_BIG || op.type == OP_CHAIN)
+      for (int i = op.begin; i < op.end; ++i) big[i] = op.type == OP_BIG ? 1 : 2;
   for (int64_t i = 0; out && i < cap && i < *n; ++i) {
     const StepRec& s = plan->steps[i];
     tn_step_info_t& o = out[i];
@@ -440,13 +443,17 @@ uint64_t host_pext(uint64_t x, uint64_t m) {
 
 template <typename T, int NIN>
 void launch_bucket_n(const BigArgs& a, cudaStream_t st) {
-  constexpr int VEC = VecT<T>::n;
-  constexpr uint64_t TILE = (uint64_t)kBucketThreads * VEC * kBucketIters;
+  constexpr uint64_t TILE = 1ull << TileBits<T>::v;
   const uint64_t n_out = 1ull << a.out_rank;
   const uint64_t tiles = (n_out + TILE - 1) / TILE;
-  const uint64_t cap = (uint64_t)num_sms() * 8;
+  const uint64_t cap = (uint64_t)num_sms() * 4;
   const unsigned grid = (unsigned)std::min<uint64_t>(tiles, cap);
-  k_bucket<T, NIN><<<grid, kBucketThreads, 0, st>>>(a);
+  bool wide = false;   // any input with more than 32 bits -> 64-bit offsets
+  for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
+  if (wide)
+    k_bucket<T, NIN, uint64_t><<<grid, kBucketThreads, 0, st>>>(a);
+  else
+    k_bucket<T, NIN, uint32_t><<<grid, kBucketThreads, 0, st>>>(a);
 }
 
 template <typename T>
@@ -504,6 +511,40 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         cudaEventRecord(pr.a, st);
       }
       launch_bucket<T>(a, st);
+      if (pl->profiling) {
+        cudaEventRecord(pr.b, st);
+        pl->prof.push_back(pr);
+      }
+    } else if (op.type == OP_CHAIN) {
+      const StepRec& h = pl->steps[op.begin];
+      const StepRec& last = pl->steps[op.end - 1];
+      ChainArgs c;
+      std::memset(&c, 0, sizeof(c));
+      c.m = op.end - op.begin;
+      c.out = ws + last.out_off;
+      c.out_rank = last.out_rank;
+      auto soff = [&](const InRec& in) {
+        return in.slice_mask ? (host_pext(j, in.slice_mask) << in.rank) : 0ull;
+      };
+      c.A = ws + h.in[0].off + soff(h.in[0]);
+      for (int i = 0; i < c.m; ++i) {
+        const StepRec& sk = pl->steps[op.begin + i];
+        c.nw[i] = sk.n_in - 1;
+        for (int k = 1; k < sk.n_in; ++k) c.w[i][k - 1] = ws + sk.in[k].off + soff(sk.in[k]);
+      }
+      const double bytes = (std::ldexp(1.0, (int)h.in[0].rank) + std::ldexp(1.0, c.out_rank)) * sizeof(T);
+      ProfRec pr{};
+      if (pl->profiling) {
+        pr.a = pool_event(pl);
+        pr.b = pool_event(pl);
+        pr.bytes = bytes;
+        cudaEventRecord(pr.a, st);
+      }
+      constexpr int VEC = VecT<T>::n;
+      const uint64_t work = ((1ull << c.out_rank) + VEC - 1) / VEC;
+      const uint64_t blocks = (work + kBucketThreads - 1) / kBucketThreads;
+      const unsigned grid = (unsigned)std::min<uint64_t>(blocks, (uint64_t)num_sms() * 8);
+      k_chain<T><<<grid, kBucketThreads, 0, st>>>(c);
       if (pl->profiling) {
         cudaEventRecord(pr.b, st);
         pl->prof.push_back(pr);

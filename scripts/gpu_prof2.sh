@@ -1,0 +1,6 @@
+set -x; mkdir -p gpurun_out
+export PATH=/usr/local/cuda/bin:$PATH
+python scripts/profile_c5a.py > gpurun_out/prof_plain.log 2>&1; echo "plain exit $?"
+SKIP=$(python scripts/profile_c5a.py --print-skip 164)
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_bucket -s $SKIP -c 2 -o gpurun_out/prof_c5a_v2 python scripts/profile_c5a.py > gpurun_out/ncu_full_v2.log 2>&1; echo "ncu full exit $?"
+tail -3 gpurun_out/ncu_full_v2.log
