@@ -166,6 +166,16 @@ tn_status tn_profile_enable(tn_plan* plan, int32_t enable);
 tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms, double* total_bytes,
                           uint64_t* all_launches);
 
+/* The per-launch records behind tn_profile_read (call it BEFORE tn_profile_read, which clears
+ * them): one record per standalone launch (k_bucket / k_chain) with its plan step range, kind
+ * (1 = k_bucket, 2 = k_chain), device milliseconds and algorithmic bytes.  out: host array of cap
+ * records (may be NULL to query *n). */
+typedef struct {
+  int32_t step_begin, step_end, kind, out_rank;
+  double ms, bytes;
+} tn_prof_record_t;
+tn_status tn_profile_records(tn_plan* plan, tn_prof_record_t* out, int64_t cap, int64_t* n);
+
 const char* tn_last_error(void);
 int32_t tn_version(void);
 

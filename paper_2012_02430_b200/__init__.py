@@ -103,6 +103,10 @@ class Plan:
     def profile_read(self):
         return B.tn_profile_read(self.handle)
 
+    def profile_records(self):
+        """Per-launch (step range, kernel, ms, algorithmic bytes); call before profile_read()."""
+        return B.tn_profile_records(self.handle)
+
 
 def build_plan(graph, p: int, kind: str = "amplitude", orderer: str = "min-fill", n_sliced: int = 0,
                r: int = 0, max_width: int = 0, small_log2: int = -1) -> Plan:

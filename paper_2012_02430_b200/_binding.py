@@ -25,7 +25,7 @@ STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4
 
 SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_plan_load", "tn_plan_free", "tn_plan_info",
            "tn_plan_schedule", "tn_plan_steps", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy",
-           "tn_eliminate", "tn_profile_enable", "tn_profile_read", "tn_last_error", "tn_version"]
+           "tn_eliminate", "tn_profile_enable", "tn_profile_read", "tn_profile_records", "tn_last_error", "tn_version"]
 
 
 class TnError(RuntimeError):
@@ -65,6 +65,11 @@ class tn_step_info_t(C.Structure):
                 ("bytes_c64", C.c_double)]
 
 
+class tn_prof_record_t(C.Structure):
+    _fields_ = [("step_begin", C.c_int32), ("step_end", C.c_int32), ("kind", C.c_int32),
+                ("out_rank", C.c_int32), ("ms", C.c_double), ("bytes", C.c_double)]
+
+
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _lib.tn_plan_build.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
@@ -87,6 +92,7 @@ _lib.tn_eliminate.argtypes = [C.c_int, C.c_int32, C.POINTER(_P), C.POINTER(C.c_u
                               C.c_int32, _P]
 _lib.tn_profile_enable.argtypes = [_P, C.c_int32]
 _lib.tn_profile_read.argtypes = [_P, C.POINTER(C.c_uint64), _D, _D, C.POINTER(C.c_uint64)]
+_lib.tn_profile_records.argtypes = [_P, C.POINTER(tn_prof_record_t), C.c_int64, C.POINTER(C.c_int64)]
 _lib.tn_last_error.restype = C.c_char_p
 _lib.tn_version.restype = C.c_int32
 for _n in SYMBOLS:
@@ -220,3 +226,12 @@ def tn_profile_read(h: int):
     ms, by = C.c_double(), C.c_double()
     _check(_lib.tn_profile_read(h, C.byref(n), C.byref(ms), C.byref(by), C.byref(alln)), "tn_profile_read")
     return {"launches": n.value, "ms": ms.value, "bytes": by.value, "all_launches": alln.value}
+
+
+def tn_profile_records(h: int):
+    n = C.c_int64()
+    _check(_lib.tn_profile_records(h, None, 0, C.byref(n)), "tn_profile_records")
+    arr = (tn_prof_record_t * max(1, n.value))()
+    _check(_lib.tn_profile_records(h, arr, n.value, C.byref(n)), "tn_profile_records")
+    return [{"step_begin": r.step_begin, "step_end": r.step_end, "kind": ("k_bucket", "k_chain")[r.kind - 1],
+             "out_rank": r.out_rank, "ms": r.ms, "bytes": r.bytes} for r in arr[:n.value]]

@@ -119,8 +119,14 @@ struct BigArgs {
   uint64_t out_mask[kMaxIn];
   uint32_t pv[kMaxIn];
   uint32_t flags[kMaxIn];
+  uint32_t stage_off[kMaxIn];  // staged inputs: element offset of buffer 0 in dynamic smem
+  uint32_t nlow[kMaxIn];       // staged inputs: log2 of the per-tile chunk (per x)
+  uint32_t stage_elems;        // elements of one smem buffer (all staged inputs, both x)
   int32_t out_rank;
   int32_t n_in;
+  uint8_t perm[64];            // traversal order of the tile-index bits (logical bit b -> output
+                               // bit TB + perm[b]); bits absent from the big inputs go first so
+                               // tiles that share an input chunk run back to back (L2 / smem reuse)
 };
 
 template <typename T> struct VecT;
@@ -128,7 +134,7 @@ template <> struct VecT<float2> { using type = float4; static constexpr int n = 
 template <> struct VecT<double2> { using type = double2; static constexpr int n = 1; };
 
 template <typename T>
-__device__ __forceinline__ T ld_in(const T* p, bool stream) {
+__device__ __forceinline__ T ld_in(const T* p, bool stream) {  // stream: evict-first
   return stream ? __ldcs(p) : __ldg(p);
 }
 __device__ __forceinline__ float4 ld_in4(const float4* p, bool stream) {
@@ -148,7 +154,20 @@ template <> struct TileBits<double2> { static constexpr int v = 11; };  // 256 t
 //   VEC:   the input holds the output's bit 0 at its bit 0 -> 16-byte vector loads (c64)
 //   BCAST: the input lacks output bit 0 -> one load serves both elements of a pair (c64)
 //   PAIR:  output bit 0 sits elsewhere in the input -> two scalar loads (c64)
+// Orthogonally an input is STAGED (flags bit1, set by the host) when it holds only part of a
+// tile's low bits and those are its lowest positions: its per-tile chunk (two contiguous runs of
+// 2^nlow elements, x = 0 and 1) is copied into shared memory with cp.async one tile ahead
+// (double buffer) -- the reused merge operands -- instead of latency-bound direct loads.
 enum : uint32_t { M_CONST = 0, M_VEC = 1, M_BCAST = 2, M_PAIR = 3 };
+constexpr uint32_t F_STREAM = 1u, F_STAGED = 2u;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // OffT = uint32_t when every input has <= 32 bits (element offsets < 2^32), else uint64_t.
 template <typename T, int NIN, typename OffT>
@@ -161,32 +180,44 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
   const uint64_t n_out = 1ull << a.out_rank;
   const uint64_t n_tiles = (n_out + TILE - 1) >> TB;
   const uint32_t tid = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T* stage = reinterpret_cast<T*>(dsm);
 
   __shared__ OffT kofs[NIN][kBucketIters];
   __shared__ OffT fbit[NIN][NB];
   __shared__ OffT fcum[NIN][NB + 1];
+  __shared__ uint64_t pbit[NB], pcum[NB + 1];
   if (tid < NIN * kBucketIters) {
     const int t = tid / kBucketIters, kk = tid % kBucketIters;
     kofs[t][kk] = (OffT)fmap((uint64_t)kk * STRIDE, a.out_mask[t], a.pv[t]);
   }
   for (int i = tid; i < NIN * NB; i += kBucketThreads) {
     const int t = i / NB, b = i % NB;
-    fbit[t][b] = (OffT)fmap(1ull << (TB + b), a.out_mask[t], a.pv[t]);
+    fbit[t][b] = (OffT)fmap(1ull << (TB + a.perm[b]), a.out_mask[t], a.pv[t]);
   }
+  for (int b = tid; b < NB; b += kBucketThreads) pbit[b] = 1ull << a.perm[b];
   __syncthreads();
   if (tid < NIN) {
     OffT c = 0;
     fcum[tid][0] = 0;
     for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
   }
-  // this CTA's contiguous range of tiles
+  if (tid == NIN) {
+    uint64_t c = 0;
+    pcum[0] = 0;
+    for (int b = 0; b < NB; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+  }
+  // this CTA's contiguous range of LOGICAL tiles; the physical tile is the perm-deposit of it
   const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * per;
   const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t ptile = 0;
+  for (int b = 0; b < NB && (t0 >> b); ++b)
+    if ((t0 >> b) & 1) ptile |= 1ull << a.perm[b];
 
-  OffT thr[NIN], S[NIN], cur[NIN];
+  OffT thr[NIN], S[NIN], cur[NIN], pf[NIN], s1v[NIN];
   uint32_t mode[NIN];
-  bool strm[NIN];
+  bool strm[NIN], stg[NIN];
   const T* in[NIN];
   const uint64_t inner = TILE - 1;
 #pragma unroll
@@ -194,22 +225,65 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
     in[t] = static_cast<const T*>(a.in[t]);
     thr[t] = (OffT)fmap((uint64_t)tid * VEC, a.out_mask[t], a.pv[t]);
     S[t] = (OffT)1 << a.pv[t];
-    const uint64_t s1 = fmap(1, a.out_mask[t], a.pv[t]);
+    s1v[t] = (OffT)fmap(1, a.out_mask[t], a.pv[t]);
     mode[t] = ((a.out_mask[t] & inner) == 0) ? M_CONST
-              : (VEC == 1 || s1 == 1)        ? M_VEC
-              : (s1 == 0)                    ? M_BCAST
+              : (VEC == 1 || s1v[t] == 1)    ? M_VEC
+              : (s1v[t] == 0)                ? M_BCAST
                                              : M_PAIR;
-    strm[t] = (a.flags[t] & 1u) != 0;
-    cur[t] = (OffT)fmap(t0 << TB, a.out_mask[t], a.pv[t]);
+    strm[t] = (a.flags[t] & F_STREAM) != 0;
+    stg[t] = (a.flags[t] & F_STAGED) != 0 && mode[t] != M_CONST;
+    cur[t] = (OffT)fmap(ptile << TB, a.out_mask[t], a.pv[t]);
+    pf[t] = cur[t];
   }
-  OffT s1v[NIN];
-#pragma unroll
-  for (int t = 0; t < NIN; ++t) s1v[t] = (OffT)fmap(1, a.out_mask[t], a.pv[t]);
   T* out = static_cast<T*>(a.out);
+  bool any_stage = false;
+#pragma unroll
+  for (int t = 0; t < NIN; ++t) any_stage |= stg[t];
   __syncthreads();
 
+  // issue the cp.async copies of one tile's staged chunks into buffer `buf`
+  auto prefetch = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      if (!stg[t]) continue;
+      const uint32_t n = 1u << a.nlow[t];                 // elements per x
+      const uint32_t n16 = (n * sizeof(T)) >> 4;          // 16-byte pieces per x
+      T* dst = stage + buf * a.stage_elems + a.stage_off[t];
+      for (uint32_t c = tid; c < 2 * n16; c += kBucketThreads) {
+        const uint32_t x = c >= n16, piece = c - x * n16;
+        const char* src = reinterpret_cast<const char*>(in[t] + pf[t] + (x ? S[t] : (OffT)0)) + piece * 16;
+        cp_async16(reinterpret_cast<char*>(dst + x * n) + piece * 16, src);
+      }
+    }
+    cp_async_commit();
+  };
+  int buf = 0;
+  if (any_stage && t0 < t1) prefetch(0);
+
   for (uint64_t tile = t0; tile < t1; ++tile) {
-    const uint64_t base = tile << TB;
+    const uint64_t base = ptile << TB;
+    const int r = __ffsll((long long)~tile) - 1;     // tile -> tile + 1: clear r ones, set bit r
+    const bool has_next = tile + 1 < t1;
+    bool same = true;                                 // next tile's staged chunks == current ones
+    if (any_stage) {
+      if (has_next) {
+#pragma unroll
+        for (int t = 0; t < NIN; ++t)
+          if (stg[t]) same &= (fbit[t][r] == fcum[t][r]);
+        if (!same) {
+#pragma unroll
+          for (int t = 0; t < NIN; ++t) pf[t] = pf[t] + fbit[t][r] - fcum[t][r];
+          prefetch(buf ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+    }
+    const T* sb = stage + buf * a.stage_elems;
     // tile constants: product of the CONST inputs for x = 0 and x = 1
     T C0 = cfrom<T>(1.0, 0.0), C1 = cfrom<T>(1.0, 0.0);
     bool has_c = false;
@@ -234,22 +308,40 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
 #pragma unroll
         for (int t = 0; t < NIN; ++t) {
           if (mode[t] == M_CONST) continue;
-          const OffT off = cur[t] + thr[t] + kofs[t][kk];
-          const float2* pt = reinterpret_cast<const float2*>(in[t]);
           float2 x0[2], x1[2];
-          if (mode[t] == M_VEC) {
-            const float4 u0 = ld_in4(reinterpret_cast<const float4*>(pt + off), strm[t]);
-            const float4 u1 = ld_in4(reinterpret_cast<const float4*>(pt + off + S[t]), strm[t]);
-            x0[0] = make_float2(u0.x, u0.y); x0[1] = make_float2(u0.z, u0.w);
-            x1[0] = make_float2(u1.x, u1.y); x1[1] = make_float2(u1.z, u1.w);
-          } else if (mode[t] == M_BCAST) {
-            x0[0] = x0[1] = ld_in(pt + off, strm[t]);
-            x1[0] = x1[1] = ld_in(pt + off + S[t], strm[t]);
+          if (stg[t]) {
+            const uint32_t off = (uint32_t)(thr[t] + kofs[t][kk]);
+            const float2* p = reinterpret_cast<const float2*>(sb + a.stage_off[t]);
+            const uint32_t n = 1u << a.nlow[t];
+            if (mode[t] == M_VEC) {
+              const float4 u0 = *reinterpret_cast<const float4*>(p + off);
+              const float4 u1 = *reinterpret_cast<const float4*>(p + n + off);
+              x0[0] = make_float2(u0.x, u0.y); x0[1] = make_float2(u0.z, u0.w);
+              x1[0] = make_float2(u1.x, u1.y); x1[1] = make_float2(u1.z, u1.w);
+            } else if (mode[t] == M_BCAST) {
+              x0[0] = x0[1] = p[off];
+              x1[0] = x1[1] = p[n + off];
+            } else {
+              x0[0] = p[off]; x0[1] = p[off + s1v[t]];
+              x1[0] = p[n + off]; x1[1] = p[n + off + s1v[t]];
+            }
           } else {
-            x0[0] = ld_in(pt + off, strm[t]);
-            x0[1] = ld_in(pt + off + s1v[t], strm[t]);
-            x1[0] = ld_in(pt + off + S[t], strm[t]);
-            x1[1] = ld_in(pt + off + s1v[t] + S[t], strm[t]);
+            const OffT off = cur[t] + thr[t] + kofs[t][kk];
+            const float2* pt = reinterpret_cast<const float2*>(in[t]);
+            if (mode[t] == M_VEC) {
+              const float4 u0 = ld_in4(reinterpret_cast<const float4*>(pt + off), strm[t]);
+              const float4 u1 = ld_in4(reinterpret_cast<const float4*>(pt + off + S[t]), strm[t]);
+              x0[0] = make_float2(u0.x, u0.y); x0[1] = make_float2(u0.z, u0.w);
+              x1[0] = make_float2(u1.x, u1.y); x1[1] = make_float2(u1.z, u1.w);
+            } else if (mode[t] == M_BCAST) {
+              x0[0] = x0[1] = ld_in(pt + off, strm[t]);
+              x1[0] = x1[1] = ld_in(pt + off + S[t], strm[t]);
+            } else {
+              x0[0] = ld_in(pt + off, strm[t]);
+              x0[1] = ld_in(pt + off + s1v[t], strm[t]);
+              x1[0] = ld_in(pt + off + S[t], strm[t]);
+              x1[1] = ld_in(pt + off + s1v[t] + S[t], strm[t]);
+            }
           }
           if (first) {
             p0[0] = x0[0]; p0[1] = x0[1]; p1[0] = x1[0]; p1[1] = x1[1];
@@ -267,19 +359,240 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
 #pragma unroll
         for (int t = 0; t < NIN; ++t) {
           if (mode[t] == M_CONST) continue;
-          const OffT off = cur[t] + thr[t] + kofs[t][kk];
-          const T x0 = ld_in(in[t] + off, strm[t]);
-          const T x1 = ld_in(in[t] + off + S[t], strm[t]);
+          T x0, x1;
+          if (stg[t]) {
+            const uint32_t off = (uint32_t)(thr[t] + kofs[t][kk]);
+            const T* p = sb + a.stage_off[t];
+            x0 = p[off];
+            x1 = p[(1u << a.nlow[t]) + off];
+          } else {
+            const OffT off = cur[t] + thr[t] + kofs[t][kk];
+            x0 = ld_in(in[t] + off, strm[t]);
+            x1 = ld_in(in[t] + off + S[t], strm[t]);
+          }
           if (first) { p0 = x0; p1 = x1; first = false; }
           else { p0 = cmul(p0, x0); p1 = cmul(p1, x1); }
         }
         __stcs(out + o, cadd(p0, p1));
       }
     }
-    // next tile: tile -> tile + 1 clears the r trailing ones and sets bit r
-    const int r = __ffsll((long long)~tile) - 1;
+    if (any_stage) {
+      __syncthreads();   // all reads of `buf` done before it is refilled
+      if (has_next && !same) buf ^= 1;
+    }
 #pragma unroll
     for (int t = 0; t < NIN; ++t) cur[t] = cur[t] + fbit[t][r] - fcum[t][r];
+    ptile = ptile + pbit[r] - pcum[r];
+  }
+}
+
+// ------------------------------------------------------------------ specialised bucket step
+// Host-classified inputs (see runtime.cu try_launch_specialised):
+//   dir[0..NDIR)  hold ALL low tile bits -> 16-byte global loads (evict-first when read once)
+//   stg[0..NSTG)  hold SOME low tile bits at their lowest positions -> per-tile chunks staged in
+//                 shared memory by cp.async one tile ahead
+//   cst[0..nc)    hold NO low tile bit -> loaded once per tile into C0 / C1
+// The inner loop has no per-input branches.
+struct TArgs {
+  void* out;
+  const void* in[kMaxIn];      // order: dir..., stg..., cst...
+  uint64_t out_mask[kMaxIn];
+  uint32_t pv[kMaxIn];
+  uint32_t stream[kMaxIn];     // dir: evict-first loads
+  uint32_t stage_off[kMaxIn];  // stg: element offset in a smem buffer
+  uint32_t nlow[kMaxIn];       // stg: log2 chunk per x
+  uint32_t stage_elems;
+  int32_t nc;                  // number of constant inputs
+  int32_t out_rank;
+  uint8_t perm[64];
+};
+
+template <typename T, typename OffT, int NDIR, int NSTG>
+__global__ void __launch_bounds__(kBucketThreads, 4) k_bucket_t(const TArgs a) {
+  constexpr int VEC = VecT<T>::n;
+  constexpr int TB = TileBits<T>::v;
+  constexpr int STRIDE = kBucketThreads * VEC;
+  constexpr uint64_t TILE = 1ull << TB;
+  constexpr int NB = 64 - TB;
+  constexpr int NV = NDIR + NSTG;             // inputs that vary inside a tile
+  const int nin = NV + a.nc;
+  const uint64_t n_out = 1ull << a.out_rank;
+  const uint64_t n_tiles = (n_out + TILE - 1) >> TB;
+  const uint32_t tid = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T* stage = reinterpret_cast<T*>(dsm);
+
+  __shared__ OffT kofs[NV > 0 ? NV : 1][kBucketIters];
+  __shared__ OffT fbit[kMaxIn][NB];
+  __shared__ OffT fcum[kMaxIn][NB + 1];
+  __shared__ uint64_t pbit[NB], pcum[NB + 1];
+  if (tid < NV * kBucketIters) {
+    const int t = tid / kBucketIters, kk = tid % kBucketIters;
+    kofs[t][kk] = (OffT)fmap((uint64_t)kk * STRIDE, a.out_mask[t], a.pv[t]);
+  }
+  for (int i = tid; i < nin * NB; i += kBucketThreads) {
+    const int t = i / NB, b = i % NB;
+    fbit[t][b] = (OffT)fmap(1ull << (TB + a.perm[b]), a.out_mask[t], a.pv[t]);
+  }
+  for (int b = tid; b < NB; b += kBucketThreads) pbit[b] = 1ull << a.perm[b];
+  __syncthreads();
+  if (tid < (uint32_t)nin) {
+    OffT c = 0;
+    fcum[tid][0] = 0;
+    for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+  }
+  if (tid == (uint32_t)nin) {
+    uint64_t c = 0;
+    pcum[0] = 0;
+    for (int b = 0; b < NB; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+  }
+  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t ptile = 0;
+  for (int b = 0; b < NB && (t0 >> b); ++b)
+    if ((t0 >> b) & 1) ptile |= 1ull << a.perm[b];
+
+  // varying inputs: registers (compile-time indices); constants: per-tile only
+  OffT thr[NV > 0 ? NV : 1], S[NV > 0 ? NV : 1], cur[NV > 0 ? NV : 1];
+  OffT Sc[kMaxIn], curc[kMaxIn];
+  OffT s1v[NSTG > 0 ? NSTG : 1], chunk[NSTG > 0 ? NSTG : 1];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) thr[t] = (OffT)fmap((uint64_t)tid * VEC, a.out_mask[t], a.pv[t]);
+#pragma unroll
+  for (int u = 0; u < NSTG; ++u) {
+    s1v[u] = (OffT)fmap(1, a.out_mask[NDIR + u], a.pv[NDIR + u]);
+    chunk[u] = (OffT)1 << a.nlow[NDIR + u];
+  }
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    S[t] = (OffT)1 << a.pv[t];
+    cur[t] = (OffT)fmap(ptile << TB, a.out_mask[t], a.pv[t]);
+  }
+  for (int t = NV; t < nin; ++t) {
+    Sc[t] = (OffT)1 << a.pv[t];
+    curc[t] = (OffT)fmap(ptile << TB, a.out_mask[t], a.pv[t]);
+  }
+  OffT pf[NSTG > 0 ? NSTG : 1];
+#pragma unroll
+  for (int u = 0; u < NSTG; ++u) pf[u] = cur[NDIR + u];
+  T* out = static_cast<T*>(a.out);
+  __syncthreads();
+
+  auto prefetch = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < NSTG; ++u) {
+      const int t = NDIR + u;
+      const uint32_t n = 1u << a.nlow[t];
+      const uint32_t n16 = (n * sizeof(T)) >> 4;
+      T* dst = stage + buf * a.stage_elems + a.stage_off[t];
+      const T* src0 = static_cast<const T*>(a.in[t]) + pf[u];
+      for (uint32_t c = tid; c < 2 * n16; c += kBucketThreads) {
+        const uint32_t x = c >= n16, piece = c - x * n16;
+        cp_async16(reinterpret_cast<char*>(dst + x * n) + piece * 16,
+                   reinterpret_cast<const char*>(src0 + (x ? S[t] : (OffT)0)) + piece * 16);
+      }
+    }
+    cp_async_commit();
+  };
+  int buf = 0;
+  if (NSTG > 0 && t0 < t1) prefetch(0);
+
+  for (uint64_t tile = t0; tile < t1; ++tile) {
+    const uint64_t base = ptile << TB;
+    const int r = __ffsll((long long)~tile) - 1;
+    const bool has_next = tile + 1 < t1;
+    bool same = true;
+    if (NSTG > 0) {
+      if (has_next) {
+#pragma unroll
+        for (int u = 0; u < NSTG; ++u) same &= (fbit[NDIR + u][r] == fcum[NDIR + u][r]);
+        if (!same) {
+#pragma unroll
+          for (int u = 0; u < NSTG; ++u) pf[u] = pf[u] + fbit[NDIR + u][r] - fcum[NDIR + u][r];
+          prefetch(buf ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+    }
+    // tile constants
+    T C0 = cfrom<T>(1.0, 0.0), C1 = cfrom<T>(1.0, 0.0);
+    for (int t = NV; t < nin; ++t) {
+      const T* pc = static_cast<const T*>(a.in[t]);
+      C0 = cmul(C0, __ldg(pc + curc[t]));
+      C1 = cmul(C1, __ldg(pc + curc[t] + Sc[t]));
+    }
+    const T* sb = stage + buf * a.stage_elems;
+    OffT db[NDIR > 0 ? NDIR : 1];
+#pragma unroll
+    for (int t = 0; t < NDIR; ++t) db[t] = cur[t] + thr[t];
+#pragma unroll 2
+    for (int kk = 0; kk < kBucketIters; ++kk) {
+      const uint64_t o = base + (uint64_t)kk * STRIDE + (uint64_t)tid * VEC;
+      if (o >= n_out) break;
+      if constexpr (VEC == 2) {
+        float2 p0a, p0b, p1a, p1b;
+#pragma unroll
+        for (int t = 0; t < NDIR; ++t) {
+          const float2* pt = static_cast<const float2*>(a.in[t]) + (db[t] + kofs[t][kk]);
+          float4 u0, u1;
+          if (a.stream[t]) {
+            u0 = __ldcs(reinterpret_cast<const float4*>(pt));
+            u1 = __ldcs(reinterpret_cast<const float4*>(pt + S[t]));
+          } else {
+            u0 = __ldg(reinterpret_cast<const float4*>(pt));
+            u1 = __ldg(reinterpret_cast<const float4*>(pt + S[t]));
+          }
+          const float2 x0a = make_float2(u0.x, u0.y), x0b = make_float2(u0.z, u0.w);
+          const float2 x1a = make_float2(u1.x, u1.y), x1b = make_float2(u1.z, u1.w);
+          if (t == 0) { p0a = x0a; p0b = x0b; p1a = x1a; p1b = x1b; }
+          else { p0a = cmul(p0a, x0a); p0b = cmul(p0b, x0b); p1a = cmul(p1a, x1a); p1b = cmul(p1b, x1b); }
+        }
+#pragma unroll
+        for (int u = 0; u < NSTG; ++u) {
+          const int t = NDIR + u;
+          const float2* p = reinterpret_cast<const float2*>(sb + a.stage_off[t]) + (thr[t] + kofs[t][kk]);
+          const float2 x0a = p[0], x0b = p[s1v[u]];
+          const float2 x1a = p[chunk[u]], x1b = p[chunk[u] + s1v[u]];
+          if (NDIR == 0 && u == 0) { p0a = x0a; p0b = x0b; p1a = x1a; p1b = x1b; }
+          else { p0a = cmul(p0a, x0a); p0b = cmul(p0b, x0b); p1a = cmul(p1a, x1a); p1b = cmul(p1b, x1b); }
+        }
+        const float2 c0 = reinterpret_cast<const float2&>(C0), c1 = reinterpret_cast<const float2&>(C1);
+        const float2 r0 = cadd(cmul(p0a, c0), cmul(p1a, c1));
+        const float2 r1 = cadd(cmul(p0b, c0), cmul(p1b, c1));
+        __stcs(reinterpret_cast<float4*>(out + o), make_float4(r0.x, r0.y, r1.x, r1.y));
+      } else {
+        T p0, p1;
+#pragma unroll
+        for (int t = 0; t < NDIR; ++t) {
+          const T* pt = static_cast<const T*>(a.in[t]) + (db[t] + kofs[t][kk]);
+          const T x0 = a.stream[t] ? __ldcs(pt) : __ldg(pt);
+          const T x1 = a.stream[t] ? __ldcs(pt + S[t]) : __ldg(pt + S[t]);
+          if (t == 0) { p0 = x0; p1 = x1; } else { p0 = cmul(p0, x0); p1 = cmul(p1, x1); }
+        }
+#pragma unroll
+        for (int u = 0; u < NSTG; ++u) {
+          const int t = NDIR + u;
+          const T* p = sb + a.stage_off[t] + (thr[t] + kofs[t][kk]);
+          const T x0 = p[0], x1 = p[chunk[u]];
+          if (NDIR == 0 && u == 0) { p0 = x0; p1 = x1; } else { p0 = cmul(p0, x0); p1 = cmul(p1, x1); }
+        }
+        __stcs(out + o, cadd(cmul(p0, C0), cmul(p1, C1)));
+      }
+    }
+    if (NSTG > 0) {
+      __syncthreads();
+      if (has_next && !same) buf ^= 1;
+    }
+#pragma unroll
+    for (int t = 0; t < NV; ++t) cur[t] = cur[t] + fbit[t][r] - fcum[t][r];
+    for (int t = NV; t < nin; ++t) curc[t] = curc[t] + fbit[t][r] - fcum[t][r];
+    ptile = ptile + pbit[r] - pcum[r];
   }
 }
 

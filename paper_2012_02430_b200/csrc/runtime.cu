@@ -46,6 +46,7 @@ struct DevTables {
 struct ProfRec {
   cudaEvent_t a, b;
   double bytes;
+  int32_t step_begin, step_end, kind, out_rank;
 };
 
 struct tn_plan {
@@ -441,23 +442,189 @@ uint64_t host_pext(uint64_t x, uint64_t m) {
   return r;
 }
 
+// host side of the staging decision (see kernels.cuh): an input is staged in shared memory when
+// it holds some but not all of a tile's low output bits, those map to its lowest positions, and
+// the chunks fit the budget
+template <typename T>
+void plan_staging(BigArgs& a) {
+  constexpr int TB = TileBits<T>::v;
+  const uint64_t inner = (1ull << TB) - 1;
+  uint32_t off = 0;
+  for (int t = 0; t < a.n_in; ++t) {
+    a.flags[t] &= ~F_STAGED;
+    const uint64_t lowm = a.out_mask[t] & inner;
+    const int nlow = __builtin_popcountll(lowm);
+    if (a.out_rank <= TB || nlow == 0 || nlow >= TB || nlow > 10) continue;
+    // contiguity: the tile's low output bits must be the input's positions 0..nlow-1
+    uint64_t f = 0;
+    {
+      uint64_t m = a.out_mask[t], r = 0;
+      int k = 0;
+      for (int b = 0; b < 64 && m; ++b) {
+        if ((m >> b) & 1) {
+          if ((lowm >> b) & 1) r |= 1ull << k;
+          ++k;
+          m &= ~(1ull << b);
+        }
+      }
+      const uint64_t lo = r & ((1ull << a.pv[t]) - 1);
+      f = lo | ((r >> a.pv[t]) << (a.pv[t] + 1));
+    }
+    if (f != (1ull << nlow) - 1) continue;
+    const uint32_t need = 2u << nlow;  // both x
+    if ((off + need) * sizeof(T) * 2 > 48 * 1024) continue;
+    a.flags[t] |= F_STAGED;
+    a.nlow[t] = (uint32_t)nlow;
+    a.stage_off[t] = off;
+    off += need;
+  }
+  a.stage_elems = off;
+}
+
+// traversal order of the tile-index bits: bits absent from the largest input first (its chunk
+// is then reused by consecutive tiles), then bits absent from the second largest, then the rest
+// in ascending order.  Streaming (evict-first) loads only for inputs without reuse.
+template <typename T>
+void plan_order(BigArgs& a) {
+  constexpr int TB = TileBits<T>::v;
+  int big[2] = {-1, -1};
+  for (int t = 0; t < a.n_in; ++t) {
+    const int r = __builtin_popcountll(a.out_mask[t]);
+    if (big[0] < 0 || r > __builtin_popcountll(a.out_mask[big[0]])) { big[1] = big[0]; big[0] = t; }
+    else if (big[1] < 0 || r > __builtin_popcountll(a.out_mask[big[1]])) big[1] = t;
+  }
+  std::vector<int> bits;
+  for (int b = TB; b < 64; ++b) bits.push_back(b);
+  auto has = [&](int t, int b) { return t >= 0 && ((a.out_mask[t] >> b) & 1); };
+  std::stable_sort(bits.begin(), bits.end(), [&](int x, int y) {
+    if (has(big[0], x) != has(big[0], y)) return !has(big[0], x);
+    if (has(big[1], x) != has(big[1], y)) return !has(big[1], x);
+    return x < y;
+  });
+  // bits at or above out_rank never change within the grid; keep them last
+  std::stable_partition(bits.begin(), bits.end(), [&](int b) { return b < a.out_rank; });
+  for (int i = 0; i < 64 - TB; ++i) a.perm[i] = (uint8_t)(bits[i] - TB);
+  const uint64_t full = a.out_rank >= 64 ? ~0ull : ((1ull << a.out_rank) - 1);
+  for (int t = 0; t < a.n_in; ++t) {
+    if (a.out_mask[t] == full && a.out_rank >= 16) a.flags[t] |= F_STREAM;
+    else a.flags[t] &= ~F_STREAM;
+  }
+}
+
 template <typename T, int NIN>
-void launch_bucket_n(const BigArgs& a, cudaStream_t st) {
+void launch_bucket_n(BigArgs a, cudaStream_t st) {
   constexpr uint64_t TILE = 1ull << TileBits<T>::v;
+  plan_order<T>(a);
+  plan_staging<T>(a);
   const uint64_t n_out = 1ull << a.out_rank;
   const uint64_t tiles = (n_out + TILE - 1) / TILE;
   const uint64_t cap = (uint64_t)num_sms() * 4;
   const unsigned grid = (unsigned)std::min<uint64_t>(tiles, cap);
+  const size_t smem = (size_t)a.stage_elems * sizeof(T) * 2;
   bool wide = false;   // any input with more than 32 bits -> 64-bit offsets
   for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
   if (wide)
-    k_bucket<T, NIN, uint64_t><<<grid, kBucketThreads, 0, st>>>(a);
+    k_bucket<T, NIN, uint64_t><<<grid, kBucketThreads, smem, st>>>(a);
   else
-    k_bucket<T, NIN, uint32_t><<<grid, kBucketThreads, 0, st>>>(a);
+    k_bucket<T, NIN, uint32_t><<<grid, kBucketThreads, smem, st>>>(a);
+}
+
+// Specialised path: classify inputs into direct / staged / constant groups (kernels.cuh
+// k_bucket_t).  Returns false when the step does not fit (then the generic k_bucket runs).
+template <typename T, typename OffT, int NDIR, int NSTG>
+void launch_t(const TArgs& ta, unsigned grid, size_t smem, cudaStream_t st) {
+  k_bucket_t<T, OffT, NDIR, NSTG><<<grid, kBucketThreads, smem, st>>>(ta);
+}
+
+template <typename T, typename OffT>
+bool launch_t_dispatch(const TArgs& ta, int ndir, int nstg, unsigned grid, size_t smem, cudaStream_t st) {
+#define TN_T(D, G) if (ndir == D && nstg == G) { launch_t<T, OffT, D, G>(ta, grid, smem, st); return true; }
+  TN_T(1, 0) TN_T(2, 0) TN_T(3, 0) TN_T(0, 1) TN_T(1, 1) TN_T(2, 1) TN_T(0, 2) TN_T(1, 2) TN_T(2, 2)
+  TN_T(0, 3) TN_T(1, 3) TN_T(0, 4)
+#undef TN_T
+  return false;
+}
+
+template <typename T>
+bool try_launch_specialised(const BigArgs& in, cudaStream_t st) {
+  constexpr int TB = TileBits<T>::v;
+  constexpr uint64_t TILE = 1ull << TB;
+  if (in.out_rank <= TB) return false;
+  const uint64_t inner = TILE - 1;
+  BigArgs a = in;
+  plan_order<T>(a);
+  int dir[kMaxIn], stg[kMaxIn], cst[kMaxIn], nd = 0, ns = 0, nc = 0;
+  uint32_t soff = 0;
+  for (int t = 0; t < a.n_in; ++t) {
+    const uint64_t lowm = a.out_mask[t] & inner;
+    const int nlow = __builtin_popcountll(lowm);
+    if (nlow == 0) { cst[nc++] = t; continue; }
+    // direct 16-byte loads need output bit 0 at input position 0 (always true for c128)
+    const bool vec_ok = (VecT<T>::n == 1) || ((a.out_mask[t] & 1) && a.pv[t] != 0);
+    if (nlow == TB) {
+      if (!vec_ok) return false;
+      dir[nd++] = t;
+      continue;
+    }
+    // staging: the tile's low output bits must be the input's lowest positions (pv above them)
+    uint64_t r = 0;
+    {
+      uint64_t m = a.out_mask[t];
+      int k = 0;
+      for (int b = 0; b < 64 && m; ++b)
+        if ((m >> b) & 1) { if ((lowm >> b) & 1) r |= 1ull << k; ++k; m &= ~(1ull << b); }
+    }
+    const uint32_t need = 2u << nlow;
+    const bool stageable = (int)a.pv[t] >= nlow && r == (1ull << nlow) - 1 && nlow <= 10 &&
+                           (soff + need) * sizeof(T) * 2 <= 48 * 1024;
+    if (stageable) {
+      stg[ns++] = t;
+      soff += need;
+    } else if (vec_ok) {
+      dir[nd++] = t;   // large partial input: direct loads, intra-tile reuse from L1
+    } else {
+      return false;
+    }
+  }
+  if (nd + ns == 0) return false;
+  TArgs ta;
+  std::memset(&ta, 0, sizeof(ta));
+  ta.out = a.out;
+  ta.out_rank = a.out_rank;
+  ta.nc = nc;
+  std::memcpy(ta.perm, a.perm, sizeof(ta.perm));
+  int k = 0;
+  uint32_t off = 0;
+  auto put = [&](int t) {
+    ta.in[k] = a.in[t];
+    ta.out_mask[k] = a.out_mask[t];
+    ta.pv[k] = a.pv[t];
+    ta.stream[k] = (a.flags[t] & F_STREAM) ? 1u : 0u;
+    ++k;
+  };
+  for (int i = 0; i < nd; ++i) put(dir[i]);
+  for (int i = 0; i < ns; ++i) {
+    const int t = stg[i];
+    const int nlow = __builtin_popcountll(a.out_mask[t] & inner);
+    ta.nlow[k] = (uint32_t)nlow;
+    ta.stage_off[k] = off;
+    off += 2u << nlow;
+    put(t);
+  }
+  for (int i = 0; i < nc; ++i) put(cst[i]);
+  ta.stage_elems = off;
+  const uint64_t tiles = ((1ull << a.out_rank) + TILE - 1) / TILE;
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 4);
+  const size_t smem = (size_t)off * sizeof(T) * 2;
+  bool wide = false;
+  for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
+  return wide ? launch_t_dispatch<T, uint64_t>(ta, nd, ns, grid, smem, st)
+              : launch_t_dispatch<T, uint32_t>(ta, nd, ns, grid, smem, st);
 }
 
 template <typename T>
 void launch_bucket(const BigArgs& a, cudaStream_t st) {
+  if (try_launch_specialised<T>(a, st)) return;
   switch (a.n_in) {
     case 1: launch_bucket_n<T, 1>(a, st); break;
     case 2: launch_bucket_n<T, 2>(a, st); break;
@@ -508,6 +675,10 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         pr.a = pool_event(pl);
         pr.b = pool_event(pl);
         pr.bytes = bytes;
+        pr.step_begin = op.begin;
+        pr.step_end = op.end;
+        pr.kind = 1;
+        pr.out_rank = s.out_rank;
         cudaEventRecord(pr.a, st);
       }
       launch_bucket<T>(a, st);
@@ -538,6 +709,10 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         pr.a = pool_event(pl);
         pr.b = pool_event(pl);
         pr.bytes = bytes;
+        pr.step_begin = op.begin;
+        pr.step_end = op.end;
+        pr.kind = 2;
+        pr.out_rank = c.out_rank;
         cudaEventRecord(pr.a, st);
       }
       constexpr int VEC = VecT<T>::n;
@@ -771,6 +946,24 @@ extern "C" tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* 
   if (all_launches) *all_launches = plan->all_launches;
   plan->prof.clear();
   plan->all_launches = 0;
+  return TN_OK;
+}
+
+extern "C" tn_status tn_profile_records(tn_plan* plan, tn_prof_record_t* out, int64_t cap, int64_t* n) {
+  if (!plan || !n) return fail(TN_E_INVAL, "null argument");
+  *n = (int64_t)plan->prof.size();
+  for (int64_t i = 0; out && i < cap && i < *n; ++i) {
+    ProfRec& p = plan->prof[i];
+    CU(cudaEventSynchronize(p.b));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, p.a, p.b));
+    out[i].step_begin = p.step_begin;
+    out[i].step_end = p.step_end;
+    out[i].kind = p.kind;
+    out[i].out_rank = p.out_rank;
+    out[i].ms = t;
+    out[i].bytes = p.bytes;
+  }
   return TN_OK;
 }
 

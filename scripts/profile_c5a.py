@@ -20,8 +20,8 @@ def main():
     args = ap.parse_args()
     plan, g, ga, be, meta = bench.build_workload_plan(args.workload)
     steps = plan.steps()
-    big_a = [i for i, s in enumerate(steps) if s["standalone"] and s["phase"] == 0]
-    big_b = [i for i, s in enumerate(steps) if s["standalone"] and s["phase"] == 1]
+    big_a = [i for i, s in enumerate(steps) if s["standalone"] == 1 and s["phase"] == 0]
+    big_b = [i for i, s in enumerate(steps) if s["standalone"] == 1 and s["phase"] == 1]
     if args.list or args.print_skip is not None:
         if args.list:
             for o, i in enumerate(big_b):

@@ -62,6 +62,11 @@ def _oracle_step(arrays, masks, pvs, out_rank):
     arr, labs = contract._einsum_bucket(ts, 100)
     # oracle output axes are ascending labels = ascending output bit; flatten most-significant first
     want = tuple(reversed(range(out_rank)))
+    # output bits held by no input: the result is constant along them (broadcast)
+    for l in want:
+        if l not in labs:
+            arr = np.stack([arr, arr], axis=-1)
+            labs = tuple(labs) + (l,)
     if labs:
         arr = np.transpose(arr, [labs.index(l) for l in want])
     return arr.reshape(-1)
@@ -83,6 +88,36 @@ def test_eliminate_vs_oracle(dtype, out_rank, n_in):
     ref = _oracle_step(arrays, masks, pvs, out_rank)
     scale = np.max(np.abs(ref)) + 1e-30
     assert np.max(np.abs(got - ref)) / scale < TOL[dtype] * 0.1
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+@pytest.mark.parametrize("out_rank,kinds", [(13, "FS"), (14, "FSC"), (15, "SSC"), (16, "FFS"), (17, "SC"),
+                                            (18, "FSSC"), (20, "FC"), (21, "SSSC"), (22, "FFSC"), (19, "CS")])
+def test_eliminate_specialised_vs_oracle(dtype, out_rank, kinds):
+    # plan-like steps (summed index on top of every input): F = holds every low tile bit,
+    # S = some low bits (staged in shared memory), C = no low bit (per-tile constant)
+    rng = np.random.default_rng(out_rank * 13 + len(kinds) + dtype)
+    tb = 12 if dtype == T.TN_C64 else 11
+    masks, pvs, shapes = [], [], []
+    for k in kinds:
+        low = (1 << tb) - 1 if k == "F" else (0 if k == "C" else int(rng.integers(1, (1 << tb) - 1)))
+        high = 0
+        for b in range(tb, out_rank):
+            if rng.random() < 0.5:
+                high |= 1 << b
+        m = low | high
+        masks.append(m)
+        pvs.append(bin(m).count("1"))
+        shapes.append(bin(m).count("1") + 1)
+    arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+    dev = [torch.tensor(a, dtype=DT[dtype], device="cuda") for a in arrays]
+    out = torch.empty(2 ** out_rank, dtype=DT[dtype], device="cuda")
+    B.tn_eliminate(dtype, [d.data_ptr() for d in dev], masks, pvs, out.data_ptr(), out_rank,
+                   torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.complex128)
+    ref = _oracle_step(arrays, masks, pvs, out_rank)
+    assert np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30) < TOL[dtype] * 0.1
 
 
 # ------------------------------------------------------------------ amplitudes, small/medium
