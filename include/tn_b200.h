@@ -113,7 +113,7 @@ typedef struct {
   int32_t n_in;
   int32_t inplace;        /* output aliases the first input's lower half */
   int32_t standalone;     /* 1: own k_bucket launch; 2: part of a fused reduce chain (k_chain);
-                             0: inside an interpreter run */
+                             3: part of a fused merge group (k_group_t); 0: inside an interpreter run */
   int32_t in_rank[8];     /* bits of each input read per slice */
   uint64_t in_out_mask[8];
   int32_t in_pv[8];
@@ -168,7 +168,7 @@ tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms, d
 
 /* The per-launch records behind tn_profile_read (call it BEFORE tn_profile_read, which clears
  * them): one record per standalone launch (k_bucket / k_chain) with its plan step range, kind
- * (1 = k_bucket, 2 = k_chain), device milliseconds and algorithmic bytes.  out: host array of cap
+ * (1 = k_bucket, 2 = k_chain, 3 = k_group), device milliseconds and algorithmic bytes.  out: host array of cap
  * records (may be NULL to query *n). */
 typedef struct {
   int32_t step_begin, step_end, kind, out_rank;

@@ -233,5 +233,5 @@ def tn_profile_records(h: int):
     _check(_lib.tn_profile_records(h, None, 0, C.byref(n)), "tn_profile_records")
     arr = (tn_prof_record_t * max(1, n.value))()
     _check(_lib.tn_profile_records(h, arr, n.value, C.byref(n)), "tn_profile_records")
-    return [{"step_begin": r.step_begin, "step_end": r.step_end, "kind": ("k_bucket", "k_chain")[r.kind - 1],
+    return [{"step_begin": r.step_begin, "step_end": r.step_end, "kind": ("k_bucket", "k_chain", "k_group")[r.kind - 1],
              "out_rank": r.out_rank, "ms": r.ms, "bytes": r.bytes} for r in arr[:n.value]]

@@ -386,35 +386,48 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ specialised bucket step
-// Host-classified inputs (see runtime.cu try_launch_specialised):
-//   dir[0..NDIR)  hold ALL low tile bits -> 16-byte global loads (evict-first when read once)
-//   stg[0..NSTG)  hold SOME low tile bits at their lowest positions -> per-tile chunks staged in
-//                 shared memory by cp.async one tile ahead
-//   cst[0..nc)    hold NO low tile bit -> loaded once per tile into C0 / C1
-// The inner loop has no per-input branches.
-struct TArgs {
+// ------------------------------------------------------------------ specialised bucket group
+// One launch eliminates a block of M consecutive indices x = (v_s .. v_{s+M-1}) (M = 1: a single
+// bucket step; M > 1: a merge step fused with the in-place reduce steps that follow it -- exact
+// re-association of the same sum):
+//     out[o] = sum_{x < 2^M} prod_t in_t[F_t(o) + G_t(x)],   F_t(o) = ins0(pext(o, mask_t), pv_t)
+// with G_t(x) host-computed tables (kernel parameters -> constant bank, compile-time indexed).
+// Host-classified inputs (runtime.cu try_launch_group):
+//   dir[0..NDIR)  hold output bit 0 at position 0 -> 16-byte global loads (evict-first if read once)
+//   stg[0..NSTG)  hold SOME low tile bits at their lowest positions -> per-tile chunks (one per
+//                 distinct x-part) staged in shared memory by cp.async one tile ahead
+//   cst[0..nc)    hold NO low tile bit -> C[x] = prod_cst in_t[cur_t + G_t(x)] once per tile
+// The inner loops have no per-input branches.
+constexpr int kMaxGroup = 5;
+struct GArgs {
   void* out;
-  const void* in[kMaxIn];      // order: dir..., stg..., cst...
-  uint64_t out_mask[kMaxIn];
+  const void* in[kMaxIn];              // order: dir..., stg..., cst...
+  uint64_t out_mask[kMaxIn];           // output bits present (relative to the group output)
+  uint64_t gx[kMaxIn][1 << kMaxGroup]; // element offset of the x-part of input t for x
+  uint32_t sx[kMaxIn][1 << kMaxGroup]; // staged: smem element offset of x's chunk (buffer 0)
+  uint8_t rep[kMaxIn][1 << kMaxGroup]; // staged: an x for each distinct part (prefetch source)
+  uint32_t nparts[kMaxIn];             // staged: distinct x-parts
+  uint32_t nlow[kMaxIn];               // staged: log2 chunk
   uint32_t pv[kMaxIn];
-  uint32_t stream[kMaxIn];     // dir: evict-first loads
-  uint32_t stage_off[kMaxIn];  // stg: element offset in a smem buffer
-  uint32_t nlow[kMaxIn];       // stg: log2 chunk per x
+  uint32_t stream[kMaxIn];
   uint32_t stage_elems;
-  int32_t nc;                  // number of constant inputs
+  int32_t nc;
   int32_t out_rank;
   uint8_t perm[64];
 };
 
-template <typename T, typename OffT, int NDIR, int NSTG>
-__global__ void __launch_bounds__(kBucketThreads, 4) k_bucket_t(const TArgs a) {
+// NDIR direct inputs: the first NDV use 16-byte vector loads (output bit 0 at their position
+// 0), the remaining NDIR - NDV use two 8-byte loads (offsets p and p + F_t(1); F_t(1) = 0 when
+// they lack output bit 0, i.e. one value serves both elements)
+template <typename T, typename OffT, int NDIR, int NSTG, int M, int NDV>
+__global__ void __launch_bounds__(kBucketThreads, 4) k_group_t(const GArgs a) {
   constexpr int VEC = VecT<T>::n;
   constexpr int TB = TileBits<T>::v;
   constexpr int STRIDE = kBucketThreads * VEC;
   constexpr uint64_t TILE = 1ull << TB;
   constexpr int NB = 64 - TB;
-  constexpr int NV = NDIR + NSTG;             // inputs that vary inside a tile
+  constexpr int NV = NDIR + NSTG;
+  constexpr int NX = 1 << M;
   const int nin = NV + a.nc;
   const uint64_t n_out = 1ull << a.out_rank;
   const uint64_t n_tiles = (n_out + TILE - 1) >> TB;
@@ -422,10 +435,11 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket_t(const TArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   T* stage = reinterpret_cast<T*>(dsm);
 
-  __shared__ OffT kofs[NV > 0 ? NV : 1][kBucketIters];
+  __shared__ OffT kofs[NV][kBucketIters];
   __shared__ OffT fbit[kMaxIn][NB];
   __shared__ OffT fcum[kMaxIn][NB + 1];
   __shared__ uint64_t pbit[NB], pcum[NB + 1];
+  __shared__ T Cs[2][NX];
   if (tid < NV * kBucketIters) {
     const int t = tid / kBucketIters, kk = tid % kBucketIters;
     kofs[t][kk] = (OffT)fmap((uint64_t)kk * STRIDE, a.out_mask[t], a.pv[t]);
@@ -453,26 +467,20 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket_t(const TArgs a) {
   for (int b = 0; b < NB && (t0 >> b); ++b)
     if ((t0 >> b) & 1) ptile |= 1ull << a.perm[b];
 
-  // varying inputs: registers (compile-time indices); constants: per-tile only
-  OffT thr[NV > 0 ? NV : 1], S[NV > 0 ? NV : 1], cur[NV > 0 ? NV : 1];
-  OffT Sc[kMaxIn], curc[kMaxIn];
-  OffT s1v[NSTG > 0 ? NSTG : 1], chunk[NSTG > 0 ? NSTG : 1];
+  OffT thr[NV], cur[NV];
+  OffT curc[kMaxIn];
+  OffT s1v[NSTG > 0 ? NSTG : 1];
+  OffT d1v[NDIR > 0 ? NDIR : 1];
 #pragma unroll
-  for (int t = 0; t < NV; ++t) thr[t] = (OffT)fmap((uint64_t)tid * VEC, a.out_mask[t], a.pv[t]);
-#pragma unroll
-  for (int u = 0; u < NSTG; ++u) {
-    s1v[u] = (OffT)fmap(1, a.out_mask[NDIR + u], a.pv[NDIR + u]);
-    chunk[u] = (OffT)1 << a.nlow[NDIR + u];
-  }
+  for (int t = 0; t < NDIR; ++t) d1v[t] = (OffT)fmap(1, a.out_mask[t], a.pv[t]);
 #pragma unroll
   for (int t = 0; t < NV; ++t) {
-    S[t] = (OffT)1 << a.pv[t];
+    thr[t] = (OffT)fmap((uint64_t)tid * VEC, a.out_mask[t], a.pv[t]);
     cur[t] = (OffT)fmap(ptile << TB, a.out_mask[t], a.pv[t]);
   }
-  for (int t = NV; t < nin; ++t) {
-    Sc[t] = (OffT)1 << a.pv[t];
-    curc[t] = (OffT)fmap(ptile << TB, a.out_mask[t], a.pv[t]);
-  }
+#pragma unroll
+  for (int u = 0; u < NSTG; ++u) s1v[u] = (OffT)fmap(1, a.out_mask[NDIR + u], a.pv[NDIR + u]);
+  for (int t = NV; t < nin; ++t) curc[t] = (OffT)fmap(ptile << TB, a.out_mask[t], a.pv[t]);
   OffT pf[NSTG > 0 ? NSTG : 1];
 #pragma unroll
   for (int u = 0; u < NSTG; ++u) pf[u] = cur[NDIR + u];
@@ -485,23 +493,32 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket_t(const TArgs a) {
       const int t = NDIR + u;
       const uint32_t n = 1u << a.nlow[t];
       const uint32_t n16 = (n * sizeof(T)) >> 4;
-      T* dst = stage + buf * a.stage_elems + a.stage_off[t];
-      const T* src0 = static_cast<const T*>(a.in[t]) + pf[u];
-      for (uint32_t c = tid; c < 2 * n16; c += kBucketThreads) {
-        const uint32_t x = c >= n16, piece = c - x * n16;
-        cp_async16(reinterpret_cast<char*>(dst + x * n) + piece * 16,
-                   reinterpret_cast<const char*>(src0 + (x ? S[t] : (OffT)0)) + piece * 16);
+      T* dst = stage + buf * a.stage_elems;
+      const T* src = static_cast<const T*>(a.in[t]) + pf[u];
+      const uint32_t total = a.nparts[t] * n16;
+      for (uint32_t c = tid; c < total; c += kBucketThreads) {
+        const uint32_t part = c / n16, piece = c - part * n16;
+        const uint32_t xr = a.rep[t][part];
+        cp_async16(reinterpret_cast<char*>(dst + a.sx[t][xr]) + piece * 16,
+                   reinterpret_cast<const char*>(src + (OffT)a.gx[t][xr]) + piece * 16);
       }
     }
     cp_async_commit();
   };
-  int buf = 0;
+  int buf = 0, cb = 0;
   if (NSTG > 0 && t0 < t1) prefetch(0);
 
   for (uint64_t tile = t0; tile < t1; ++tile) {
     const uint64_t base = ptile << TB;
     const int r = __ffsll((long long)~tile) - 1;
     const bool has_next = tile + 1 < t1;
+    // per-tile constants C[x]
+    if (tid < (uint32_t)NX) {
+      T c = cfrom<T>(1.0, 0.0);
+      for (int t = NV; t < nin; ++t)
+        c = cmul(c, __ldg(static_cast<const T*>(a.in[t]) + curc[t] + (OffT)a.gx[t][tid]));
+      Cs[cb][tid] = c;
+    }
     bool same = true;
     if (NSTG > 0) {
       if (has_next) {
@@ -518,77 +535,75 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket_t(const TArgs a) {
       } else {
         cp_async_wait<0>();
       }
-      __syncthreads();
     }
-    // tile constants
-    T C0 = cfrom<T>(1.0, 0.0), C1 = cfrom<T>(1.0, 0.0);
-    for (int t = NV; t < nin; ++t) {
-      const T* pc = static_cast<const T*>(a.in[t]);
-      C0 = cmul(C0, __ldg(pc + curc[t]));
-      C1 = cmul(C1, __ldg(pc + curc[t] + Sc[t]));
-    }
+    __syncthreads();
     const T* sb = stage + buf * a.stage_elems;
     OffT db[NDIR > 0 ? NDIR : 1];
 #pragma unroll
     for (int t = 0; t < NDIR; ++t) db[t] = cur[t] + thr[t];
-#pragma unroll 2
+    constexpr int KU = (M == 1) ? 2 : 1;
+#pragma unroll KU
     for (int kk = 0; kk < kBucketIters; ++kk) {
       const uint64_t o = base + (uint64_t)kk * STRIDE + (uint64_t)tid * VEC;
       if (o >= n_out) break;
       if constexpr (VEC == 2) {
-        float2 p0a, p0b, p1a, p1b;
+        float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < NDIR; ++t) {
-          const float2* pt = static_cast<const float2*>(a.in[t]) + (db[t] + kofs[t][kk]);
-          float4 u0, u1;
-          if (a.stream[t]) {
-            u0 = __ldcs(reinterpret_cast<const float4*>(pt));
-            u1 = __ldcs(reinterpret_cast<const float4*>(pt + S[t]));
-          } else {
-            u0 = __ldg(reinterpret_cast<const float4*>(pt));
-            u1 = __ldg(reinterpret_cast<const float4*>(pt + S[t]));
+        for (int x = 0; x < NX; ++x) {
+          float2 pa, pb;
+#pragma unroll
+          for (int t = 0; t < NDIR; ++t) {
+            const float2* q = static_cast<const float2*>(a.in[t]) + (db[t] + kofs[t][kk] + (OffT)a.gx[t][x]);
+            float2 xa, xb;
+            if (t < NDV) {
+              const float4 u = __ldg(reinterpret_cast<const float4*>(q));
+              xa = make_float2(u.x, u.y);
+              xb = make_float2(u.z, u.w);
+            } else {
+              xa = __ldg(q);
+              xb = __ldg(q + d1v[t]);
+            }
+            if (t == 0) { pa = xa; pb = xb; } else { pa = cmul(pa, xa); pb = cmul(pb, xb); }
           }
-          const float2 x0a = make_float2(u0.x, u0.y), x0b = make_float2(u0.z, u0.w);
-          const float2 x1a = make_float2(u1.x, u1.y), x1b = make_float2(u1.z, u1.w);
-          if (t == 0) { p0a = x0a; p0b = x0b; p1a = x1a; p1b = x1b; }
-          else { p0a = cmul(p0a, x0a); p0b = cmul(p0b, x0b); p1a = cmul(p1a, x1a); p1b = cmul(p1b, x1b); }
-        }
 #pragma unroll
-        for (int u = 0; u < NSTG; ++u) {
-          const int t = NDIR + u;
-          const float2* p = reinterpret_cast<const float2*>(sb + a.stage_off[t]) + (thr[t] + kofs[t][kk]);
-          const float2 x0a = p[0], x0b = p[s1v[u]];
-          const float2 x1a = p[chunk[u]], x1b = p[chunk[u] + s1v[u]];
-          if (NDIR == 0 && u == 0) { p0a = x0a; p0b = x0b; p1a = x1a; p1b = x1b; }
-          else { p0a = cmul(p0a, x0a); p0b = cmul(p0b, x0b); p1a = cmul(p1a, x1a); p1b = cmul(p1b, x1b); }
+          for (int u = 0; u < NSTG; ++u) {
+            const int t = NDIR + u;
+            const float2* p = reinterpret_cast<const float2*>(sb + a.sx[t][x]) + (thr[t] + kofs[t][kk]);
+            const float2 xa = p[0], xb = p[s1v[u]];
+            if (NDIR == 0 && u == 0) { pa = xa; pb = xb; } else { pa = cmul(pa, xa); pb = cmul(pb, xb); }
+          }
+          const float2 c = reinterpret_cast<const float2&>(Cs[cb][x]);
+          acc_a = cadd(acc_a, cmul(pa, c));
+          acc_b = cadd(acc_b, cmul(pb, c));
         }
-        const float2 c0 = reinterpret_cast<const float2&>(C0), c1 = reinterpret_cast<const float2&>(C1);
-        const float2 r0 = cadd(cmul(p0a, c0), cmul(p1a, c1));
-        const float2 r1 = cadd(cmul(p0b, c0), cmul(p1b, c1));
-        __stcs(reinterpret_cast<float4*>(out + o), make_float4(r0.x, r0.y, r1.x, r1.y));
+        __stcs(reinterpret_cast<float4*>(out + o), make_float4(acc_a.x, acc_a.y, acc_b.x, acc_b.y));
       } else {
-        T p0, p1;
+        T acc = cfrom<T>(0.0, 0.0);
 #pragma unroll
-        for (int t = 0; t < NDIR; ++t) {
-          const T* pt = static_cast<const T*>(a.in[t]) + (db[t] + kofs[t][kk]);
-          const T x0 = a.stream[t] ? __ldcs(pt) : __ldg(pt);
-          const T x1 = a.stream[t] ? __ldcs(pt + S[t]) : __ldg(pt + S[t]);
-          if (t == 0) { p0 = x0; p1 = x1; } else { p0 = cmul(p0, x0); p1 = cmul(p1, x1); }
-        }
+        for (int x = 0; x < NX; ++x) {
+          T pr;
 #pragma unroll
-        for (int u = 0; u < NSTG; ++u) {
-          const int t = NDIR + u;
-          const T* p = sb + a.stage_off[t] + (thr[t] + kofs[t][kk]);
-          const T x0 = p[0], x1 = p[chunk[u]];
-          if (NDIR == 0 && u == 0) { p0 = x0; p1 = x1; } else { p0 = cmul(p0, x0); p1 = cmul(p1, x1); }
+          for (int t = 0; t < NDIR; ++t) {
+            const T* pt = static_cast<const T*>(a.in[t]) + (db[t] + kofs[t][kk] + (OffT)a.gx[t][x]);
+            const T v = __ldg(pt);
+            if (t == 0) pr = v; else pr = cmul(pr, v);
+          }
+#pragma unroll
+          for (int u = 0; u < NSTG; ++u) {
+            const int t = NDIR + u;
+            const T v = sb[a.sx[t][x] + thr[t] + kofs[t][kk]];
+            if (NDIR == 0 && u == 0) pr = v; else pr = cmul(pr, v);
+          }
+          acc = cadd(acc, cmul(pr, Cs[cb][x]));
         }
-        __stcs(out + o, cadd(cmul(p0, C0), cmul(p1, C1)));
+        __stcs(out + o, acc);
       }
     }
     if (NSTG > 0) {
       __syncthreads();
       if (has_next && !same) buf ^= 1;
     }
+    cb ^= 1;
 #pragma unroll
     for (int t = 0; t < NV; ++t) cur[t] = cur[t] + fbit[t][r] - fcum[t][r];
     for (int t = NV; t < nin; ++t) curc[t] = curc[t] + fbit[t][r] - fcum[t][r];

@@ -677,9 +677,12 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       i = j;
     }
   }
-  // ---- fusion of reduce chains (phase B): step i is a chain head if its first input holds
-  // every output bit with the summed bit on top and its other inputs are rank-1 weights on the
-  // summed index; step i+1 extends the chain if it is the in-place reduce of step i's output.
+  // ---- fusion (phase B).  A reduce step holds every output bit in its first input with the
+  // summed bit on top and has only rank-1 weights on the summed index as other inputs; a follower
+  // is the in-place reduce of the previous step's output.
+  //   reduce head + followers      -> OP_CHAIN (k_chain, up to kMaxChain summed indices)
+  //   other head + g followers     -> OP_GROUP (k_group_t, M = g + 1 <= kMaxGroupPlan) when the
+  //                                   time model says it pays; remaining followers form a chain
   {
     auto is_reduce = [&](const StepRec& st) {
       if (st.out_rank < 1 || st.n_in - 1 > kMaxChainW) return false;
@@ -691,43 +694,94 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
         if (st.in[t].out_mask != 0 || st.in[t].rank != 1) return false;
       return true;
     };
+    auto step_elems = [&](const StepRec& st) {
+      double e = std::ldexp(1.0, st.out_rank);
+      for (int t = 0; t < st.n_in; ++t) e += std::ldexp(1.0, (int)st.in[t].rank);
+      return e;
+    };
+    // time model (c64, seconds): HBM-bound streams at kBW; fused groups also pay per-output work
+    const double kBW = 5.5e12, kOps = 2.0e13;
+    auto t_elems = [&](double e) { return e * 8.0 / kBW; };
+    auto t_chain = [&](int RA, int m) {   // m reduce steps starting from a rank-RA input
+      if (m <= 0) return 0.0;
+      return t_elems(std::ldexp(1.0, RA) + std::ldexp(1.0, RA - m));
+    };
+    auto t_group = [&](int s0, int g) {   // head s0 + g followers
+      const StepRec& h = out.steps[s0];
+      const int M = g + 1;
+      const int Rf = out.steps[s0 + g].out_rank;
+      double e = std::ldexp(1.0, Rf);
+      int nv = 0;
+      for (int t = 0; t < h.n_in; ++t) {
+        e += std::ldexp(1.0, (int)h.in[t].rank);
+        if ((h.in[t].out_mask & ((1ull << Rf) - 1)) != 0) ++nv;
+      }
+      const double ops = std::ldexp(1.0, Rf + M) * (nv + 1) * 10.0;
+      return std::max(t_elems(e), ops / kOps);
+    };
     std::vector<OpRec> fused;
     for (size_t oi = 0; oi < out.ops.size(); ++oi) {
       const OpRec& op = out.ops[oi];
-      if (op.phase != 1 || op.type != OP_BIG || !is_reduce(out.steps[op.begin])) {
+      if (op.phase != 1 || op.type != OP_BIG) {
         fused.push_back(op);
         continue;
       }
-      size_t oj = oi + 1;
-      int end = op.begin + 1;
-      while (oj < out.ops.size() && (end - op.begin) < kMaxChain) {
-        const OpRec& nx = out.ops[oj];
-        if (nx.phase != 1 || nx.type != OP_BIG || nx.begin != end) break;
+      const int s0 = op.begin;
+      int f = 0;
+      while (oi + 1 + f < out.ops.size()) {
+        const OpRec& nx = out.ops[oi + 1 + f];
+        if (nx.phase != 1 || nx.type != OP_BIG || nx.begin != s0 + 1 + f) break;
         const StepRec& st = out.steps[nx.begin];
-        const StepRec& pv = out.steps[end - 1];
-        if (!st.inplace || !is_reduce(st) || st.in[0].off != pv.out_off || st.out_rank < 1) break;
-        ++end;
-        ++oj;
+        const StepRec& pv = out.steps[nx.begin - 1];
+        if (!st.inplace || !is_reduce(st) || st.in[0].off != pv.out_off) break;
+        ++f;
       }
-      if (end - op.begin >= 2) {
-        const int m = end - op.begin;
-        const StepRec& h = out.steps[op.begin];
-        double unf = 0.0;
-        for (int k = op.begin; k < end; ++k) {
-          const StepRec& sk = out.steps[k];
-          unf += std::ldexp(1.0, sk.out_rank);
-          for (int t = 0; t < sk.n_in; ++t) unf += std::ldexp(1.0, (int)sk.in[t].rank);
-        }
+      if (f == 0) {
+        fused.push_back(op);
+        continue;
+      }
+      double unf = 0.0;
+      if (is_reduce(out.steps[s0])) {
+        const int take = std::min(f, kMaxChain - 1);
+        const int end = s0 + 1 + take;
+        for (int k = s0; k < end; ++k) unf += step_elems(out.steps[k]);
+        const StepRec& h = out.steps[s0];
+        const int m = end - s0;
         double fz = std::ldexp(1.0, (int)h.in[0].rank) + std::ldexp(1.0, (int)h.in[0].rank - m);
-        for (int k = op.begin; k < end; ++k) fz += 2.0 * (out.steps[k].n_in - 1);
+        for (int k = s0; k < end; ++k) fz += 2.0 * (out.steps[k].n_in - 1);
         out.elems_slice += fz - unf;
         out.elems_big_slice += fz - unf;
         out.big_launches_slice -= (uint64_t)(m - 1);
-        fused.push_back(OpRec{OP_CHAIN, op.begin, end, 1});
-        oi = oj - 1;
-      } else {
-        fused.push_back(op);
+        fused.push_back(OpRec{OP_CHAIN, s0, end, 1});
+        oi += take;
+        continue;
       }
+      // merge head: choose the number of followers g to fuse
+      const StepRec& h = out.steps[s0];
+      int best_g = 0;
+      double best_t = t_elems(step_elems(h)) + t_chain(h.out_rank + 0, f) * 1.0;
+      int n_inputs = h.n_in;
+      for (int g = 1; g <= std::min(f, kMaxGroupPlan - 1); ++g) {
+        n_inputs += out.steps[s0 + g].n_in - 1;
+        if (n_inputs > kMaxIn) break;
+        const int rest = f - g;
+        const double t = t_group(s0, g) + t_chain(out.steps[s0 + g].out_rank, rest);
+        if (t < best_t) { best_t = t; best_g = g; }
+      }
+      if (best_g == 0) {
+        fused.push_back(op);
+        continue;
+      }
+      const int end = s0 + 1 + best_g;
+      for (int k = s0; k < end; ++k) unf += step_elems(out.steps[k]);
+      double fz = std::ldexp(1.0, out.steps[end - 1].out_rank);
+      for (int t = 0; t < h.n_in; ++t) fz += std::ldexp(1.0, (int)h.in[t].rank);
+      for (int k = s0 + 1; k < end; ++k) fz += 2.0 * (out.steps[k].n_in - 1);
+      out.elems_slice += fz - unf;
+      out.elems_big_slice += fz - unf;
+      out.big_launches_slice -= (uint64_t)best_g;
+      fused.push_back(OpRec{OP_GROUP, s0, end, 1});
+      oi += best_g;
     }
     out.ops.swap(fused);
   }

@@ -282,7 +282,8 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
   }
   for (const auto& o : pl->ops)
     if (o.begin < 0 || o.end > h.n_steps || o.begin >= o.end ||
-        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN) ||
+        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN && o.type != OP_GROUP) ||
+        (o.type == OP_GROUP && (o.end - o.begin > kMaxGroupPlan || o.end - o.begin < 2)) ||
         (o.type == OP_CHAIN && (o.end - o.begin > kMaxChain || pl->steps[o.end - 1].out_rank < 1)) ||
         (o.type == OP_BIG && pl->steps[o.begin].out_rank < 1))
       return fail(TN_E_PLAN, "tn_plan_load: bad op record");
@@ -346,8 +347,8 @@ extern "C" tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int
   *n = (int64_t)plan->steps.size();
   std::vector<char> big(plan->steps.size(), 0);
   for (const auto& op : plan->ops)
-    if (op.type == OP_BIG || op.type == OP_CHAIN)
-      for (int i = op.begin; i < op.end; ++i) big[i] = op.type == OP_BIG ? 1 : 2;
+    if (op.type == OP_BIG || op.type == OP_CHAIN || op.type == OP_GROUP)
+      for (int i = op.begin; i < op.end; ++i) big[i] = op.type == OP_BIG ? 1 : (op.type == OP_CHAIN ? 2 : 3);
   for (int64_t i = 0; out && i < cap && i < *n; ++i) {
     const StepRec& s = plan->steps[i];
     tn_step_info_t& o = out[i];
@@ -529,97 +530,182 @@ void launch_bucket_n(BigArgs a, cudaStream_t st) {
     k_bucket<T, NIN, uint32_t><<<grid, kBucketThreads, smem, st>>>(a);
 }
 
-// Specialised path: classify inputs into direct / staged / constant groups (kernels.cuh
-// k_bucket_t).  Returns false when the step does not fit (then the generic k_bucket runs).
-template <typename T, typename OffT, int NDIR, int NSTG>
-void launch_t(const TArgs& ta, unsigned grid, size_t smem, cudaStream_t st) {
-  k_bucket_t<T, OffT, NDIR, NSTG><<<grid, kBucketThreads, smem, st>>>(ta);
+// ---------------------------------------------------------------- k_group_t host side
+struct GIn {
+  const void* ptr;
+  uint64_t out_mask;   // output bits present (relative to the group output)
+  uint32_t pv;         // F_t(o) = ins0(pext(o, out_mask), pv)
+  uint32_t rank;       // bits of the input (for 32/64-bit offsets)
+  bool full;           // holds every output bit and every summed bit (read exactly once)
+  uint64_t gx[1 << kMaxGroup];
+};
+struct GDesc {
+  void* out;
+  int out_rank;
+  int M;
+  int n;
+  GIn in[kMaxIn];
+};
+
+uint64_t host_fmap(uint64_t o, uint64_t mask, uint32_t pv) {
+  const uint64_t r = host_pext(o, mask);
+  const uint64_t lo = r & ((1ull << pv) - 1);
+  return lo | ((r >> pv) << (pv + 1));
 }
 
-template <typename T, typename OffT>
-bool launch_t_dispatch(const TArgs& ta, int ndir, int nstg, unsigned grid, size_t smem, cudaStream_t st) {
-#define TN_T(D, G) if (ndir == D && nstg == G) { launch_t<T, OffT, D, G>(ta, grid, smem, st); return true; }
-  TN_T(1, 0) TN_T(2, 0) TN_T(3, 0) TN_T(0, 1) TN_T(1, 1) TN_T(2, 1) TN_T(0, 2) TN_T(1, 2) TN_T(2, 2)
-  TN_T(0, 3) TN_T(1, 3) TN_T(0, 4)
-#undef TN_T
+template <typename T, typename OffT, int NDIR, int NSTG, int M, int NDV>
+void launch_g(const GArgs& ga, unsigned grid, size_t smem, cudaStream_t st) {
+  k_group_t<T, OffT, NDIR, NSTG, M, NDV><<<grid, kBucketThreads, smem, st>>>(ga);
+}
+
+template <typename T, typename OffT, int M>
+bool dispatch_g(const GArgs& ga, int nd, int ns, int ndv, unsigned grid, size_t smem, cudaStream_t st) {
+#define TN_G(D, S, V) \
+  if (nd == D && ns == S && ndv == V) { launch_g<T, OffT, D, S, M, V>(ga, grid, smem, st); return true; }
+  TN_G(1, 0, 1) TN_G(2, 0, 2) TN_G(0, 1, 0) TN_G(1, 1, 1) TN_G(0, 2, 0) TN_G(2, 1, 2) TN_G(1, 2, 1)
+  TN_G(1, 0, 0) TN_G(2, 0, 1) TN_G(1, 1, 0) TN_G(2, 1, 1)
+  if constexpr (M == 1) {
+    TN_G(3, 0, 3) TN_G(2, 2, 2) TN_G(0, 3, 0) TN_G(1, 3, 1) TN_G(0, 4, 0) TN_G(3, 0, 2) TN_G(2, 0, 0)
+  }
+#undef TN_G
   return false;
 }
 
+// Classify the inputs (direct / staged / constant), build GArgs and launch k_group_t.  Returns
+// false when the shape has no instantiation (the caller then runs the generic path).
 template <typename T>
-bool try_launch_specialised(const BigArgs& in, cudaStream_t st) {
+bool try_launch_group(const GDesc& g, cudaStream_t st) {
   constexpr int TB = TileBits<T>::v;
   constexpr uint64_t TILE = 1ull << TB;
-  if (in.out_rank <= TB) return false;
+  if (g.out_rank <= TB || g.M < 1 || g.M > kMaxGroup || g.n < 1 || g.n > kMaxIn) return false;
   const uint64_t inner = TILE - 1;
-  BigArgs a = in;
-  plan_order<T>(a);
-  int dir[kMaxIn], stg[kMaxIn], cst[kMaxIn], nd = 0, ns = 0, nc = 0;
+  const int NX = 1 << g.M;
+  // traversal order of the tile bits: bits absent from the two largest varying inputs first
+  int big[2] = {-1, -1};
+  for (int t = 0; t < g.n; ++t) {
+    const int r = __builtin_popcountll(g.in[t].out_mask);
+    if (big[0] < 0 || r > __builtin_popcountll(g.in[big[0]].out_mask)) { big[1] = big[0]; big[0] = t; }
+    else if (big[1] < 0 || r > __builtin_popcountll(g.in[big[1]].out_mask)) big[1] = t;
+  }
+  auto has = [&](int t, int b) { return t >= 0 && ((g.in[t].out_mask >> b) & 1); };
+  std::vector<int> bits;
+  for (int b = TB; b < 64; ++b) bits.push_back(b);
+  std::stable_sort(bits.begin(), bits.end(), [&](int x, int y) {
+    if (has(big[0], x) != has(big[0], y)) return !has(big[0], x);
+    if (has(big[1], x) != has(big[1], y)) return !has(big[1], x);
+    return x < y;
+  });
+  std::stable_partition(bits.begin(), bits.end(), [&](int b) { return b < g.out_rank; });
+
+  int dir[kMaxIn], dirs[kMaxIn], stg[kMaxIn], cst[kMaxIn], nd = 0, nds = 0, ns = 0, nc = 0;
+  int nlow_of[kMaxIn] = {0};
+  uint32_t nparts_of[kMaxIn] = {0};
   uint32_t soff = 0;
-  for (int t = 0; t < a.n_in; ++t) {
-    const uint64_t lowm = a.out_mask[t] & inner;
+  for (int t = 0; t < g.n; ++t) {
+    const GIn& in = g.in[t];
+    const uint64_t lowm = in.out_mask & inner;
     const int nlow = __builtin_popcountll(lowm);
     if (nlow == 0) { cst[nc++] = t; continue; }
-    // direct 16-byte loads need output bit 0 at input position 0 (always true for c128)
-    const bool vec_ok = (VecT<T>::n == 1) || ((a.out_mask[t] & 1) && a.pv[t] != 0);
-    if (nlow == TB) {
-      if (!vec_ok) return false;
-      dir[nd++] = t;
-      continue;
-    }
-    // staging: the tile's low output bits must be the input's lowest positions (pv above them)
-    uint64_t r = 0;
-    {
-      uint64_t m = a.out_mask[t];
-      int k = 0;
-      for (int b = 0; b < 64 && m; ++b)
-        if ((m >> b) & 1) { if ((lowm >> b) & 1) r |= 1ull << k; ++k; m &= ~(1ull << b); }
-    }
-    const uint32_t need = 2u << nlow;
-    const bool stageable = (int)a.pv[t] >= nlow && r == (1ull << nlow) - 1 && nlow <= 10 &&
+    const bool vec_ok = (VecT<T>::n == 1) || ((in.out_mask & 1) && in.pv != 0);
+    // staging needs the tile's low output bits at the input's lowest positions
+    const bool contig = host_fmap(lowm, in.out_mask, in.pv) == (1ull << nlow) - 1;
+    std::vector<uint64_t> parts;
+    for (int x = 0; x < NX; ++x)
+      if (std::find(parts.begin(), parts.end(), in.gx[x]) == parts.end()) parts.push_back(in.gx[x]);
+    const uint32_t need = (uint32_t)parts.size() << nlow;
+    const bool stageable = contig && nlow < TB && (nlow <= TB - 3 || !vec_ok) &&
                            (soff + need) * sizeof(T) * 2 <= 48 * 1024;
     if (stageable) {
+      nlow_of[t] = nlow;
+      nparts_of[t] = (uint32_t)parts.size();
       stg[ns++] = t;
       soff += need;
     } else if (vec_ok) {
-      dir[nd++] = t;   // large partial input: direct loads, intra-tile reuse from L1
+      dir[nd++] = t;
     } else {
-      return false;
+      dirs[nds++] = t;   // direct, 8-byte loads
     }
   }
+  const int ndv = nd;
+  for (int i = 0; i < nds; ++i) dir[nd++] = dirs[i];
   if (nd + ns == 0) return false;
-  TArgs ta;
-  std::memset(&ta, 0, sizeof(ta));
-  ta.out = a.out;
-  ta.out_rank = a.out_rank;
-  ta.nc = nc;
-  std::memcpy(ta.perm, a.perm, sizeof(ta.perm));
+  GArgs ga;   // host copy; passed by value as the launch parameters
+  std::memset(&ga, 0, sizeof(ga));
+  ga.out = g.out;
+  ga.out_rank = g.out_rank;
+  ga.nc = nc;
+  for (int i = 0; i < 64 - TB; ++i) ga.perm[i] = (uint8_t)(bits[i] - TB);
+  const uint64_t full = (1ull << g.out_rank) - 1;
   int k = 0;
   uint32_t off = 0;
+  bool wide = false;
   auto put = [&](int t) {
-    ta.in[k] = a.in[t];
-    ta.out_mask[k] = a.out_mask[t];
-    ta.pv[k] = a.pv[t];
-    ta.stream[k] = (a.flags[t] & F_STREAM) ? 1u : 0u;
+    const GIn& in = g.in[t];
+    ga.in[k] = in.ptr;
+    ga.out_mask[k] = in.out_mask;
+    ga.pv[k] = in.pv;
+    ga.stream[k] = (in.full && in.out_mask == full && g.out_rank >= 16) ? 1u : 0u;
+    for (int x = 0; x < NX; ++x) ga.gx[k][x] = in.gx[x];
+    wide |= in.rank > 32;
     ++k;
   };
   for (int i = 0; i < nd; ++i) put(dir[i]);
   for (int i = 0; i < ns; ++i) {
     const int t = stg[i];
-    const int nlow = __builtin_popcountll(a.out_mask[t] & inner);
-    ta.nlow[k] = (uint32_t)nlow;
-    ta.stage_off[k] = off;
-    off += 2u << nlow;
+    std::vector<uint64_t> parts;
+    for (int x = 0; x < NX; ++x) {
+      auto it = std::find(parts.begin(), parts.end(), g.in[t].gx[x]);
+      uint32_t pi;
+      if (it == parts.end()) {
+        pi = (uint32_t)parts.size();
+        parts.push_back(g.in[t].gx[x]);
+        ga.rep[k][pi] = (uint8_t)x;
+      } else {
+        pi = (uint32_t)(it - parts.begin());
+      }
+      ga.sx[k][x] = off + (pi << nlow_of[t]);
+    }
+    ga.nlow[k] = (uint32_t)nlow_of[t];
+    ga.nparts[k] = nparts_of[t];
+    off += nparts_of[t] << nlow_of[t];
     put(t);
   }
   for (int i = 0; i < nc; ++i) put(cst[i]);
-  ta.stage_elems = off;
-  const uint64_t tiles = ((1ull << a.out_rank) + TILE - 1) / TILE;
+  ga.stage_elems = off;
+  const uint64_t tiles = ((1ull << g.out_rank) + TILE - 1) / TILE;
   const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 4);
   const size_t smem = (size_t)off * sizeof(T) * 2;
-  bool wide = false;
-  for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
-  return wide ? launch_t_dispatch<T, uint64_t>(ta, nd, ns, grid, smem, st)
-              : launch_t_dispatch<T, uint32_t>(ta, nd, ns, grid, smem, st);
+  if (wide) return g.M == 1 ? dispatch_g<T, uint64_t, 1>(ga, nd, ns, ndv, grid, smem, st) : false;
+  switch (g.M) {
+    case 1: return dispatch_g<T, uint32_t, 1>(ga, nd, ns, ndv, grid, smem, st);
+    case 2: return dispatch_g<T, uint32_t, 2>(ga, nd, ns, ndv, grid, smem, st);
+    case 3: return dispatch_g<T, uint32_t, 3>(ga, nd, ns, ndv, grid, smem, st);
+    case 4: return dispatch_g<T, uint32_t, 4>(ga, nd, ns, ndv, grid, smem, st);
+    case 5: return dispatch_g<T, uint32_t, 5>(ga, nd, ns, ndv, grid, smem, st);
+    default: return false;
+  }
+}
+
+// single bucket step as a group with M = 1 (G_t(x) = x << pv_t)
+template <typename T>
+bool try_launch_specialised(const BigArgs& a, cudaStream_t st) {
+  GDesc g;
+  std::memset(&g, 0, sizeof(g));
+  g.out = a.out;
+  g.out_rank = a.out_rank;
+  g.M = 1;
+  g.n = a.n_in;
+  const uint64_t full = a.out_rank >= 64 ? ~0ull : ((1ull << a.out_rank) - 1);
+  for (int t = 0; t < a.n_in; ++t) {
+    g.in[t].ptr = a.in[t];
+    g.in[t].out_mask = a.out_mask[t];
+    g.in[t].pv = a.pv[t];
+    g.in[t].rank = (uint32_t)__builtin_popcountll(a.out_mask[t]) + 1;
+    g.in[t].full = a.out_mask[t] == full;
+    g.in[t].gx[0] = 0;
+    g.in[t].gx[1] = 1ull << a.pv[t];
+  }
+  return try_launch_group<T>(g, st);
 }
 
 template <typename T>
@@ -649,43 +735,67 @@ cudaEvent_t pool_event(tn_plan* pl) {
 }
 
 template <typename T>
+uint64_t slice_off_of(const InRec& in, uint64_t j) {
+  return in.slice_mask ? (host_pext(j, in.slice_mask) << in.rank) : 0ull;
+}
+
+struct ProfScope {
+  tn_plan* pl;
+  cudaStream_t st;
+  ProfRec pr{};
+  ProfScope(tn_plan* p, cudaStream_t s, double bytes, int b, int e, int kind, int out_rank) : pl(p), st(s) {
+    if (!pl->profiling) return;
+    pr.a = pool_event(pl);
+    pr.b = pool_event(pl);
+    pr.bytes = bytes;
+    pr.step_begin = b;
+    pr.step_end = e;
+    pr.kind = kind;
+    pr.out_rank = out_rank;
+    cudaEventRecord(pr.a, st);
+  }
+  bool cancel = false;
+  ~ProfScope() {
+    if (!pl->profiling) return;
+    if (cancel) {
+      pl->ev_pool.push_back(pr.a);
+      pl->ev_pool.push_back(pr.b);
+      return;
+    }
+    cudaEventRecord(pr.b, st);
+    pl->prof.push_back(pr);
+  }
+};
+
+// one standalone bucket step (k_group_t with M = 1, else the generic k_bucket)
+template <typename T>
+void run_big(tn_plan* pl, int si, T* ws, uint64_t j, cudaStream_t st) {
+  const StepRec& s = pl->steps[si];
+  BigArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.out = ws + s.out_off;
+  a.out_rank = s.out_rank;
+  a.n_in = s.n_in;
+  double bytes = std::ldexp((double)sizeof(T), s.out_rank);
+  for (int t = 0; t < s.n_in; ++t) {
+    const InRec& in = s.in[t];
+    a.in[t] = ws + in.off + slice_off_of<T>(in, j);
+    a.out_mask[t] = in.out_mask;
+    a.pv[t] = in.pv;
+    a.flags[t] = in.flags | ((t == 0 && s.inplace) ? 1u : 0u);
+    bytes += std::ldexp((double)sizeof(T), (int)in.rank);
+  }
+  ProfScope ps(pl, st, bytes, si, si + 1, 1, s.out_rank);
+  launch_bucket<T>(a, st);
+}
+
+template <typename T>
 tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, uint64_t j,
                   cudaStream_t st) {
   for (int oi = op_b; oi < op_e; ++oi) {
     const OpRec& op = pl->ops[oi];
     if (op.type == OP_BIG) {
-      const StepRec& s = pl->steps[op.begin];
-      BigArgs a;
-      std::memset(&a, 0, sizeof(a));
-      a.out = ws + s.out_off;
-      a.out_rank = s.out_rank;
-      a.n_in = s.n_in;
-      double bytes = std::ldexp((double)sizeof(T), s.out_rank);
-      for (int t = 0; t < s.n_in; ++t) {
-        const InRec& in = s.in[t];
-        const uint64_t soff = in.slice_mask ? (host_pext(j, in.slice_mask) << in.rank) : 0;
-        a.in[t] = ws + in.off + soff;
-        a.out_mask[t] = in.out_mask;
-        a.pv[t] = in.pv;
-        a.flags[t] = in.flags | ((t == 0 && s.inplace) ? 1u : 0u);
-        bytes += std::ldexp((double)sizeof(T), (int)in.rank);
-      }
-      ProfRec pr{};
-      if (pl->profiling) {
-        pr.a = pool_event(pl);
-        pr.b = pool_event(pl);
-        pr.bytes = bytes;
-        pr.step_begin = op.begin;
-        pr.step_end = op.end;
-        pr.kind = 1;
-        pr.out_rank = s.out_rank;
-        cudaEventRecord(pr.a, st);
-      }
-      launch_bucket<T>(a, st);
-      if (pl->profiling) {
-        cudaEventRecord(pr.b, st);
-        pl->prof.push_back(pr);
-      }
+      run_big<T>(pl, op.begin, ws, j, st);
     } else if (op.type == OP_CHAIN) {
       const StepRec& h = pl->steps[op.begin];
       const StepRec& last = pl->steps[op.end - 1];
@@ -694,36 +804,69 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       c.m = op.end - op.begin;
       c.out = ws + last.out_off;
       c.out_rank = last.out_rank;
-      auto soff = [&](const InRec& in) {
-        return in.slice_mask ? (host_pext(j, in.slice_mask) << in.rank) : 0ull;
-      };
-      c.A = ws + h.in[0].off + soff(h.in[0]);
+      c.A = ws + h.in[0].off + slice_off_of<T>(h.in[0], j);
       for (int i = 0; i < c.m; ++i) {
         const StepRec& sk = pl->steps[op.begin + i];
         c.nw[i] = sk.n_in - 1;
-        for (int k = 1; k < sk.n_in; ++k) c.w[i][k - 1] = ws + sk.in[k].off + soff(sk.in[k]);
+        for (int k = 1; k < sk.n_in; ++k) c.w[i][k - 1] = ws + sk.in[k].off + slice_off_of<T>(sk.in[k], j);
       }
       const double bytes = (std::ldexp(1.0, (int)h.in[0].rank) + std::ldexp(1.0, c.out_rank)) * sizeof(T);
-      ProfRec pr{};
-      if (pl->profiling) {
-        pr.a = pool_event(pl);
-        pr.b = pool_event(pl);
-        pr.bytes = bytes;
-        pr.step_begin = op.begin;
-        pr.step_end = op.end;
-        pr.kind = 2;
-        pr.out_rank = c.out_rank;
-        cudaEventRecord(pr.a, st);
-      }
+      ProfScope ps(pl, st, bytes, op.begin, op.end, 2, c.out_rank);
       constexpr int VEC = VecT<T>::n;
       const uint64_t work = ((1ull << c.out_rank) + VEC - 1) / VEC;
       const uint64_t blocks = (work + kBucketThreads - 1) / kBucketThreads;
       const unsigned grid = (unsigned)std::min<uint64_t>(blocks, (uint64_t)num_sms() * 8);
       k_chain<T><<<grid, kBucketThreads, 0, st>>>(c);
-      if (pl->profiling) {
-        cudaEventRecord(pr.b, st);
-        pl->prof.push_back(pr);
+    } else if (op.type == OP_GROUP) {
+      // head step + (M-1) in-place reduce followers with rank-1 weights, summed in one pass
+      const StepRec& h = pl->steps[op.begin];
+      const StepRec& last = pl->steps[op.end - 1];
+      GDesc g;
+      std::memset(&g, 0, sizeof(g));
+      const int M = op.end - op.begin;
+      const int Rf = last.out_rank;
+      const uint64_t low = (1ull << Rf) - 1, xrest = (1ull << (M - 1)) - 1;
+      const uint64_t hfull = (1ull << h.out_rank) - 1;
+      g.out = ws + last.out_off;
+      g.out_rank = Rf;
+      g.M = M;
+      double bytes = std::ldexp(1.0, Rf);
+      bool ok = true;
+      for (int t = 0; t < h.n_in && ok; ++t) {
+        const InRec& in = h.in[t];
+        GIn& gi = g.in[g.n++];
+        gi.ptr = ws + in.off + slice_off_of<T>(in, j);
+        gi.out_mask = in.out_mask & low;
+        gi.pv = in.pv;
+        gi.rank = in.rank;
+        gi.full = in.out_mask == hfull;
+        for (int x = 0; x < (1 << M); ++x)
+          gi.gx[x] = host_fmap(((uint64_t)x & xrest) << Rf, in.out_mask, in.pv) +
+                     ((uint64_t)((x >> (M - 1)) & 1) << in.pv);
+        bytes += std::ldexp(1.0, (int)in.rank);
       }
+      for (int i = 1; i < M && ok; ++i) {
+        const StepRec& sk = pl->steps[op.begin + i];
+        for (int k = 1; k < sk.n_in; ++k) {
+          if (g.n >= kMaxIn) { ok = false; break; }
+          GIn& gi = g.in[g.n++];
+          gi.ptr = ws + sk.in[k].off + slice_off_of<T>(sk.in[k], j);
+          gi.out_mask = 0;
+          gi.pv = 0;
+          gi.rank = 1;
+          gi.full = false;
+          for (int x = 0; x < (1 << M); ++x) gi.gx[x] = (uint64_t)((x >> (M - 1 - i)) & 1);
+          bytes += 2.0;
+        }
+      }
+      bool launched = false;
+      if (ok) {
+        ProfScope ps(pl, st, bytes * sizeof(T), op.begin, op.end, 3, Rf);
+        launched = try_launch_group<T>(g, st);
+        ps.cancel = !launched;
+      }
+      if (!launched)   // no instantiation for this shape: run the steps one by one
+        for (int si = op.begin; si < op.end; ++si) run_big<T>(pl, si, ws, j, st);
     } else {
       k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
                                                   dt.scalars, nullptr, 0);
