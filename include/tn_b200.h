@@ -42,7 +42,12 @@ typedef enum {
 } tn_status;
 
 typedef enum { TN_KIND_AMPLITUDE = 0, TN_KIND_ENERGY = 1 } tn_kind;
-typedef enum { TN_ORDER_MIN_FILL = 0, TN_ORDER_MIN_DEGREE = 1 } tn_orderer;
+typedef enum {
+  TN_ORDER_MIN_FILL = 0,    /* greedy, fewest fill-in edges first */
+  TN_ORDER_MIN_DEGREE = 1,  /* greedy, lowest degree first */
+  TN_ORDER_RGREEDY = 2,     /* "rgreedy": p(v) ~ exp(-N_G(v)/tau), best of q runs */
+  TN_ORDER_RGREEDY_FILL = 3 /* the same Boltzmann sampling on the fill-in count (extension) */
+} tn_orderer;
 
 /* Planner options (§5.1 ordering; §5.3 step-dependent slicing). */
 typedef struct {
@@ -56,7 +61,11 @@ typedef struct {
   int32_t max_width;      /* > 0: fail with TN_E_TOO_WIDE if the contraction width exceeds it */
   int32_t small_log2;     /* steps whose output has <= small_log2 indices run in the batched
                              interpreter kernel; < 0 selects the default (12) */
-  int32_t reserved[4];    /* must be 0 */
+  int32_t rg_q;           /* rgreedy: number of randomized runs q (>= 1; 0 -> 8); the deterministic
+                             greedy run is always included, so the result is never worse */
+  int32_t rg_tau_milli;   /* rgreedy: temperature tau x 1000 (0 -> tau = 0.5) */
+  uint32_t rg_seed;       /* rgreedy: seed (runs are deterministic for a seed) */
+  int32_t reserved;       /* must be 0 */
 } tn_build_opts;
 
 typedef struct {

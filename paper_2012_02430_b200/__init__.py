@@ -21,7 +21,8 @@ from ._binding import (TN_C64, TN_C128, TN_KIND_AMPLITUDE, TN_KIND_ENERGY, TN_OR
 __all__ = ["Plan", "TN_C64", "TN_C128", "TN_KIND_AMPLITUDE", "TN_KIND_ENERGY", "TN_ORDER_MIN_FILL",
            "TN_ORDER_MIN_DEGREE", "TnError", "build_plan", "select_sliced_plan"]
 
-ORDERERS = {"min-fill": TN_ORDER_MIN_FILL, "min-degree": TN_ORDER_MIN_DEGREE}
+ORDERERS = {"min-fill": TN_ORDER_MIN_FILL, "min-degree": TN_ORDER_MIN_DEGREE, "rgreedy": B.TN_ORDER_RGREEDY,
+            "rgreedy-fill": B.TN_ORDER_RGREEDY_FILL}
 
 
 class Plan:
@@ -109,31 +110,41 @@ class Plan:
 
 
 def build_plan(graph, p: int, kind: str = "amplitude", orderer: str = "min-fill", n_sliced: int = 0,
-               r: int = 0, max_width: int = 0, small_log2: int = -1) -> Plan:
+               r: int = 0, max_width: int = 0, small_log2: int = -1, rg_q: int = 0, rg_tau: float = 0.0,
+               rg_seed: int = 0) -> Plan:
     """Plan for a tn_inputs.Graph (or any object with .n and .edges)."""
     k = TN_KIND_AMPLITUDE if kind == "amplitude" else TN_KIND_ENERGY
     buf = B.tn_plan_build(graph.n, graph.edges, p, kind=k, orderer=ORDERERS[orderer], n_sliced=n_sliced,
-                          r=r, max_width=max_width, small_log2=small_log2)
+                          r=r, max_width=max_width, small_log2=small_log2, rg_q=rg_q, rg_tau=rg_tau,
+                          rg_seed=rg_seed)
     plan = Plan(buf)
     plan.orderer = orderer
     return plan
 
 
+DEFAULT_ORDERERS = (("min-fill", 0, 0.0), ("min-degree", 0, 0.0), ("rgreedy", 8, 0.5), ("rgreedy-fill", 8, 0.5))
+
+
 def select_sliced_plan(graph, p: int, max_width: int, k_min: int = 0, k_max: int = 12,
-                       orderers: Sequence[str] = ("min-fill", "min-degree"), r: int = 0,
-                       small_log2: int = -1) -> Tuple[Plan, List[dict]]:
+                       orderers=DEFAULT_ORDERERS, r: int = 0, small_log2: int = -1,
+                       rg_seed: int = 0) -> Tuple[Plan, List[dict]]:
     """Reading A11: the smallest k in [k_min, k_max] whose width <= max_width; among the
-    orderers at that k, the plan with fewer predicted bytes (ties -> min-degree)."""
+    orderers at that k (greedy min-fill / min-degree, and rgreedy,
+    PAPER.md:465-475, given as (name, q, tau)), the plan with the fewest predicted bytes
+    (ties -> the earlier orderer in the list)."""
     tried: List[dict] = []
     for k in range(k_min, k_max + 1):
         cands = []
-        for o in orderers:
-            pl = build_plan(graph, p, "amplitude", o, n_sliced=k, r=r, small_log2=small_log2)
+        for idx, spec in enumerate(orderers):
+            o, q, tau = spec if isinstance(spec, tuple) else (spec, 0, 0.0)
+            pl = build_plan(graph, p, "amplitude", o, n_sliced=k, r=r, small_log2=small_log2,
+                            rg_q=q, rg_tau=tau, rg_seed=rg_seed)
+            pl.orderer = o if not q else f"{o}(q={q},tau={tau})"
             total = pl.info["pred_bytes_per_slice"][0] * pl.n_slices + pl.info["pred_bytes_prefix"][0]
-            tried.append({"k": k, "orderer": o, "width": pl.width, "pred_bytes_c64": total,
+            tried.append({"k": k, "orderer": pl.orderer, "width": pl.width, "pred_bytes_c64": total,
                           "unsliced_width": pl.info["unsliced_width"], "slice_step": pl.info["slice_step"]})
             if pl.width <= max_width:
-                cands.append((total, 0 if o == "min-degree" else 1, pl))
+                cands.append((total, idx, pl))
         if cands:
             cands.sort(key=lambda c: (c[0], c[1]))
             return cands[0][2], tried

@@ -19,7 +19,7 @@ _lib = C.CDLL(LIB_PATH)
 
 TN_C64, TN_C128 = 0, 1
 TN_KIND_AMPLITUDE, TN_KIND_ENERGY = 0, 1
-TN_ORDER_MIN_FILL, TN_ORDER_MIN_DEGREE = 0, 1
+TN_ORDER_MIN_FILL, TN_ORDER_MIN_DEGREE, TN_ORDER_RGREEDY, TN_ORDER_RGREEDY_FILL = 0, 1, 2, 3
 STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4: "TN_E_NOMEM",
           -5: "TN_E_CUDA", -6: "TN_E_DTYPE"}
 
@@ -37,7 +37,8 @@ class TnError(RuntimeError):
 
 class tn_build_opts(C.Structure):
     _fields_ = [("kind", C.c_int32), ("orderer", C.c_int32), ("n_sliced", C.c_int32), ("r", C.c_int32),
-                ("max_width", C.c_int32), ("small_log2", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("max_width", C.c_int32), ("small_log2", C.c_int32), ("rg_q", C.c_int32),
+                ("rg_tau_milli", C.c_int32), ("rg_seed", C.c_uint32), ("reserved", C.c_int32)]
 
 
 class tn_plan_info_t(C.Structure):
@@ -120,12 +121,14 @@ def tn_version() -> int:
 
 def tn_plan_build(n_qubits: int, edges, p: int, kind: int = TN_KIND_AMPLITUDE,
                   orderer: int = TN_ORDER_MIN_FILL, n_sliced: int = 0, r: int = 0,
-                  max_width: int = 0, small_log2: int = -1) -> bytes:
+                  max_width: int = 0, small_log2: int = -1, rg_q: int = 0, rg_tau: float = 0.0,
+                  rg_seed: int = 0) -> bytes:
     flat = []
     for e in edges:
         flat.extend((int(e[0]), int(e[1])))
     arr = (C.c_int32 * max(1, len(flat)))(*flat)
-    opts = tn_build_opts(kind, orderer, n_sliced, r, max_width, small_log2)
+    opts = tn_build_opts(kind, orderer, n_sliced, r, max_width, small_log2, rg_q, int(round(rg_tau * 1000)),
+                         rg_seed, 0)
     buf, ln = _P(), C.c_size_t()
     _check(_lib.tn_plan_build(n_qubits, len(flat) // 2, arr, p, C.byref(opts), C.byref(buf), C.byref(ln)),
            "tn_plan_build")

@@ -269,10 +269,77 @@ Ordering greedy_order(BitGraph g, int orderer) {
   return o;
 }
 
+// ============================================================== rgreedy
+namespace {
+inline uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+struct Rng {
+  uint64_t s;
+  double uniform() {
+    s = mix64(s);
+    return (s >> 11) * (1.0 / 9007199254740992.0);
+  }
+};
+
+// one randomized elimination: vertex v is chosen with probability ~ exp(-key(v)/tau), key =
+// degree (rgreedy) or fill-in (rgreedy-fill)
+Ordering boltzmann_run(BitGraph g, bool by_fill, double tau, uint64_t seed) {
+  const int n = g.size();
+  Ordering o;
+  Rng rng{seed};
+  std::vector<double> w(n);
+  while (g.n_alive() > 0) {
+    int64_t kmin = INT64_MAX;
+    std::vector<int64_t> key(n, 0);
+    for (int v = 0; v < n; ++v) {
+      if (!g.alive(v)) continue;
+      key[v] = by_fill ? g.fill_in(v) : g.degree(v);
+      kmin = std::min(kmin, key[v]);
+    }
+    double tot = 0.0;
+    for (int v = 0; v < n; ++v) {
+      w[v] = g.alive(v) ? std::exp(-(double)(key[v] - kmin) / tau) : 0.0;
+      tot += w[v];
+    }
+    double u = rng.uniform() * tot;
+    int pick = -1;
+    for (int v = 0; v < n; ++v) {
+      if (!g.alive(v)) continue;
+      pick = v;
+      u -= w[v];
+      if (u <= 0.0) break;
+    }
+    const int d = g.degree(pick);
+    o.order.push_back(pick);
+    o.degrees.push_back(d);
+    o.width = std::max(o.width, d);
+    o.cost += std::ldexp(1.0, d);
+    g.eliminate(pick);
+  }
+  return o;
+}
+}  // namespace
+
+Ordering order_graph(const BitGraph& g, const OrderSpec& spec, uint64_t salt) {
+  if (spec.orderer == TN_ORDER_MIN_FILL || spec.orderer == TN_ORDER_MIN_DEGREE)
+    return greedy_order(g, spec.orderer);
+  const bool by_fill = spec.orderer == TN_ORDER_RGREEDY_FILL;
+  Ordering best = greedy_order(g, by_fill ? TN_ORDER_MIN_FILL : TN_ORDER_MIN_DEGREE);
+  for (int i = 0; i < spec.q; ++i) {
+    Ordering o = boltzmann_run(g, by_fill, spec.tau, mix64(spec.seed ^ mix64(salt * 1000003ull + i)));
+    if (o.width < best.width || (o.width == best.width && o.cost < best.cost)) best = std::move(o);
+  }
+  return best;
+}
+
 // ============================================================== step-dependent slicing
-Schedule slice_search(const BitGraph& g0, int n, int r, int orderer) {
+Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec) {
   Schedule sch;
-  Ordering full0 = greedy_order(g0, orderer);
+  Ordering full0 = order_graph(g0, spec, 0);
   sch.unsliced_width = full0.width;
   if (n <= 0) {
     sch.residual = full0.order;
@@ -290,7 +357,7 @@ Schedule slice_search(const BitGraph& g0, int n, int r, int orderer) {
   std::vector<int> phaseB_prefix;
   while (n_done < n) {
     const int rr = std::min(r, n - n_done);
-    Ordering full = first_round ? full0 : greedy_order(g, orderer);
+    Ordering full = first_round ? full0 : order_graph(g, spec, 1000 + n_done);
     int peak = 0;
     for (size_t i = 0; i < full.degrees.size(); ++i)
       if (full.degrees[i] > full.degrees[peak]) peak = (int)i;
@@ -318,7 +385,7 @@ Schedule slice_search(const BitGraph& g0, int n, int r, int orderer) {
       std::vector<int> S(cand.begin(), cand.begin() + rr);
       BitGraph gr = gs;
       for (int v : S) gr.remove(v);
-      Ordering res = greedy_order(gr, orderer);
+      Ordering res = order_graph(gr, spec, 1 + s + 7919ull * n_done);
       const int w = std::max(pmax, res.width);
       const double cost = prefix_cost + pcost + std::ldexp(res.cost, n_done + rr);
       // best: smaller width, then fewer predicted operations, then smaller s (reading A10)
@@ -345,7 +412,7 @@ Schedule slice_search(const BitGraph& g0, int n, int r, int orderer) {
     n_done += rr;
     first_round = false;
   }
-  Ordering res = greedy_order(g, orderer);
+  Ordering res = order_graph(g, spec, 999983);
   sch.residual = phaseB_prefix;
   sch.residual.insert(sch.residual.end(), res.order.begin(), res.order.end());
   std::sort(sch.sliced.begin(), sch.sliced.end());

@@ -68,8 +68,18 @@ struct Ordering {
   double cost = 0.0;          // sum_i 2^{degree_i} ("C ~ 2^c")
 };
 
-// greedy orderers: orderer = TN_ORDER_MIN_FILL / TN_ORDER_MIN_DEGREE
+// orderer + rgreedy parameters
+struct OrderSpec {
+  int orderer = 0;       // TN_ORDER_*
+  int q = 1;             // rgreedy runs
+  double tau = 0.5;      // rgreedy temperature
+  uint64_t seed = 0;
+};
+
+// greedy orderers: TN_ORDER_MIN_FILL / TN_ORDER_MIN_DEGREE;
+// rgreedy: best of the deterministic greedy run and q Boltzmann-sampled runs
 Ordering greedy_order(BitGraph g, int orderer);
+Ordering order_graph(const BitGraph& g, const OrderSpec& spec, uint64_t salt = 0);
 
 struct Schedule {
   std::vector<int> prefix;    // phase A order (first slicing round's prefix, s indices)
@@ -80,7 +90,7 @@ struct Schedule {
 };
 
 // step-dependent slicing (Fig. slice_algo): n indices in rounds of r
-Schedule slice_search(const BitGraph& g0, int n, int r, int orderer);
+Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec);
 
 struct LoweredProgram {
   std::vector<LeafRec> leaves;

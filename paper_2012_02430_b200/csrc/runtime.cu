@@ -113,8 +113,15 @@ extern "C" tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int3
   if (!opts || !buf || !len || (n_edges > 0 && !edges) || n_qubits <= 0 || n_edges < 0)
     return fail(TN_E_INVAL, "tn_plan_build: null or negative argument");
   if (p < 1 || p > kMaxP) return fail(TN_E_INVAL, "tn_plan_build: p out of range [1, 16]");
-  if (opts->orderer != TN_ORDER_MIN_FILL && opts->orderer != TN_ORDER_MIN_DEGREE)
+  if (opts->orderer < TN_ORDER_MIN_FILL || opts->orderer > TN_ORDER_RGREEDY_FILL)
     return fail(TN_E_INVAL, "tn_plan_build: unknown orderer");
+  if (opts->rg_q < 0 || opts->rg_q > 4096 || opts->rg_tau_milli < 0)
+    return fail(TN_E_INVAL, "tn_plan_build: bad rgreedy parameters");
+  OrderSpec spec;
+  spec.orderer = opts->orderer;
+  spec.q = opts->rg_q == 0 ? 8 : opts->rg_q;
+  spec.tau = opts->rg_tau_milli == 0 ? 0.5 : opts->rg_tau_milli / 1000.0;
+  spec.seed = opts->rg_seed;
   if (opts->kind != TN_KIND_AMPLITUDE && opts->kind != TN_KIND_ENERGY)
     return fail(TN_E_INVAL, "tn_plan_build: unknown kind");
   if (opts->n_sliced < 0 || opts->n_sliced > 30 || opts->r < 0)
@@ -153,7 +160,7 @@ extern "C" tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int3
     for (size_t ni = 0; ni < nets.size(); ++ni) {
       const Network& net = nets[ni];
       BitGraph g = BitGraph::from_network(net);
-      Schedule sch = slice_search(g, opts->n_sliced, opts->r, opts->orderer);
+      Schedule sch = slice_search(g, opts->n_sliced, opts->r, spec);
       if (opts->max_width > 0 && sch.width > opts->max_width) {
         return fail(TN_E_TOO_WIDE, "contraction width " + std::to_string(sch.width) +
                                        " exceeds max_width " + std::to_string(opts->max_width));

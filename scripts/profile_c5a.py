@@ -20,8 +20,12 @@ def main():
     args = ap.parse_args()
     plan, g, ga, be, meta = bench.build_workload_plan(args.workload)
     steps = plan.steps()
-    big_a = [i for i, s in enumerate(steps) if s["standalone"] == 1 and s["phase"] == 0]
-    big_b = [i for i, s in enumerate(steps) if s["standalone"] == 1 and s["phase"] == 1]
+    # k_bucket / k_group launches: standalone steps and the head of every fused group
+    heads = lambda ph: [i for i, s in enumerate(steps) if s["phase"] == ph and (
+        s["standalone"] == 1 or (s["standalone"] == 3 and (i == 0 or steps[i - 1]["standalone"] != 3
+                                                             or steps[i]["n_in"] > 2)))]
+    big_a = heads(0)
+    big_b = heads(1)
     if args.list or args.print_skip is not None:
         if args.list:
             for o, i in enumerate(big_b):
