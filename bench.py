@@ -32,7 +32,7 @@ if ROOT not in sys.path:
 from tn_inputs import WORKLOADS, qaoa_angles, random_regular_graph  # noqa: E402
 
 MAX_WIDTH = {"C4a": 30, "C4b": 30, "C5a": 32, "C5b": 32, "C2": 62}
-K_RANGE = {"C4a": (8, 12), "C4b": (8, 12), "C5a": (3, 12), "C5b": (3, 14), "C2": (0, 0)}
+K_RANGE = {"C4a": (8, 12), "C4b": (8, 12), "C5a": (3, 8), "C5b": (8, 16), "C2": (0, 0)}
 METRIC = "sliced single-amplitude contraction throughput (QAOA MaxCut, 3-regular)"
 
 
@@ -47,7 +47,7 @@ def build_workload_plan(name: str = "C5a", seed: int = 0):
     kmin, kmax = K_RANGE.get(name, (0, 12))
     plan, tried = T.select_sliced_plan(g, w.p, MAX_WIDTH.get(name, 32), k_min=kmin, k_max=kmax)
     plan_s = time.perf_counter() - t0
-    meta = {"plan_s": plan_s, "tried": tried}
+    meta = {"plan_s": plan_s, "tried": tried, "candidates": len(tried)}
     return plan, g, ga, be, meta
 
 
@@ -170,7 +170,7 @@ def oracle_sample(plan, g, ga, be, budget_s: float = 15.0, max_width: int = 22):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C5a")

@@ -122,30 +122,43 @@ def build_plan(graph, p: int, kind: str = "amplitude", orderer: str = "min-fill"
     return plan
 
 
-DEFAULT_ORDERERS = (("min-fill", 0, 0.0), ("min-degree", 0, 0.0), ("rgreedy", 8, 0.5), ("rgreedy-fill", 8, 0.5))
+DEFAULT_ORDERERS = (("min-fill", 0, 0.0, 0), ("min-degree", 0, 0.0, 0),
+                    ("rgreedy", 8, 0.5, 0), ("rgreedy-fill", 8, 0.3, 0), ("rgreedy-fill", 8, 0.5, 0),
+                    ("rgreedy-fill", 8, 1.0, 0), ("rgreedy-fill", 8, 0.3, 1), ("rgreedy-fill", 8, 0.5, 1))
 
 
 def select_sliced_plan(graph, p: int, max_width: int, k_min: int = 0, k_max: int = 12,
                        orderers=DEFAULT_ORDERERS, r: int = 0, small_log2: int = -1,
-                       rg_seed: int = 0) -> Tuple[Plan, List[dict]]:
-    """Reading A11: the smallest k in [k_min, k_max] whose width <= max_width; among the
-    orderers at that k (greedy min-fill / min-degree, and rgreedy,
-    PAPER.md:465-475, given as (name, q, tau)), the plan with the fewest predicted bytes
-    (ties -> the earlier orderer in the list)."""
-    tried: List[dict] = []
-    for k in range(k_min, k_max + 1):
-        cands = []
-        for idx, spec in enumerate(orderers):
-            o, q, tau = spec if isinstance(spec, tuple) else (spec, 0, 0.0)
-            pl = build_plan(graph, p, "amplitude", o, n_sliced=k, r=r, small_log2=small_log2,
-                            rg_q=q, rg_tau=tau, rg_seed=rg_seed)
-            pl.orderer = o if not q else f"{o}(q={q},tau={tau})"
-            total = pl.info["pred_bytes_per_slice"][0] * pl.n_slices + pl.info["pred_bytes_prefix"][0]
-            tried.append({"k": k, "orderer": pl.orderer, "width": pl.width, "pred_bytes_c64": total,
-                          "unsliced_width": pl.info["unsliced_width"], "slice_step": pl.info["slice_step"]})
-            if pl.width <= max_width:
-                cands.append((total, idx, pl))
-        if cands:
-            cands.sort(key=lambda c: (c[0], c[1]))
-            return cands[0][2], tried
-    raise TnError(-3, f"no plan with width <= {max_width} for k <= {k_max}")
+                       workers: int = 0) -> Tuple[Plan, List[dict]]:
+    """Reading A11: among k in [k_min, k_max] and the orderers -- greedy min-fill /
+    min-degree (PAPER.md:459-463) and rgreedy (PAPER.md:465-475) given as (name, q, tau, seed)
+    -- the plan with the fewest predicted bytes subject to width <= max_width (ties -> smaller k,
+    then the earlier orderer).  Candidates are planned in parallel host threads (the C planner
+    runs with the GIL released)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs = [(k, idx, spec) for k in range(k_min, k_max + 1) for idx, spec in enumerate(orderers)]
+
+    def run(job):
+        k, idx, spec = job
+        o, q, tau, seed = spec if len(spec) == 4 else (*spec, 0)
+        pl = build_plan(graph, p, "amplitude", o, n_sliced=k, r=r, small_log2=small_log2,
+                        rg_q=q, rg_tau=tau, rg_seed=seed)
+        pl.orderer = o if not q else f"{o}(q={q},tau={tau},seed={seed})"
+        total = pl.info["pred_bytes_per_slice"][0] * pl.n_slices + pl.info["pred_bytes_prefix"][0]
+        return k, idx, pl, total
+
+    nw = workers or min(len(jobs), max(1, (os.cpu_count() or 4)))
+    with ThreadPoolExecutor(max_workers=nw) as ex:
+        results = list(ex.map(run, jobs))
+    tried, cands = [], []
+    for k, idx, pl, total in results:
+        tried.append({"k": k, "orderer": pl.orderer, "width": pl.width, "pred_bytes_c64": total,
+                      "unsliced_width": pl.info["unsliced_width"], "slice_step": pl.info["slice_step"]})
+        if pl.width <= max_width:
+            cands.append((total, k, idx, pl))
+    if not cands:
+        raise TnError(-3, f"no plan with width <= {max_width} for k in [{k_min}, {k_max}]")
+    cands.sort(key=lambda c: (c[0], c[1], c[2]))
+    return cands[0][3], tried

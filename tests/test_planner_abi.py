@@ -156,3 +156,34 @@ def test_workspace_and_bytes_model():
     assert info["workspace_bytes"][0] >= 8 * 2 ** plan.width
     assert info["workspace_bytes"][1] >= 16 * 2 ** plan.width
     assert math.isclose(info["pred_bytes_per_slice"][1], 2 * info["pred_bytes_per_slice"][0])
+
+
+def test_rgreedy_deterministic_and_not_worse():
+    # Boltzmann sampling p(v) ~ exp(-N_G(v)/tau), best of q runs; our runs
+    # always include the deterministic greedy run, so the width never gets worse
+    g = random_regular_graph(80, 3, 5)
+    ga, be = qaoa_angles(2, 5)
+    tens = network.qaoa_amplitude_network(80, g.edges, ga, be)
+    for base, rg in (("min-degree", "rgreedy"), ("min-fill", "rgreedy-fill")):
+        w0 = T.build_plan(g, 2, "amplitude", base).width
+        b1 = B.tn_plan_build(g.n, g.edges, 2, orderer=T.ORDERERS[rg], rg_q=6, rg_tau=0.5, rg_seed=11)
+        b2 = B.tn_plan_build(g.n, g.edges, 2, orderer=T.ORDERERS[rg], rg_q=6, rg_tau=0.5, rg_seed=11)
+        assert b1 == b2
+        pl = T.Plan(b1)
+        assert pl.width <= w0
+        pre, sl, res, degs = pl.schedule()
+        assert _replay(tens, pre, sl, res) == degs
+        # sliced rgreedy plans replay too
+        pl2 = T.build_plan(g, 2, "amplitude", rg, n_sliced=3, rg_q=4, rg_tau=0.5, rg_seed=3)
+        pre, sl, res, degs = pl2.schedule()
+        assert _replay(tens, pre, sl, res) == degs
+
+
+def test_select_sliced_plan_rule_a11():
+    g = random_regular_graph(100, 3, 1)
+    plan, tried = T.select_sliced_plan(g, 1, 14, k_min=2, k_max=6)
+    assert plan.width <= 14
+    feas = [t for t in tried if t["width"] <= 14]
+    best = min(t["pred_bytes_c64"] for t in feas)                  # fewest predicted bytes
+    mine = [t for t in feas if t["orderer"] == plan.orderer and t["k"] == plan.info["k"]][0]
+    assert mine["pred_bytes_c64"] == best
