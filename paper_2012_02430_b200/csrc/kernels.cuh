@@ -611,6 +611,170 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_group_t(const GArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ register-blocked pair group
+// A fused group whose varying inputs are exactly two tensors A and B is a batched complex GEMM
+// with K = 2^M: out[o] = sum_x C[x] A[F_A(o) + G_A(x)] B[F_B(o) + G_B(x)], C[x] the
+// per-tile product of the constant inputs.  Per tile (2^kPairTB outputs) the A and B chunks
+// (one per distinct x-part) are staged in shared memory with cp.async (double buffer); every
+// thread computes a 2x2 register block: outputs o, o + 2^rb, o + 2^ra, o + 2^ra + 2^rb where ra is
+// a tile bit held by A only and rb one held by B only, so each loaded A value feeds two outputs
+// and each B value two: per x, 4 shared loads + 2 cmul (A x C) + 4 complex FMA for 4 outputs.
+constexpr int kPairTB = 10;
+struct PArgs {
+  void* out;
+  const void* in[2];                   // A, B
+  uint64_t mask[2];
+  uint32_t pv[2];
+  uint64_t gx[2][1 << kMaxGroup];      // global element offset of the x-part
+  uint32_t sx[2][1 << kMaxGroup];      // staged chunk offset (buffer-relative)
+  uint8_t rep[2][1 << kMaxGroup];
+  uint32_t nparts[2], nlow[2];
+  uint32_t stage_elems;
+  const void* cin[kMaxIn];             // constant inputs
+  uint64_t cmask[kMaxIn];
+  uint32_t cpv[kMaxIn];
+  uint64_t cgx[kMaxIn][1 << kMaxGroup];
+  int32_t nc;
+  int32_t out_rank;
+  uint32_t ra, rb;                     // block bits (< kPairTB)
+  uint32_t tbits[8];                   // tile bits taken from the thread index, ascending
+  uint8_t perm[64];
+};
+
+template <typename T, typename OffT, int M>
+__global__ void __launch_bounds__(kBucketThreads, 2) k_pair(const PArgs a) {
+  constexpr int TB = kPairTB;
+  constexpr uint64_t TILE = 1ull << TB;
+  constexpr int NB = 64 - TB;
+  constexpr int NX = 1 << M;
+  const int nin = 2 + a.nc;
+  const uint64_t n_out = 1ull << a.out_rank;
+  const uint64_t n_tiles = (n_out + TILE - 1) >> TB;
+  const uint32_t tid = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T* stage = reinterpret_cast<T*>(dsm);
+  __shared__ OffT fbit[2 + kMaxIn][NB];
+  __shared__ OffT fcum[2 + kMaxIn][NB + 1];
+  __shared__ uint64_t pbit[NB], pcum[NB + 1];
+  __shared__ T Cs[2][NX];
+  auto mask_of = [&](int t) { return t < 2 ? a.mask[t] : a.cmask[t - 2]; };
+  auto pv_of = [&](int t) { return t < 2 ? a.pv[t] : a.cpv[t - 2]; };
+  for (int i = tid; i < nin * NB; i += kBucketThreads) {
+    const int t = i / NB, b = i % NB;
+    fbit[t][b] = (OffT)fmap(1ull << (TB + a.perm[b]), mask_of(t), pv_of(t));
+  }
+  for (int b = tid; b < NB; b += kBucketThreads) pbit[b] = 1ull << a.perm[b];
+  __syncthreads();
+  if (tid < (uint32_t)nin) {
+    OffT c = 0;
+    fcum[tid][0] = 0;
+    for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+  }
+  if (tid == (uint32_t)nin) {
+    uint64_t c = 0;
+    pcum[0] = 0;
+    for (int b = 0; b < NB; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+  }
+  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t ptile = 0;
+  for (int b = 0; b < NB && (t0 >> b); ++b)
+    if ((t0 >> b) & 1) ptile |= 1ull << a.perm[b];
+  // this thread's four outputs inside a tile and their chunk offsets
+  uint32_t ol = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ol |= ((tid >> i) & 1u) << a.tbits[i];
+  const uint32_t oA = (uint32_t)fmap(ol, a.mask[0], a.pv[0]);
+  const uint32_t oB = (uint32_t)fmap(ol, a.mask[1], a.pv[1]);
+  const uint32_t dA = (uint32_t)fmap(1ull << a.ra, a.mask[0], a.pv[0]);
+  const uint32_t dB = (uint32_t)fmap(1ull << a.rb, a.mask[1], a.pv[1]);
+  const uint64_t sa = 1ull << a.ra, sbit = 1ull << a.rb;
+  OffT cur[2], curc[kMaxIn];
+  for (int t = 0; t < nin; ++t) {
+    const OffT v = (OffT)fmap(ptile << TB, mask_of(t), pv_of(t));
+    if (t < 2) cur[t] = v; else curc[t - 2] = v;
+  }
+  OffT pf[2] = {cur[0], cur[1]};
+  T* out = static_cast<T*>(a.out);
+  __syncthreads();
+
+  auto prefetch = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t n = 1u << a.nlow[u];
+      const uint32_t n16 = (n * sizeof(T)) >> 4;
+      T* dst = stage + buf * a.stage_elems;
+      const T* src = static_cast<const T*>(a.in[u]) + pf[u];
+      const uint32_t total = a.nparts[u] * n16;
+      for (uint32_t c = tid; c < total; c += kBucketThreads) {
+        const uint32_t part = c / n16, piece = c - part * n16;
+        const uint32_t xr = a.rep[u][part];
+        cp_async16(reinterpret_cast<char*>(dst + a.sx[u][xr]) + piece * 16,
+                   reinterpret_cast<const char*>(src + (OffT)a.gx[u][xr]) + piece * 16);
+      }
+    }
+    cp_async_commit();
+  };
+  int buf = 0, cb = 0;
+  if (t0 < t1) prefetch(0);
+  for (uint64_t tile = t0; tile < t1; ++tile) {
+    const uint64_t base = ptile << TB;
+    const int r = __ffsll((long long)~tile) - 1;
+    const bool has_next = tile + 1 < t1;
+    if (tid < (uint32_t)NX) {
+      T c = cfrom<T>(1.0, 0.0);
+      for (int t = 0; t < a.nc; ++t)
+        c = cmul(c, __ldg(static_cast<const T*>(a.cin[t]) + curc[t] + (OffT)a.cgx[t][tid]));
+      Cs[cb][tid] = c;
+    }
+    bool same = true;
+    if (has_next) {
+      same = (fbit[0][r] == fcum[0][r]) && (fbit[1][r] == fcum[1][r]);
+      if (!same) {
+        pf[0] = pf[0] + fbit[0][r] - fcum[0][r];
+        pf[1] = pf[1] + fbit[1][r] - fcum[1][r];
+        prefetch(buf ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const T* sb = stage + buf * a.stage_elems;
+    T acc00 = cfrom<T>(0.0, 0.0), acc01 = acc00, acc10 = acc00, acc11 = acc00;
+    constexpr int XU = NX < 8 ? NX : 8;
+#pragma unroll XU
+    for (int x = 0; x < NX; ++x) {
+      const T c = Cs[cb][x];
+      const T* pa = sb + a.sx[0][x] + oA;
+      const T* pb = sb + a.sx[1][x] + oB;
+      const T a0 = cmul(pa[0], c), a1 = cmul(pa[dA], c);
+      const T b0 = pb[0], b1 = pb[dB];
+      acc00 = cadd(acc00, cmul(a0, b0));
+      acc01 = cadd(acc01, cmul(a0, b1));
+      acc10 = cadd(acc10, cmul(a1, b0));
+      acc11 = cadd(acc11, cmul(a1, b1));
+    }
+    const uint64_t o = base + ol;
+    if (o < n_out) {
+      __stcs(out + o, acc00);
+      __stcs(out + o + sbit, acc01);
+      __stcs(out + o + sa, acc10);
+      __stcs(out + o + sa + sbit, acc11);
+    }
+    __syncthreads();
+    if (has_next && !same) buf ^= 1;
+    cb ^= 1;
+    cur[0] = cur[0] + fbit[0][r] - fcum[0][r];
+    cur[1] = cur[1] + fbit[1][r] - fcum[1][r];
+    for (int t = 0; t < a.nc; ++t) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
+    ptile = ptile + pbit[r] - pcum[r];
+  }
+}
+
 // ------------------------------------------------------------------ fused reduce chain
 // m consecutive reduce steps eliminate the top m bits of A; the weights of step i are rank-1 on
 // its summed index.  Re-associated (exact): out[o] = sum_x W[x] A[o + x n_out], W[x] =

@@ -147,6 +147,22 @@ def test_interpreter_only_and_big_only_agree(dtype):
         assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
 
 
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+@pytest.mark.parametrize("n,p,k,orderer", [(50, 2, 2, "min-fill"), (36, 3, 3, "rgreedy-fill"),
+                                           (90, 1, 2, "rgreedy-fill")])
+def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
+    # every step standalone (small_log2 = 0): reduce chains (k_chain), merge groups (k_group_t,
+    # k_pair) and single steps all run at moderate widths, checked against the oracle
+    g = random_regular_graph(n, 3, 7 * n + p)
+    ga, be = qaoa_angles(p, n + 1)
+    plan = T.build_plan(g, p, "amplitude", orderer, n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
+    kinds = {s["standalone"] for s in plan.steps()}
+    assert 3 in kinds or 2 in kinds
+    pre, sl, res, _ = plan.schedule()
+    ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
+    assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
+
+
 def test_slice_partials_vs_oracle_per_slice():
     """Every per-slice partial of a sliced plan vs the oracle's slice (plan schedule as data)."""
     n, p, k = 40, 1, 3
