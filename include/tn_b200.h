@@ -87,6 +87,9 @@ typedef struct {
   double pred_bytes_prefix[2];
   double pred_bytes_big_per_slice[2]; /* the part of pred_bytes_per_slice in standalone launches */
   uint64_t big_launches_per_slice;    /* standalone bucket-kernel launches per slice */
+  int32_t slices_batchable;  /* 1: every per-slice step runs in the interpreter, so slices run
+                                batched (one CTA per slice) when the workspace holds windows */
+  int32_t reserved_info;
 } tn_plan_info_t;
 
 /* ---------------------------------------------------------------- planning (host only) */
@@ -157,6 +160,20 @@ tn_status tn_sum_partials(const tn_plan* plan, const double* partials_host, doub
 tn_status tn_energy(const tn_plan* plan, tn_dtype dtype, const double* gamma, const double* beta,
                     int32_t p, void* ws, size_t ws_bytes, void* stream, double* zz,
                     double* zz_imag_max, double* energy);
+
+/* Parameter-batched energy (the QAOA outer loop reuses one plan across parameters,
+ * PAPER.md:671-673): `batch` sets of angles, gammas/betas host double[batch * p] (set b at
+ * [b*p, b*p + p)), all E x batch light cones in ONE launch.  ws >= tn_workspace_bytes(plan, dtype,
+ * batch).  zz: host double[batch * E]; zz_imag_max, energy: host double[batch] (may be NULL). */
+tn_status tn_energy_batch(const tn_plan* plan, tn_dtype dtype, const double* gammas,
+                          const double* betas, int32_t p, uint64_t batch, void* ws, size_t ws_bytes,
+                          void* stream, double* zz, double* zz_imag_max, double* energy);
+
+/* Workspace bytes for `batch` windows: energy plans -- `batch` parameter sets (tn_energy_batch);
+ * amplitude plans whose per-slice steps all run in the interpreter -- up to `batch` slices per
+ * launch in tn_contract_sliced / tn_contract (slice batching; the library uses as
+ * many windows as the given ws_bytes holds).  batch <= 1 gives workspace_bytes[dtype]. 0 on error. */
+size_t tn_workspace_bytes(const tn_plan* plan, tn_dtype dtype, uint64_t batch);
 
 /* One bucket step -- "elimination of vertex (index) v" (§4.2) -- on caller
  * tensors:  out[o] = sum_{x in {0,1}} prod_t in_t[ins(pext(o, out_mask[t]), pv[t], x)],

@@ -36,7 +36,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h:
+        if h and B is not None and getattr(B, "_lib", None) is not None:
             B.tn_plan_free(h)
             self.handle = None
 
@@ -60,14 +60,27 @@ class Plan:
     def workspace_bytes(self, dtype: int) -> int:
         return int(self.info["workspace_bytes"][dtype])
 
-    def workspace(self, dtype: int, device=None):
+    # slice batching: windows for up to this many bytes of per-slice tensors
+    BATCH_WINDOW_BYTES = 4 << 30
+
+    def batch_windows(self, dtype: int) -> int:
+        """Slices run per launch when every per-slice step is an interpreter step."""
+        if not self.info["slices_batchable"] or self.n_slices <= 1:
+            return 1
+        one = B.tn_workspace_bytes(self.handle, dtype, 2) - B.tn_workspace_bytes(self.handle, dtype, 1)
+        return int(max(1, min(self.n_slices, self.BATCH_WINDOW_BYTES // max(1, one))))
+
+    def workspace(self, dtype: int, device=None, batch: int = 0):
+        """Device workspace (torch.empty), cached per (dtype, device, batch).  batch = 0: the
+        plan's default (slice batching windows when batchable)."""
         import torch
 
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        key = (dtype, str(dev))
+        nb = self.batch_windows(dtype) if batch == 0 else batch
+        key = (dtype, str(dev), nb)
         ws = self._ws.get(key)
         if ws is None:
-            ws = torch.empty(self.workspace_bytes(dtype), dtype=torch.uint8, device=dev)
+            ws = torch.empty(B.tn_workspace_bytes(self.handle, dtype, nb), dtype=torch.uint8, device=dev)
             self._ws[key] = ws
         return ws
 
@@ -95,8 +108,14 @@ class Plan:
         return B.tn_sum_partials(self.handle, partials_host)
 
     def energy(self, gammas, betas, dtype: int = TN_C64, stream=None):
-        ws = self.workspace(dtype)
+        ws = self.workspace(dtype, batch=1)
         return B.tn_energy(self.handle, dtype, gammas, betas, ws.data_ptr(), ws.numel(), self._stream(stream))
+
+    def energy_batch(self, gammas_sets, betas_sets, dtype: int = TN_C64, stream=None):
+        """B parameter sets in one launch (tn_energy_batch): (zz[B][E], imag_max[B], energy[B])."""
+        ws = self.workspace(dtype, batch=len(gammas_sets))
+        return B.tn_energy_batch(self.handle, dtype, gammas_sets, betas_sets, ws.data_ptr(), ws.numel(),
+                                 self._stream(stream))
 
     def profile(self, enable: bool = True):
         B.tn_profile_enable(self.handle, enable)

@@ -24,7 +24,8 @@ STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4
           -5: "TN_E_CUDA", -6: "TN_E_DTYPE"}
 
 SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_plan_load", "tn_plan_free", "tn_plan_info",
-           "tn_plan_schedule", "tn_plan_steps", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy",
+           "tn_plan_schedule", "tn_plan_steps", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy", "tn_energy_batch",
+           "tn_workspace_bytes",
            "tn_eliminate", "tn_profile_enable", "tn_profile_read", "tn_profile_records", "tn_last_error", "tn_version"]
 
 
@@ -49,7 +50,8 @@ class tn_plan_info_t(C.Structure):
                 ("launches_prefix", C.c_uint64), ("launches_per_slice", C.c_uint64),
                 ("workspace_bytes", C.c_size_t * 2), ("pred_bytes_per_slice", C.c_double * 2),
                 ("pred_bytes_prefix", C.c_double * 2), ("pred_bytes_big_per_slice", C.c_double * 2),
-                ("big_launches_per_slice", C.c_uint64)]
+                ("big_launches_per_slice", C.c_uint64), ("slices_batchable", C.c_int32),
+                ("reserved_info", C.c_int32)]
 
     def as_dict(self):
         d = {}
@@ -89,6 +91,8 @@ _lib.tn_contract_sliced.argtypes = [_P, C.c_int, _D, _D, C.c_int32, C.c_uint64, 
                                     C.c_size_t, _P, _P]
 _lib.tn_sum_partials.argtypes = [_P, _D, _D]
 _lib.tn_energy.argtypes = [_P, C.c_int, _D, _D, C.c_int32, _P, C.c_size_t, _P, _D, _D, _D]
+_lib.tn_energy_batch.argtypes = [_P, C.c_int, _D, _D, C.c_int32, C.c_uint64, _P, C.c_size_t, _P, _D, _D, _D]
+_lib.tn_workspace_bytes.argtypes = [_P, C.c_int, C.c_uint64]
 _lib.tn_eliminate.argtypes = [C.c_int, C.c_int32, C.POINTER(_P), C.POINTER(C.c_uint64), _I32P, _P,
                               C.c_int32, _P]
 _lib.tn_profile_enable.argtypes = [_P, C.c_int32]
@@ -97,8 +101,9 @@ _lib.tn_profile_records.argtypes = [_P, C.POINTER(tn_prof_record_t), C.c_int64, 
 _lib.tn_last_error.restype = C.c_char_p
 _lib.tn_version.restype = C.c_int32
 for _n in SYMBOLS:
-    if _n not in ("tn_buffer_free", "tn_plan_free", "tn_last_error", "tn_version"):
+    if _n not in ("tn_buffer_free", "tn_plan_free", "tn_last_error", "tn_version", "tn_workspace_bytes"):
         getattr(_lib, _n).restype = C.c_int
+_lib.tn_workspace_bytes.restype = C.c_size_t
 
 
 def last_error() -> str:
@@ -210,6 +215,24 @@ def tn_energy(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, str
     _check(_lib.tn_energy(h, dtype, _dbl(gammas), _dbl(betas), len(gammas), ws_ptr, ws_bytes, stream,
                           zz, C.byref(im), C.byref(en)), "tn_energy")
     return list(zz), im.value, en.value
+
+
+def tn_workspace_bytes(h: int, dtype: int, batch: int) -> int:
+    return int(_lib.tn_workspace_bytes(h, dtype, batch))
+
+
+def tn_energy_batch(h: int, dtype: int, gammas_sets, betas_sets, ws_ptr: int, ws_bytes: int, stream: int):
+    """gammas_sets / betas_sets: B sequences of p angles each."""
+    B = len(gammas_sets)
+    p = len(gammas_sets[0])
+    E = tn_plan_info(h)["n_programs"]
+    zz = (C.c_double * (E * B))()
+    im = (C.c_double * B)()
+    en = (C.c_double * B)()
+    _check(_lib.tn_energy_batch(h, dtype, _dbl([x for g in gammas_sets for x in g]),
+                                _dbl([x for b in betas_sets for x in b]), p, B, ws_ptr, ws_bytes, stream,
+                                zz, im, en), "tn_energy_batch")
+    return [list(zz[b * E:(b + 1) * E]) for b in range(B)], list(im), list(en)
 
 
 def tn_eliminate(dtype: int, in_ptrs, out_masks, pvs, out_ptr: int, out_rank: int, stream: int) -> None:

@@ -70,14 +70,18 @@ struct Angles {
   int p;
 };
 
+// blockIdx.y = parameter set y (batched energy): angles from dev_angles[y] (or `ang` when null),
+// written into window y
 template <typename T>
 __global__ void k_materialize(const LeafRec* __restrict__ leaves, int n_leaves, Angles ang,
-                              T* __restrict__ ws) {
+                              const Angles* __restrict__ dev_angles, T* __restrict__ ws,
+                              uint64_t win0, uint64_t win_elems) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int li = idx >> 2, e = idx & 3;
   if (li >= n_leaves) return;
   const LeafRec lr = leaves[li];
   if (e >= (1 << lr.rank)) return;
+  const Angles& A = dev_angles ? dev_angles[blockIdx.y] : ang;
   double re = 1.0, im = 0.0;
   for (int f = 0; f < lr.nfact; ++f) {
     double fr = 1.0, fi = 0.0;
@@ -88,17 +92,17 @@ __global__ void k_materialize(const LeafRec* __restrict__ leaves, int n_leaves, 
       case LC_ZOBS: fr = e ? -1.0 : 1.0; break;
       case LC_RXROW0: {
         double s, c;
-        sincos(ang.beta[l], &s, &c);
+        sincos(A.beta[l], &s, &c);
         if (e == 0) { fr = c; } else { fr = 0.0; fi = -s; }
         break;
       }
       case LC_ZZ: {
-        if (a != b) { double s, c; sincos(ang.gamma[l], &s, &c); fr = c; fi = -s; }
+        if (a != b) { double s, c; sincos(A.gamma[l], &s, &c); fr = c; fi = -s; }
         break;
       }
       case LC_RX: {
         double s, c;
-        sincos(ang.beta[l], &s, &c);
+        sincos(A.beta[l], &s, &c);
         if (a == b) { fr = c; } else { fr = 0.0; fi = -s; }
         break;
       }
@@ -109,7 +113,8 @@ __global__ void k_materialize(const LeafRec* __restrict__ leaves, int n_leaves, 
     re = nr;
     im = ni;
   }
-  ws[lr.off + e] = cfrom<T>(re, im);
+  const uint64_t rel = blockIdx.y == 0 ? 0ull : win0 + (uint64_t)(blockIdx.y - 1) * win_elems;
+  ws[rel + lr.off + e] = cfrom<T>(re, im);
 }
 
 // ------------------------------------------------------------------ standalone bucket step
@@ -835,16 +840,19 @@ __device__ __forceinline__ uint64_t slice_offset(uint64_t j, uint32_t slice_mask
   return slice_mask ? (pext_bits(j, slice_mask) << rank) : 0ull;
 }
 
+// rel: element offset added to per-slice tensors (F_REL inputs, every output) -- the window of a
+// batched slice; 0 otherwise
 template <typename T>
-__device__ void run_step(const StepRec& st, T* ws, uint64_t j) {
+__device__ void run_step(const StepRec& st, T* ws, uint64_t j, uint64_t rel, bool rel_all) {
   const uint64_t n_out = 1ull << st.out_rank;
-  T* out = ws + st.out_off;
+  T* out = ws + st.out_off + rel;
   const int nin = st.n_in;
   for (uint64_t o = threadIdx.x; o < n_out; o += blockDim.x) {
     T p0 = cfrom<T>(1.0, 0.0), p1 = cfrom<T>(1.0, 0.0);
     for (int t = 0; t < nin; ++t) {
       const InRec& ir = st.in[t];
-      const T* base = ws + ir.off + slice_offset(j, ir.slice_mask, ir.rank);
+      const T* base = ws + ir.off + ((rel_all || (ir.flags & F_REL)) ? rel : 0ull) +
+                      slice_offset(j, ir.slice_mask, ir.rank);
       const uint64_t off = fmap(o, ir.out_mask, ir.pv);
       const T x0 = base[off];
       const T x1 = base[off + (1ull << ir.pv)];
@@ -857,10 +865,12 @@ __device__ void run_step(const StepRec& st, T* ws, uint64_t j) {
 
 template <typename T>
 __device__ double2 final_product(const ScalarRec* scal, int b, int e, const T* ws, uint64_t j,
-                                 double log2_scale) {
-  double re = ldexp(1.0, 0), im = 0.0;
+                                 double log2_scale, uint64_t rel, bool rel_all = false) {
+  double re = 1.0, im = 0.0;
   for (int i = b; i < e; ++i) {
-    const double2 v = to_d2(ws[scal[i].off + (scal[i].slice_mask ? pext_bits(j, scal[i].slice_mask) : 0)]);
+    const uint64_t off = scal[i].off + ((rel_all || (scal[i].flags & F_REL)) ? rel : 0ull) +
+                         (scal[i].slice_mask ? pext_bits(j, scal[i].slice_mask) : 0);
+    const double2 v = to_d2(ws[off]);
     const double nr = re * v.x - im * v.y, ni = re * v.y + im * v.x;
     re = nr;
     im = ni;
@@ -869,27 +879,47 @@ __device__ double2 final_product(const ScalarRec* scal, int b, int e, const T* w
   return make_double2(re * s, im * s);
 }
 
-// mode 0: CTA 0 runs steps [begin, end) of the plan.
-// mode 1: CTA b runs program b's phase-B steps, then writes its final value to results[b].
+// window of batch member b: b = 0 -> the base arena; b >= 1 -> win0 + (b - 1) * win_elems
+__device__ __forceinline__ uint64_t window_rel(uint32_t b, uint64_t win0, uint64_t win_elems) {
+  return b == 0 ? 0ull : win0 + (uint64_t)(b - 1) * win_elems;
+}
+
+// mode 0: CTA 0 runs steps [begin, end) of the plan (slice j).
+// mode 1: CTA (b, y) runs program b's phase-B steps in window y (parameter set y of a batched
+//         energy), then writes its final value to results[y * gridDim.x + b].
+// mode 2: CTA b runs program 0's phase-B steps for slice j + b in window b (batched slices) and
+//         writes the slice's complex128 result to results[j + b].
 template <typename T>
 __global__ void __launch_bounds__(kProgramThreads) k_program(const StepRec* __restrict__ steps,
                                                              int begin, int end, T* ws, uint64_t j,
                                                              const ProgramRec* __restrict__ progs,
                                                              const ScalarRec* __restrict__ scal,
-                                                             double2* results, int mode) {
+                                                             double2* results, int mode,
+                                                             uint64_t win0, uint64_t win_elems) {
   int b = begin, e = end;
+  uint64_t rel = 0, jj = j;
+  const ProgramRec* pr = nullptr;
   if (mode == 1) {
-    const ProgramRec& pr = progs[blockIdx.x];
-    b = pr.stepB_begin;
-    e = pr.stepB_end;
+    pr = &progs[blockIdx.x];
+    rel = window_rel(blockIdx.y, win0, win_elems);
+  } else if (mode == 2) {
+    pr = &progs[0];
+    rel = window_rel(blockIdx.x, win0, win_elems);
+    jj = j + blockIdx.x;
   }
+  if (pr) {
+    b = pr->stepB_begin;
+    e = pr->stepB_end;
+  }
+  // mode 1 (energy batch): the whole network, leaves included, lives in window y
   for (int s = b; s < e; ++s) {
-    run_step<T>(steps[s], ws, j);
+    run_step<T>(steps[s], ws, jj, rel, mode == 1);
     __syncthreads();
   }
-  if (mode == 1 && threadIdx.x == 0) {
-    const ProgramRec& pr = progs[blockIdx.x];
-    results[blockIdx.x] = final_product<T>(scal, pr.scal_begin, pr.scal_end, ws, j, pr.log2_scale);
+  if (pr && threadIdx.x == 0) {
+    const double2 v = final_product<T>(scal, pr->scal_begin, pr->scal_end, ws, jj, pr->log2_scale, rel, mode == 1);
+    if (mode == 1) results[(uint64_t)blockIdx.y * gridDim.x + blockIdx.x] = v;
+    else results[jj] = v;
   }
 }
 
@@ -897,7 +927,7 @@ template <typename T>
 __global__ void k_finalize(const ScalarRec* __restrict__ scal, int b, int e, const T* ws,
                            uint64_t j, double log2_scale, double* __restrict__ dst) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    const double2 v = final_product<T>(scal, b, e, ws, j, log2_scale);
+    const double2 v = final_product<T>(scal, b, e, ws, j, log2_scale, 0ull);
     dst[0] = v.x;
     dst[1] = v.y;
   }

@@ -18,7 +18,7 @@
 namespace tnb {
 
 constexpr uint32_t kPlanMagic = 0x32424E54u;  // "TNB2"
-constexpr uint32_t kPlanVersion = 5;
+constexpr uint32_t kPlanVersion = 6;
 constexpr int kMaxIn = 8;     // inputs per bucket step
 constexpr int kMaxP = 16;     // QAOA depth supported by the materializer
 constexpr int kMaxFactors = 4;
@@ -50,8 +50,10 @@ struct InRec {
   uint32_t rank;       // bits of this input in the current phase (excl. sliced bits in phase B)
   uint32_t slice_mask; // phase B: which slice bits this tensor holds (its top bits); else 0
   uint32_t pv;         // bit position of the summed index in the input
-  uint32_t flags;      // bit0: streamed (read once, large)
+  uint32_t flags;      // bit0: streamed (read once, large); bit2: F_REL -- a per-slice tensor
+                       // (relocated into the slice's window when slices run batched)
 };
+constexpr uint32_t F_REL = 4u;
 
 struct StepRec {
   uint64_t out_off;
@@ -85,6 +87,8 @@ struct ScalarRec {       // per-slice final factors: rank-0 tensors and tensors 
   uint64_t off;
   uint32_t slice_mask;
   int32_t program;
+  uint32_t flags;        // F_REL: produced per slice
+  uint32_t pad;
 };
 
 struct ProgramRec {      // amplitude: one program; energy: one per edge (light cone)

@@ -611,6 +611,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
         return out;
       }
       in.flags = (in.rank + 2 >= (uint32_t)R && R >= 16) ? 1u : 0u;
+      if (phaseB && s.phaseB_born) in.flags |= F_REL;
     }
     // in-place: in[0] is an intermediate of this phase holding every output bit with v on top
     {
@@ -713,6 +714,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     uint32_t m = 0;
     for (int l : syms[id].idx) m |= 1u << slice_bit[l];
     sr.slice_mask = m;
+    sr.flags = syms[id].phaseB_born ? F_REL : 0u;
     out.scalars.push_back(sr);
   }
   // ---- ops: runs of small steps go to the interpreter, the rest are standalone launches

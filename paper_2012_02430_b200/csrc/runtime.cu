@@ -63,6 +63,7 @@ struct tn_plan {
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
   uint64_t all_launches = 0;
+  bool batchable = false;   // every per-slice op is an interpreter run -> slices can run batched
   ~tn_plan() {
     for (auto& kv : dev) {
       cudaSetDevice(kv.first);
@@ -301,11 +302,27 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
     if (pr.stepB_begin < 0 || pr.stepB_end > h.n_steps || pr.scal_begin < 0 || pr.scal_end > h.n_scalars ||
         pr.opA_begin < 0 || pr.opB_end > h.n_ops)
       return fail(TN_E_PLAN, "tn_plan_load: bad program record");
+  pl->batchable = pl->h.kind == TN_KIND_AMPLITUDE && pl->h.n_programs == 1;
+  for (int oi = pl->progs[0].opB_begin; oi < pl->progs[0].opB_end; ++oi)
+    if (pl->ops[oi].type != OP_RUN) pl->batchable = false;
   *out = pl.release();
   return TN_OK;
 }
 
 extern "C" void tn_plan_free(tn_plan* plan) { delete plan; }
+
+// workspace with `batch` windows: [base layout][windows 1..batch-1][batch results][batch angles]
+static size_t ws_bytes_batched(const PlanHeader& h, int dtype, uint64_t batch) {
+  const size_t es = dtype == TN_C64 ? 8 : 16;
+  if (batch <= 1) return ws_bytes_for(h, dtype);
+  return ws_bytes_for(h, dtype) + (batch - 1) * h.arena_elems * es +
+         align256(16 * batch * (uint64_t)h.n_programs) + align256(sizeof(Angles) * batch);
+}
+
+extern "C" size_t tn_workspace_bytes(const tn_plan* plan, tn_dtype dtype, uint64_t batch) {
+  if (!plan || (dtype != TN_C64 && dtype != TN_C128)) return 0;
+  return ws_bytes_batched(plan->h, dtype, batch);
+}
 
 extern "C" tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* o) {
   if (!plan || !o) return fail(TN_E_INVAL, "tn_plan_info: null argument");
@@ -336,6 +353,7 @@ extern "C" tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* o) {
     o->pred_bytes_big_per_slice[d] = h.pred_elems_big_slice * es;
   }
   o->big_launches_per_slice = h.big_launches_slice;
+  o->slices_batchable = plan->batchable ? 1 : 0;
   return TN_OK;
 }
 
@@ -980,7 +998,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         for (int si = op.begin; si < op.end; ++si) run_big<T>(pl, si, ws, j, st);
     } else {
       k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
-                                                  dt.scalars, nullptr, 0);
+                                                  dt.scalars, nullptr, 0, 0, 0);
     }
     pl->all_launches++;
   }
@@ -999,7 +1017,8 @@ tn_status materialize(tn_plan* pl, const DevTables& dt, const double* gamma, con
   }
   ang.p = p;
   const int n = (int)pl->leaves.size() * 4;
-  if (n > 0) k_materialize<T><<<(n + 255) / 256, 256, 0, st>>>(dt.leaves, (int)pl->leaves.size(), ang, ws);
+  if (n > 0)
+    k_materialize<T><<<(n + 255) / 256, 256, 0, st>>>(dt.leaves, (int)pl->leaves.size(), ang, nullptr, ws, 0, 0);
   pl->all_launches++;
   CU(cudaGetLastError());
   return TN_OK;
@@ -1017,7 +1036,7 @@ tn_status check_call(const tn_plan* plan, int dtype, const double* gamma, const 
 
 template <typename T>
 tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int p, uint64_t begin,
-                      uint64_t end, void* wsv, cudaStream_t st, double* partials_dev) {
+                      uint64_t end, void* wsv, size_t ws_bytes, cudaStream_t st, double* partials_dev) {
   DevTables* dt = nullptr;
   tn_status s = ensure_dev(pl, &dt);
   if (s != TN_OK) return s;
@@ -1025,6 +1044,26 @@ tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int 
   if ((s = materialize<T>(pl, *dt, gamma, beta, p, ws, st)) != TN_OK) return s;
   const ProgramRec& pr = pl->progs[0];
   if ((s = run_ops<T>(pl, *dt, pr.opA_begin, pr.opA_end, ws, 0, st)) != TN_OK) return s;
+  // batched slices: every per-slice step runs in the interpreter -> one launch
+  // runs up to nb slices, each CTA in its own window for the per-slice tensors
+  const size_t es = sizeof(T);
+  const size_t base_bytes = ws_bytes_for(pl->h, es == 8 ? TN_C64 : TN_C128);
+  const uint64_t win_bytes = pl->h.arena_elems * es;
+  uint64_t nb = 1;
+  if (pl->batchable && win_bytes > 0 && ws_bytes > base_bytes)
+    nb = 1 + (ws_bytes - base_bytes) / win_bytes;
+  if (pl->batchable && nb >= 2) {
+    const uint64_t win0 = base_bytes / es;
+    for (uint64_t j = begin; j < end; j += nb) {
+      const uint64_t cnt = std::min<uint64_t>(nb, end - j);
+      k_program<T><<<(unsigned)cnt, kProgramThreads, 0, st>>>(dt->steps, 0, 0, ws, j, dt->progs, dt->scalars,
+                                                               reinterpret_cast<double2*>(partials_dev), 2,
+                                                               win0, pl->h.arena_elems);
+      pl->all_launches++;
+    }
+    CU(cudaGetLastError());
+    return TN_OK;
+  }
   for (uint64_t j = begin; j < end; ++j) {
     if ((s = run_ops<T>(pl, *dt, pr.opB_begin, pr.opB_end, ws, j, st)) != TN_OK) return s;
     k_finalize<T><<<1, 32, 0, st>>>(dt->scalars, pr.scal_begin, pr.scal_end, ws, j, pr.log2_scale,
@@ -1054,8 +1093,8 @@ extern "C" tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, con
   if (begin > end || end > (1ull << plan->h.k)) return fail(TN_E_INVAL, "bad slice range");
   tn_plan* pl = const_cast<tn_plan*>(plan);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return dtype == TN_C64 ? sliced_impl<float2>(pl, gamma, beta, p, begin, end, ws, st, partials_dev)
-                         : sliced_impl<double2>(pl, gamma, beta, p, begin, end, ws, st, partials_dev);
+  return dtype == TN_C64 ? sliced_impl<float2>(pl, gamma, beta, p, begin, end, ws, ws_bytes, st, partials_dev)
+                         : sliced_impl<double2>(pl, gamma, beta, p, begin, end, ws, ws_bytes, st, partials_dev);
 }
 
 extern "C" tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma,
@@ -1080,44 +1119,78 @@ extern "C" tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const doub
   return TN_OK;
 }
 
+template <typename T>
+tn_status energy_impl(tn_plan* pl, const double* gammas, const double* betas, int p, uint64_t B,
+                      void* wsv, cudaStream_t st, double* zz, double* zz_imag_max, double* energy) {
+  DevTables* dt = nullptr;
+  tn_status s;
+  if ((s = ensure_dev(pl, &dt)) != TN_OK) return s;
+  T* ws = static_cast<T*>(wsv);
+  const size_t es = sizeof(T);
+  const int E = pl->h.n_programs;
+  const size_t base_bytes = ws_bytes_for(pl->h, es == 8 ? TN_C64 : TN_C128);
+  const uint64_t win0 = base_bytes / es;
+  uint8_t* tail = static_cast<uint8_t*>(wsv) + base_bytes + (B > 1 ? (B - 1) * pl->h.arena_elems * es : 0);
+  double2* results = B > 1 ? reinterpret_cast<double2*>(tail)
+                           : reinterpret_cast<double2*>(scratch_ptr(pl, es == 8 ? TN_C64 : TN_C128, wsv));
+  Angles* dang = B > 1 ? reinterpret_cast<Angles*>(tail + align256(16 * B * (uint64_t)E)) : nullptr;
+  std::vector<Angles> hang(B);
+  for (uint64_t b = 0; b < B; ++b) {
+    std::memset(&hang[b], 0, sizeof(Angles));
+    for (int l = 0; l < p; ++l) {
+      hang[b].gamma[l] = gammas[b * p + l];
+      hang[b].beta[l] = betas[b * p + l];
+    }
+    hang[b].p = p;
+  }
+  if (dang) CU(cudaMemcpyAsync(dang, hang.data(), sizeof(Angles) * B, cudaMemcpyHostToDevice, st));
+  const int n = (int)pl->leaves.size() * 4;
+  if (n > 0) {
+    dim3 grid((n + 255) / 256, (unsigned)B);
+    k_materialize<T><<<grid, 256, 0, st>>>(dt->leaves, (int)pl->leaves.size(), hang[0], dang, ws, win0,
+                                           pl->h.arena_elems);
+  }
+  dim3 grid((unsigned)E, (unsigned)B);
+  k_program<T><<<grid, kProgramThreads, 0, st>>>(dt->steps, 0, 0, ws, 0, dt->progs, dt->scalars, results, 1,
+                                                 win0, pl->h.arena_elems);
+  pl->all_launches += 2;
+  CU(cudaGetLastError());
+  std::vector<double> h(2 * (size_t)E * B);
+  CU(cudaMemcpyAsync(h.data(), results, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (uint64_t b = 0; b < B; ++b) {
+    double im = 0.0, en = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double re = h[2 * (b * E + e)], ie = h[2 * (b * E + e) + 1];
+      zz[b * E + e] = re;
+      im = std::max(im, std::fabs(ie));
+      en += (1.0 - re) / 2.0;
+    }
+    if (zz_imag_max) zz_imag_max[b] = im;
+    if (energy) energy[b] = en;
+  }
+  return TN_OK;
+}
+
+extern "C" tn_status tn_energy_batch(const tn_plan* plan, tn_dtype dtype, const double* gammas,
+                                     const double* betas, int32_t p, uint64_t batch, void* ws,
+                                     size_t ws_bytes, void* stream, double* zz, double* zz_imag_max,
+                                     double* energy) {
+  tn_status s = check_call(plan, dtype, gammas, betas, p, ws, ws_bytes);
+  if (s != TN_OK) return s;
+  if (plan->h.kind != TN_KIND_ENERGY) return fail(TN_E_INVAL, "not an energy plan");
+  if (!zz || batch < 1 || batch > 65535) return fail(TN_E_INVAL, "bad zz / batch");
+  if (ws_bytes < ws_bytes_batched(plan->h, dtype, batch)) return fail(TN_E_INVAL, "workspace too small for the batch");
+  tn_plan* pl = const_cast<tn_plan*>(plan);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return dtype == TN_C64 ? energy_impl<float2>(pl, gammas, betas, p, batch, ws, st, zz, zz_imag_max, energy)
+                         : energy_impl<double2>(pl, gammas, betas, p, batch, ws, st, zz, zz_imag_max, energy);
+}
+
 extern "C" tn_status tn_energy(const tn_plan* plan, tn_dtype dtype, const double* gamma,
                                const double* beta, int32_t p, void* ws, size_t ws_bytes,
                                void* stream, double* zz, double* zz_imag_max, double* energy) {
-  tn_status s = check_call(plan, dtype, gamma, beta, p, ws, ws_bytes);
-  if (s != TN_OK) return s;
-  if (plan->h.kind != TN_KIND_ENERGY) return fail(TN_E_INVAL, "not an energy plan");
-  if (!zz) return fail(TN_E_INVAL, "null zz");
-  tn_plan* pl = const_cast<tn_plan*>(plan);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DevTables* dt = nullptr;
-  if ((s = ensure_dev(pl, &dt)) != TN_OK) return s;
-  double* scratch = scratch_ptr(plan, dtype, ws);
-  const int E = plan->h.n_programs;
-  if (dtype == TN_C64) {
-    float2* w = static_cast<float2*>(ws);
-    if ((s = materialize<float2>(pl, *dt, gamma, beta, p, w, st)) != TN_OK) return s;
-    k_program<float2><<<E, kProgramThreads, 0, st>>>(dt->steps, 0, 0, w, 0, dt->progs, dt->scalars,
-                                                     reinterpret_cast<double2*>(scratch), 1);
-  } else {
-    double2* w = static_cast<double2*>(ws);
-    if ((s = materialize<double2>(pl, *dt, gamma, beta, p, w, st)) != TN_OK) return s;
-    k_program<double2><<<E, kProgramThreads, 0, st>>>(dt->steps, 0, 0, w, 0, dt->progs, dt->scalars,
-                                                      reinterpret_cast<double2*>(scratch), 1);
-  }
-  pl->all_launches++;
-  CU(cudaGetLastError());
-  std::vector<double> h(2 * (size_t)E);
-  CU(cudaMemcpyAsync(h.data(), scratch, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  double im = 0.0, en = 0.0;
-  for (int e = 0; e < E; ++e) {
-    zz[e] = h[2 * e];
-    im = std::max(im, std::fabs(h[2 * e + 1]));
-    en += (1.0 - h[2 * e]) / 2.0;
-  }
-  if (zz_imag_max) *zz_imag_max = im;
-  if (energy) *energy = en;
-  return TN_OK;
+  return tn_energy_batch(plan, dtype, gamma, beta, p, 1, ws, ws_bytes, stream, zz, zz_imag_max, energy);
 }
 
 extern "C" tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* const* in_dev,
@@ -1163,9 +1236,9 @@ extern "C" tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* cons
     }
     CU(cudaMemcpyAsync(d, &rec, sizeof(rec), cudaMemcpyHostToDevice, st));
     if (dtype == TN_C64)
-      k_program<float2><<<1, 32, 0, st>>>(d, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0);
+      k_program<float2><<<1, 32, 0, st>>>(d, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, 0);
     else
-      k_program<double2><<<1, 32, 0, st>>>(d, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0);
+      k_program<double2><<<1, 32, 0, st>>>(d, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, 0);
     CU(cudaFreeAsync(d, st));
     CU(cudaGetLastError());
     return TN_OK;

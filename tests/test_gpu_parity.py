@@ -247,3 +247,39 @@ def test_c5a_full_scale_closed_forms(which):
         ga, ref = [math.pi], cf.amp_gamma_pi(n, be)
     got, _ = run_sliced(plan, ga, be, dtype=T.TN_C64)
     assert rel(got, ref) < 1e-4
+
+
+# ------------------------------------------------------------------ batching
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+def test_batched_slices_match_sequential_and_oracle(dtype):
+    n, p = 40, 2
+    g = random_regular_graph(n, 3, 17)
+    ga, be = qaoa_angles(p, 17)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=5, small_log2=30)
+    assert plan.info["slices_batchable"] == 1 and plan.batch_windows(dtype) == plan.n_slices
+    outs = []
+    for batch in (1, 3, plan.n_slices):
+        ws = plan.workspace(dtype, batch=batch)
+        part = torch.zeros(2 * plan.n_slices, dtype=torch.float64, device="cuda")
+        B.tn_contract_sliced(plan.handle, dtype, ga, be, 0, plan.n_slices, ws.data_ptr(), ws.numel(),
+                             torch.cuda.current_stream().cuda_stream, part.data_ptr())
+        torch.cuda.synchronize()
+        outs.append(part.cpu())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])   # same arithmetic
+    pre, sl, res, _ = plan.schedule()
+    ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
+    assert rel(plan.sum_partials(outs[2].tolist()), ref) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C128, T.TN_C64])
+def test_energy_batch_matches_single_and_oracle(dtype):
+    n, p = 30, 2
+    g = random_regular_graph(n, 3, 3)
+    plan = T.build_plan(g, p, "energy", "min-fill")
+    sets = [qaoa_angles(p, 100 + b) for b in range(5)]
+    zzs, ims, ens = plan.energy_batch([s[0] for s in sets], [s[1] for s in sets], dtype=dtype)
+    for b, (ga, be) in enumerate(sets):
+        zz1, im1, e1 = plan.energy(ga, be, dtype=dtype)
+        assert zz1 == zzs[b] and e1 == ens[b]                                   # same arithmetic
+        Eref, _ = energy.maxcut_energy(n, g.edges, ga, be)
+        assert abs(ens[b] - Eref) < TOL[dtype] * len(g.edges)

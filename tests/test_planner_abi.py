@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_library_exports_every_header_symbol():
     hdr = open(os.path.join(ROOT, "include", "tn_b200.h")).read()
-    decl = set(re.findall(r"^(?:tn_status|void|const char\*|int32_t)\s+(tn_[a-z_]+)\(", hdr, re.M))
+    decl = set(re.findall(r"^(?:tn_status|void|const char\*|int32_t|size_t)\s+(tn_[a-z_]+)\(", hdr, re.M))
     assert decl == set(B.SYMBOLS), decl ^ set(B.SYMBOLS)
     lib = ctypes.CDLL(B.LIB_PATH)
     for name in decl:
