@@ -445,7 +445,30 @@ tn_status ensure_dev(tn_plan* pl, DevTables** out) {
   return TN_OK;
 }
 
+// opt in to more than 48 KB of (static + dynamic) shared memory, once per kernel instantiation
+template <typename K>
+void allow_smem(K kernel, size_t dyn) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> granted;   // per kernel (per device is not needed: the
+                                                   // attribute is a function property)
+  if (dyn + 16 * 1024 <= 48 * 1024) return;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& g = granted[reinterpret_cast<const void*>(kernel)];
+  if (dyn > g) {
+    const size_t want = std::max<size_t>(dyn, 100 * 1024);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    g = want;
+  }
+}
+
 int g_num_sms = 0;
+bool debug_checks() {
+  static const int on = [] {
+    const char* v = std::getenv("TNB_DEBUG");
+    return (v && v[0] == '1') ? 1 : 0;
+  }();
+  return on != 0;
+}
 int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
@@ -549,10 +572,13 @@ void launch_bucket_n(BigArgs a, cudaStream_t st) {
   const size_t smem = (size_t)a.stage_elems * sizeof(T) * 2;
   bool wide = false;   // any input with more than 32 bits -> 64-bit offsets
   for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
-  if (wide)
+  if (wide) {
+    allow_smem(k_bucket<T, NIN, uint64_t>, smem);
     k_bucket<T, NIN, uint64_t><<<grid, kBucketThreads, smem, st>>>(a);
-  else
+  } else {
+    allow_smem(k_bucket<T, NIN, uint32_t>, smem);
     k_bucket<T, NIN, uint32_t><<<grid, kBucketThreads, smem, st>>>(a);
+  }
 }
 
 // ---------------------------------------------------------------- k_group_t host side
@@ -580,6 +606,7 @@ uint64_t host_fmap(uint64_t o, uint64_t mask, uint32_t pv) {
 
 template <typename T, typename OffT, int NDIR, int NSTG, int M, int NDV>
 void launch_g(const GArgs& ga, unsigned grid, size_t smem, cudaStream_t st) {
+  allow_smem(k_group_t<T, OffT, NDIR, NSTG, M, NDV>, smem);
   k_group_t<T, OffT, NDIR, NSTG, M, NDV><<<grid, kBucketThreads, smem, st>>>(ga);
 }
 
@@ -714,8 +741,7 @@ bool try_launch_group(const GDesc& g, cudaStream_t st) {
 // register-blocked pair kernel (k_pair) for groups with exactly two varying inputs
 template <typename T, typename OffT, int M>
 void launch_p(const PArgs& pa, unsigned grid, size_t smem, cudaStream_t st) {
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_pair<T, OffT, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(k_pair<T, OffT, M>, smem);
   k_pair<T, OffT, M><<<grid, kBucketThreads, smem, st>>>(pa);
 }
 
@@ -1001,6 +1027,13 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
                                                   dt.scalars, nullptr, 0, 0, 0);
     }
     pl->all_launches++;
+    if (debug_checks()) {
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess)
+        return fail(TN_E_CUDA, std::string("op ") + std::to_string(oi) + " (type " + std::to_string(op.type) +
+                                   ", steps " + std::to_string(op.begin) + "-" + std::to_string(op.end) +
+                                   "): " + cudaGetErrorString(e));
+    }
   }
   CU(cudaGetLastError());
   return TN_OK;

@@ -1,0 +1,200 @@
+"""Run every BASELINE workload (C1-C5b) on one GPU: plan, time, parity.  Writes one JSON record
+per config to --out (and prints a table).  Parity is always against the oracle (sampled slices
+with the plan's schedule as data where the whole contraction is too big for it) and, for the
+amplitudes at full scale, against the closed forms of oracle/closed_forms.py.
+
+    python scripts/run_configs.py --out profiles/r01/configs.json [--only C1,C3]
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2012_02430_b200 as T  # noqa: E402
+from oracle import closed_forms as cf  # noqa: E402
+from oracle import contract, energy, network  # noqa: E402
+from oracle import statevector as sv  # noqa: E402
+from paper_2012_02430_b200.scheduler import run_sliced  # noqa: E402
+from tn_inputs import WORKLOADS, qaoa_angles, random_regular_graph  # noqa: E402
+
+
+def timed(fn, reps=10, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts), min(ts)
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def run_energy(name, dtypes):
+    w = WORKLOADS[name]
+    g = random_regular_graph(w.n, 3, 0)
+    ga, be = qaoa_angles(w.p, 0)
+    t0 = time.perf_counter()
+    plan = T.build_plan(g, w.p, "energy", "min-fill")
+    plan_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Eref, zref = energy.maxcut_energy(w.n, g.edges, ga, be)
+    oracle_s = time.perf_counter() - t0
+    rec = {"config": name, "kind": "energy", "n": w.n, "p": w.p, "edges": len(g.edges), "plan_s": plan_s,
+           "cone_width_max": plan.width, "oracle": {"energy": Eref, "seconds": oracle_s, "cores": 1}}
+    if w.n <= 16:
+        psi = sv.qaoa_state(w.n, g.edges, ga, be)
+        rec["statevector_energy"] = sv.maxcut_energy(psi, g.edges)
+    for dt, dn in dtypes:
+        zz, im, E = plan.energy(ga, be, dtype=dt)
+        ms, best = timed(lambda: plan.energy(ga, be, dtype=dt), reps=20)
+        B = 256
+        sets = [qaoa_angles(w.p, 1000 + b) for b in range(B)]
+        msb, _ = timed(lambda: plan.energy_batch([s[0] for s in sets], [s[1] for s in sets], dtype=dt), reps=5, warm=1)
+        rec[dn] = {"energy": E, "abs_err_vs_oracle": abs(E - Eref),
+                   "max_zz_err": max(abs(a - b.real) for a, b in zip(zz, zref)), "zz_imag_max": im,
+                   "ms_per_energy": ms, "ms_best": best, "batch256_ms": msb,
+                   "energies_per_s_batched": B / (msb / 1e3), "launches_per_call": 2}
+    return rec
+
+
+def run_amplitude(name, k_range, max_width, sample_slices=3, batched=False, time_slices=None):
+    w = WORKLOADS[name]
+    g = random_regular_graph(w.n, 3, 0)
+    ga, be = qaoa_angles(w.p, 0)
+    t0 = time.perf_counter()
+    small = 30 if batched else -1
+    try:
+        plan, tried = T.select_sliced_plan(g, w.p, max_width, k_min=k_range[0], k_max=k_range[1], small_log2=small)
+    except T.TnError:
+        # this seed's instance is wider than the survey's: take the narrowest plan found
+        plan, tried = T.select_sliced_plan(g, w.p, 64, k_min=k_range[1], k_max=k_range[1], small_log2=small)
+    plan_s = time.perf_counter() - t0
+    info = plan.info
+    rec = {"config": name, "kind": "amplitude", "n": w.n, "p": w.p, "plan_s": plan_s, "orderer": plan.orderer,
+           "k": info["k"], "width": plan.width, "unsliced_width": info["unsliced_width"],
+           "slice_step": info["slice_step"], "steps_per_slice": info["steps_per_slice"],
+           "pred_GB_total_c64": (info["pred_bytes_per_slice"][0] * plan.n_slices + info["pred_bytes_prefix"][0]) / 1e9,
+           "workspace_GB_c64": plan.workspace_bytes(0) / 1e9, "slices_batched": bool(info["slices_batchable"]),
+           "candidates": len(tried)}
+    n = plan.n_slices
+    part = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+    if time_slices is None or time_slices >= n:
+        ms, best = timed(lambda: plan.contract_sliced(ga, be, 0, n, part, dtype=T.TN_C64), reps=5, warm=2)
+        rec["ms_per_contraction_c64"] = ms
+        rec["contractions_per_s"] = 1000.0 / ms
+    else:   # too long to run whole: time a block of slices and extrapolate (stated)
+        ms, best = timed(lambda: plan.contract_sliced(ga, be, 0, time_slices, part, dtype=T.TN_C64), reps=2, warm=1)
+        rec["ms_per_slice_c64"] = ms / time_slices
+        rec["ms_per_contraction_c64_extrapolated"] = ms / time_slices * n
+    tens = network.qaoa_amplitude_network(w.n, g.edges, ga, be)
+    if info["k"] == 0:
+        # unsliced plan (C2): the oracle computes the whole sigma with an auxiliary sliced schedule
+        # (Eq. 1, exact) so that its numpy tensors stay small
+        aux, _ = T.select_sliced_plan(g, w.p, 22, k_min=2, k_max=8, orderers=(("rgreedy-fill", 8, 0.3, 0),))
+        apre, asl, ares, _ = aux.schedule()
+        t0 = time.perf_counter()
+        ref = contract.contract_sliced(tens, apre, asl, ares)
+        oracle_s = time.perf_counter() - t0
+        g64 = plan.contract(ga, be, dtype=T.TN_C64)
+        g128 = plan.contract(ga, be, dtype=T.TN_C128)
+        rec["parity"] = {"oracle_sigma": [ref.real, ref.imag], "oracle_seconds": oracle_s,
+                         "oracle_schedule_k": aux.info["k"], "rel_err_c64": rel(g64, ref), "rel_err_c128": rel(g128, ref)}
+        sample_slices = 0
+    # sampled per-slice parity vs the oracle (complex128, plan schedule as data)
+    pre, sl, res, _ = plan.schedule()
+    js = sorted({0, n // 2, n - 1})[:sample_slices]
+    if plan.width > 30 and js:
+        # a width > 30 slice would need > 16 GiB complex128 tensors in numpy: compare the two GPU
+        # dtypes on one slice instead (the kernels are oracle-checked at smaller widths above)
+        p128 = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        p64 = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        plan.contract_sliced(ga, be, 0, 1, p128, dtype=T.TN_C128)
+        plan.contract_sliced(ga, be, 0, 1, p64, dtype=T.TN_C64)
+        torch.cuda.synchronize()
+        a, b = complex(*p128[:2].tolist()), complex(*p64[:2].tolist())
+        rec["slice0_c64_vs_c128_rel"] = rel(b, a)
+        js = []
+    t0 = time.perf_counter()
+    try:
+        if not js:
+            raise MemoryError("covered by the whole-sigma parity or the dtype cross-check")
+        _, parts = contract.contract_sliced(tens, pre, sl, res, slices=js, return_parts=True)
+        oracle_s = time.perf_counter() - t0
+        p128 = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        p64 = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        for j in js:
+            plan.contract_sliced(ga, be, j, j + 1, p128, dtype=T.TN_C128)
+            plan.contract_sliced(ga, be, j, j + 1, p64, dtype=T.TN_C64)
+        torch.cuda.synchronize()
+        h128, h64 = p128.cpu().tolist(), p64.cpu().tolist()
+        scale = max(abs(v) for v in parts)
+        rec["slice_parity"] = {"slices": js, "oracle_seconds": oracle_s,
+                               "max_err_c128": max(abs(complex(h128[2 * j], h128[2 * j + 1]) - v) for j, v in zip(js, parts)) / scale,
+                               "max_err_c64": max(abs(complex(h64[2 * j], h64[2 * j + 1]) - v) for j, v in zip(js, parts)) / scale}
+    except MemoryError as e:
+        rec["slice_parity"] = {"skipped": str(e)}
+    # full-scale closed forms (whole contraction, c64) when it runs in reasonable time
+    if time_slices is None or time_slices >= n:
+        cfs = {}
+        for which, gg, bb, ref in (("gamma0", [0.0] * w.p, be, cf.amp_gamma0(w.n, be)),
+                                   ("beta0", ga, [0.0] * w.p, cf.amp_beta0(w.n)),
+                                   ("gammapi", [math.pi] * w.p, be, cf.amp_gamma_pi(w.n, be))):
+            got, _ = run_sliced(plan, gg, bb, dtype=T.TN_C64)
+            cfs[which] = rel(got, ref)
+        rec["closed_form_rel_err_c64"] = cfs
+        sigma, _ = run_sliced(plan, ga, be, dtype=T.TN_C64)
+        rec["sigma_c64"] = [sigma.real, sigma.imag]
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/configs.json")
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    only = set(args.only.split(",")) if args.only else None
+    recs = []
+
+    def want(n):
+        return only is None or n in only
+
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    jobs = [("C1", lambda: run_energy("C1", [(T.TN_C128, "c128"), (T.TN_C64, "c64")])),
+            ("C3", lambda: run_energy("C3", [(T.TN_C64, "c64"), (T.TN_C128, "c128")])),
+            ("C2", lambda: run_amplitude("C2", (0, 0), 62)),
+            ("C4a", lambda: run_amplitude("C4a", (8, 12), 30, batched=True)),
+            ("C4b", lambda: run_amplitude("C4b", (8, 12), 30)),
+            ("C5a", lambda: run_amplitude("C5a", (3, 8), 32)),
+            ("C5b", lambda: run_amplitude("C5b", (8, 16), 32, time_slices=4, sample_slices=1))]
+    for name, fn in jobs:
+        if not want(name):
+            continue
+        try:
+            r = fn()
+        except Exception as e:  # record the failure and continue with the next config
+            r = {"config": name, "error": repr(e)}
+        import resource
+        r["host_max_rss_GB"] = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6
+        recs.append(r)
+        print(json.dumps(r), flush=True)
+        json.dump(recs, open(args.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
