@@ -185,6 +185,20 @@ tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* const* in_dev,
                        const uint64_t* out_mask, const int32_t* pv, void* out_dev, int32_t out_rank,
                        void* stream);
 
+/* A fused group: M consecutive bucket steps eliminating indices x_0 .. x_{M-1} in one pass --
+ * the exact re-association of the same sum (PAPER.md:361-368 applied M times):
+ *     out[o] = sum_{x in {0,1}^M} prod_t in_t[pext(o, out_mask[t]) + X_t(x)].
+ * Input t holds the output bits out_mask[t] as its LOW bits (in order) and the summed indices
+ * selected by x_mask[t] (bit i = x_i) as its TOP bits, x_0 the most significant (the plan's
+ * elimination-order layout).  Input t has popcount(out_mask[t]) + popcount(x_mask[t]) bits;
+ * every input must hold at least one summed index.  1 <= M <= 5, 1 <= n_in <= 8,
+ * 11 <= out_rank <= 40.  kernel: 0 = the library's choice (as in a plan), 1 = k_gemm
+ * (register-blocked batched complex GEMM, c64 only), 2 = k_pair, 3 = k_group_t; TN_E_INVAL when
+ * the requested kernel does not take this shape.  Asynchronous on `stream`. */
+tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in, const void* const* in_dev,
+                             const uint64_t* out_mask, const uint32_t* x_mask, void* out_dev,
+                             int32_t out_rank, int32_t kernel, void* stream);
+
 /* Per-step device timing for the next calls on this plan (CUDA events on the launching stream).
  * enable != 0 turns it on.  tn_profile_read returns, for standalone bucket-kernel launches since
  * the last read: count, total milliseconds and total algorithmic bytes (host outputs). */

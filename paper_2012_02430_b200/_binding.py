@@ -26,7 +26,7 @@ STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4
 SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_plan_load", "tn_plan_free", "tn_plan_info",
            "tn_plan_schedule", "tn_plan_steps", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy", "tn_energy_batch",
            "tn_workspace_bytes",
-           "tn_eliminate", "tn_profile_enable", "tn_profile_read", "tn_profile_records", "tn_last_error", "tn_version"]
+           "tn_eliminate", "tn_eliminate_group", "tn_profile_enable", "tn_profile_read", "tn_profile_records", "tn_last_error", "tn_version"]
 
 
 class TnError(RuntimeError):
@@ -99,6 +99,8 @@ _lib.tn_profile_enable.argtypes = [_P, C.c_int32]
 _lib.tn_profile_read.argtypes = [_P, C.POINTER(C.c_uint64), _D, _D, C.POINTER(C.c_uint64)]
 _lib.tn_profile_records.argtypes = [_P, C.POINTER(tn_prof_record_t), C.c_int64, C.POINTER(C.c_int64)]
 _lib.tn_last_error.restype = C.c_char_p
+_lib.tn_eliminate_group.argtypes = [C.c_int, C.c_int32, C.c_int32, C.POINTER(_P), C.POINTER(C.c_uint64),
+                                    C.POINTER(C.c_uint32), _P, C.c_int32, C.c_int32, _P]
 _lib.tn_version.restype = C.c_int32
 for _n in SYMBOLS:
     if _n not in ("tn_buffer_free", "tn_plan_free", "tn_last_error", "tn_version", "tn_workspace_bytes"):
@@ -241,6 +243,16 @@ def tn_eliminate(dtype: int, in_ptrs, out_masks, pvs, out_ptr: int, out_rank: in
     masks = (C.c_uint64 * n)(*out_masks)
     pv = (C.c_int32 * n)(*pvs)
     _check(_lib.tn_eliminate(dtype, n, ins, masks, pv, out_ptr, out_rank, stream), "tn_eliminate")
+
+
+def tn_eliminate_group(dtype: int, M: int, in_ptrs, out_masks, x_masks, out_ptr: int, out_rank: int,
+                       kernel: int, stream: int) -> None:
+    n = len(in_ptrs)
+    ins = (_P * n)(*in_ptrs)
+    masks = (C.c_uint64 * n)(*out_masks)
+    xm = (C.c_uint32 * n)(*x_masks)
+    _check(_lib.tn_eliminate_group(dtype, M, n, ins, masks, xm, out_ptr, out_rank, kernel, stream),
+           "tn_eliminate_group")
 
 
 def tn_profile_enable(h: int, enable: bool) -> None:

@@ -202,15 +202,16 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_bucket(const BigArgs a) {
   }
   for (int b = tid; b < NB; b += kBucketThreads) pbit[b] = 1ull << a.perm[b];
   __syncthreads();
+  const int nbu = min(NB - 1, max(0, (int)a.out_rank - TB));   // tile-index bits in use
   if (tid < NIN) {
     OffT c = 0;
     fcum[tid][0] = 0;
-    for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
   }
   if (tid == NIN) {
     uint64_t c = 0;
     pcum[0] = 0;
-    for (int b = 0; b < NB; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
   }
   // this CTA's contiguous range of LOGICAL tiles; the physical tile is the perm-deposit of it
   const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
@@ -455,15 +456,16 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_group_t(const GArgs a) {
   }
   for (int b = tid; b < NB; b += kBucketThreads) pbit[b] = 1ull << a.perm[b];
   __syncthreads();
+  const int nbu = min(NB - 1, max(0, (int)a.out_rank - TB));   // tile-index bits in use
   if (tid < (uint32_t)nin) {
     OffT c = 0;
     fcum[tid][0] = 0;
-    for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
   }
   if (tid == (uint32_t)nin) {
     uint64_t c = 0;
     pcum[0] = 0;
-    for (int b = 0; b < NB; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
   }
   const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * per;
@@ -670,15 +672,16 @@ __global__ void __launch_bounds__(kBucketThreads, 2) k_pair(const PArgs a) {
   }
   for (int b = tid; b < NB; b += kBucketThreads) pbit[b] = 1ull << a.perm[b];
   __syncthreads();
+  const int nbu = min(NB - 1, max(0, (int)a.out_rank - TB));   // tile-index bits in use
   if (tid < (uint32_t)nin) {
     OffT c = 0;
     fcum[tid][0] = 0;
-    for (int b = 0; b < NB; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
   }
   if (tid == (uint32_t)nin) {
     uint64_t c = 0;
     pcum[0] = 0;
-    for (int b = 0; b < NB; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
   }
   const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * per;
@@ -780,6 +783,245 @@ __global__ void __launch_bounds__(kBucketThreads, 2) k_pair(const PArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ register-blocked GEMM group
+// k_gemm: a fused group (or single step) whose varying inputs are exactly two tensors A and B is a
+// batched complex GEMM with K = 2^M:
+//     out[o] = sum_{x < K} C[x] A[F_A(o) + G_A(x)] B[F_B(o) + G_B(x)]
+// Output bits are of class a (in A only), b (in B only), c (in both: the batch).  A CTA tile is a
+// set of TB = 8 + RAB + RBB output bits chosen by the host (runtime.cu try_launch_gemm):
+//   tile-local bits 0..4  = output bits 0..4 (lanes: every warp store is 256 contiguous bytes),
+//   tile-local bits 5..7  = three more output bits (warps), preferably of class a / b,
+//   tile-local bits 8..   = RAB a-bits and RBB b-bits: each thread owns a 2^RAB x 2^RBB register
+//                           block, so every A value feeds 2^RBB outputs and every B value 2^RAB.
+// Per tile the A and B chunks (every x-row, every tile bit the input holds) are copied to shared
+// memory with cp.async one tile ahead (double buffer per input; a chunk that does not change
+// between consecutive tiles is not reloaded).  The tile-constant factor C[x] (inputs without tile
+// bits) multiplies the B values.  Complex multiply-adds use packed FP32x2 FMAs (FFMA2: one complex
+// MAC = 2 instructions).  Output written once with streaming stores.
+constexpr int kGemmThreads = 256;
+constexpr int kGemmMaxTB = 12;
+struct MArgs {
+  void* out;
+  const void* in[2];                   // A, B
+  uint64_t mask[2];                    // F_t(o) = ins0(pext(o, mask_t), pv_t)
+  uint32_t pv[2];
+  uint32_t rowoff[2][1 << kMaxGroup];  // element offset G_t(x) of chunk row r (distinct x-part)
+  uint8_t row[2][1 << kMaxGroup];      // x -> chunk row
+  uint32_t nrows[2];
+  uint32_t nch[2];                     // tile bits held by the input (chunk row = 2^nch elements)
+  uint32_t lv[2];                      // 1: chunk bit 0 is the input's position 0 (16-byte copies)
+  uint32_t posoff[2][kGemmMaxTB];      // element offset (within the input) of chunk bit k
+  int8_t chbit[2][kGemmMaxTB];         // tile-local bit u -> chunk bit of A / B (-1: absent)
+  uint8_t outbit[kGemmMaxTB];          // tile-local bit u -> output bit
+  uint32_t sm_in[2][2];                // dynamic smem element offset of buffer (input, buf)
+  uint32_t sm_dep[2];                  // dynamic smem uint32 offset of the chunk-piece offset table
+  const void* cin[kMaxIn];             // constant inputs (no tile bit)
+  uint64_t cmask[kMaxIn];
+  uint32_t cpv[kMaxIn];
+  uint32_t cgx[kMaxIn][1 << kMaxGroup];
+  int32_t nc;
+  int32_t out_rank;
+  uint8_t perm[64];                    // logical tile-index bit b -> output bit (traversal order)
+};
+
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// acc += a * b (complex, packed FP32x2: ptxas folds the broadcasts / swaps into FFMA2 operand
+// modifiers)
+__device__ __forceinline__ void cmac2(uint64_t& acc, float2 a, float2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(f2_pack(a.x, a.x)), "l"(f2_pack(b.x, b.y)));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(f2_pack(-a.y, a.y)), "l"(f2_pack(b.y, b.x)));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
+template <int M, int RAB, int RBB, bool HASC>
+__global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
+  constexpr int K = 1 << M, RA = 1 << RAB, RB = 1 << RBB;
+  constexpr int TB = 8 + RAB + RBB;
+  constexpr int NB = 64 - TB;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t n_tiles = 1ull << (a.out_rank - TB);
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float2* sm = reinterpret_cast<float2*>(dsm);
+  uint32_t* smu = reinterpret_cast<uint32_t*>(dsm);
+  __shared__ uint32_t fbit[2 + kMaxIn][NB];
+  __shared__ uint32_t fcum[2 + kMaxIn][NB + 1];
+  __shared__ uint64_t pbit[NB], pcum[NB + 1];
+  __shared__ float2 Cs[K];
+  const int nin = 2 + (HASC ? a.nc : 0);
+  auto mask_of = [&](int t) { return t < 2 ? a.mask[t] : a.cmask[t - 2]; };
+  auto pv_of = [&](int t) { return t < 2 ? a.pv[t] : a.cpv[t - 2]; };
+  const int nperm = a.out_rank - TB;
+  for (int i = tid; i < nin * NB; i += kGemmThreads) {
+    const int t = i / NB, b = i % NB;
+    fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], mask_of(t), pv_of(t)) : 0u;
+  }
+  for (int b = tid; b < NB; b += kGemmThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
+  // chunk-piece offset tables: piece ip (2^lv elements) of a chunk row -> element offset
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t np = 1u << (a.nch[u] - a.lv[u]);
+    for (uint32_t ip = tid; ip < np; ip += kGemmThreads) {
+      const uint32_t ia = ip << a.lv[u];
+      uint32_t off = 0;
+      for (uint32_t k = a.lv[u]; k < a.nch[u]; ++k)
+        if ((ia >> k) & 1u) off += a.posoff[u][k];
+      smu[a.sm_dep[u] + ip] = off;
+    }
+  }
+  __syncthreads();
+  const int nbu = min(NB - 1, max(0, (int)a.out_rank - TB));   // tile-index bits in use
+  if (tid < (uint32_t)nin) {
+    uint32_t c = 0;
+    fcum[tid][0] = 0;
+    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+  }
+  if (tid == (uint32_t)nin) {
+    uint64_t c = 0;
+    pcum[0] = 0;
+    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+  }
+  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t obase = 0;
+  for (int b = 0; b < nperm && (t0 >> b); ++b)
+    if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
+  // this thread's tile-local output offset and chunk indices (lanes + warps), register blocks
+  uint64_t othr = 0;
+  uint32_t iathr = 0, ibthr = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if ((tid >> k) & 1u) {
+      othr += 1ull << a.outbit[k];
+      if (a.chbit[0][k] >= 0) iathr += 1u << a.chbit[0][k];
+      if (a.chbit[1][k] >= 0) ibthr += 1u << a.chbit[1][k];
+    }
+  }
+  uint64_t ora[RA], orb[RB];
+  uint32_t iar[RA], ibr[RB];
+#pragma unroll
+  for (int i = 0; i < RA; ++i) {
+    ora[i] = 0; iar[i] = 0;
+#pragma unroll
+    for (int k = 0; k < RAB; ++k)
+      if ((i >> k) & 1) { ora[i] += 1ull << a.outbit[8 + k]; iar[i] += 1u << a.chbit[0][8 + k]; }
+  }
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    orb[j] = 0; ibr[j] = 0;
+#pragma unroll
+    for (int k = 0; k < RBB; ++k)
+      if ((j >> k) & 1) { orb[j] += 1ull << a.outbit[8 + RAB + k]; ibr[j] += 1u << a.chbit[1][8 + RAB + k]; }
+  }
+  uint32_t cur[2], curc[kMaxIn - 2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
+#pragma unroll
+  for (int t = 0; t < kMaxIn - 2; ++t)
+    curc[t] = (HASC && t < a.nc) ? (uint32_t)fmap(obase, a.cmask[t], a.cpv[t]) : 0u;
+  float2* out = static_cast<float2*>(a.out);
+  __syncthreads();
+
+  // cp.async of input u's chunk (all rows) at base offset `base` into buffer `buf`
+  auto prefetch = [&](int u, uint32_t base, int buf) {
+    const float2* src = static_cast<const float2*>(a.in[u]) + base;
+    float2* dst = sm + a.sm_in[u][buf];
+    const uint32_t lp = a.nch[u] - a.lv[u];
+    const uint32_t np = a.nrows[u] << lp;
+    const uint32_t* dep = smu + a.sm_dep[u];
+    if (a.lv[u]) {
+      for (uint32_t c = tid; c < np; c += kGemmThreads) {
+        const uint32_t r = c >> lp, ip = c & ((1u << lp) - 1u);
+        cp_async16(dst + (c << 1), src + a.rowoff[u][r] + dep[ip]);
+      }
+    } else {
+      for (uint32_t c = tid; c < np; c += kGemmThreads) {
+        const uint32_t r = c >> lp, ip = c & ((1u << lp) - 1u);
+        cp_async8(dst + c, src + a.rowoff[u][r] + dep[ip]);
+      }
+    }
+  };
+  int bA = 0, bB = 0;
+  if (t0 < t1) { prefetch(0, cur[0], 0); prefetch(1, cur[1], 0); }
+  cp_async_commit();
+
+  for (uint64_t tile = t0; tile < t1; ++tile) {
+    const int r = __ffsll((long long)~tile) - 1;
+    const bool has_next = tile + 1 < t1;
+    if (HASC && tid < (uint32_t)K) {
+      float2 c = make_float2(1.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kMaxIn - 2; ++t)
+        if (t < a.nc) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + curc[t] + a.cgx[t][tid]));
+      Cs[tid] = c;
+    }
+    bool chA = false, chB = false;
+    if (has_next) {
+      chA = fbit[0][r] != fcum[0][r];
+      chB = fbit[1][r] != fcum[1][r];
+      if (chA) prefetch(0, cur[0] + fbit[0][r] - fcum[0][r], bA ^ 1);
+      if (chB) prefetch(1, cur[1] + fbit[1][r] - fcum[1][r], bB ^ 1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const float2* sA = sm + a.sm_in[0][bA] + iathr;
+    const float2* sB = sm + a.sm_in[1][bB] + ibthr;
+    uint64_t acc[RA][RB];
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+      for (int j = 0; j < RB; ++j) acc[i][j] = 0ull;
+#pragma unroll
+    for (int x = 0; x < K; ++x) {
+      const float2* pa = sA + ((uint32_t)a.row[0][x] << a.nch[0]);
+      const float2* pb = sB + ((uint32_t)a.row[1][x] << a.nch[1]);
+      float2 av[RA], bv[RB];
+#pragma unroll
+      for (int i = 0; i < RA; ++i) av[i] = pa[iar[i]];
+#pragma unroll
+      for (int j = 0; j < RB; ++j) bv[j] = pb[ibr[j]];
+      if (HASC) {
+        const float2 c = Cs[x];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) bv[j] = cmul(bv[j], c);
+      }
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < RB; ++j) cmac2(acc[i][j], av[i], bv[j]);
+    }
+    float2* ot = out + obase + othr;
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+      for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(acc[i][j]));
+    __syncthreads();
+    if (chA) bA ^= 1;
+    if (chB) bB ^= 1;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) cur[u] = cur[u] + fbit[u][r] - fcum[u][r];
+#pragma unroll
+    for (int t = 0; t < kMaxIn - 2; ++t)
+      if (HASC && t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
+    obase = obase + pbit[r] - pcum[r];
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------ fused reduce chain
 // m consecutive reduce steps eliminate the top m bits of A; the weights of step i are rank-1 on
 // its summed index.  Re-associated (exact): out[o] = sum_x W[x] A[o + x n_out], W[x] =
@@ -794,9 +1036,7 @@ struct ChainArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kBucketThreads) k_chain(const ChainArgs a) {
-  constexpr int VEC = VecT<T>::n;
-  __shared__ T W[1 << kMaxChain];
+__device__ __forceinline__ void chain_weights(const ChainArgs& a, T* W) {
   const int nx = 1 << a.m;
   for (int x = threadIdx.x; x < nx; x += blockDim.x) {
     T acc = cfrom<T>(1.0, 0.0);
@@ -806,6 +1046,64 @@ __global__ void __launch_bounds__(kBucketThreads) k_chain(const ChainArgs a) {
     }
     W[x] = acc;
   }
+}
+
+// small outputs: the x range is split over the 8 warps of a CTA (lane = one output vector, 32
+// consecutive vectors per CTA), partial sums combined in shared memory -- 2^out/(32 VEC) CTAs
+// instead of 2^out/(256 VEC) threads each walking all 2^m rows
+template <typename T>
+__global__ void __launch_bounds__(kBucketThreads) k_chain_split(const ChainArgs a) {
+  constexpr int VEC = VecT<T>::n;
+  constexpr int NW = kBucketThreads / 32;
+  __shared__ T W[1 << kMaxChain];
+  __shared__ T part[NW][32 * VEC];
+  chain_weights<T>(a, W);
+  __syncthreads();
+  const uint64_t n_out = 1ull << a.out_rank;
+  const T* A = static_cast<const T*>(a.A);
+  T* out = static_cast<T*>(a.out);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nx = 1 << a.m;
+  const int per = (nx + NW - 1) / NW;
+  const int x0 = w * per, x1 = min(nx, x0 + per);
+  for (uint64_t blk = blockIdx.x; blk * 32 * VEC < n_out; blk += gridDim.x) {
+    const uint64_t o = (blk * 32 + lane) * VEC;
+    if constexpr (VEC == 2) {
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int x = x0; x < x1; ++x) {
+        const float4 u = __ldcs(reinterpret_cast<const float4*>(A + o + (uint64_t)x * n_out));
+        const float2 wv = reinterpret_cast<const float2&>(W[x]);
+        acc0.x = fmaf(wv.x, u.x, fmaf(-wv.y, u.y, acc0.x));
+        acc0.y = fmaf(wv.x, u.y, fmaf(wv.y, u.x, acc0.y));
+        acc1.x = fmaf(wv.x, u.z, fmaf(-wv.y, u.w, acc1.x));
+        acc1.y = fmaf(wv.x, u.w, fmaf(wv.y, u.z, acc1.y));
+      }
+      part[w][2 * lane] = reinterpret_cast<const T&>(acc0);
+      part[w][2 * lane + 1] = reinterpret_cast<const T&>(acc1);
+    } else {
+      T acc = cfrom<T>(0.0, 0.0);
+#pragma unroll 4
+      for (int x = x0; x < x1; ++x) acc = cadd(acc, cmul(W[x], __ldcs(A + o + (uint64_t)x * n_out)));
+      part[w][lane] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 * VEC) {
+      T s = part[0][threadIdx.x];
+#pragma unroll
+      for (int k = 1; k < NW; ++k) s = cadd(s, part[k][threadIdx.x]);   // fixed order
+      out[blk * 32 * VEC + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBucketThreads) k_chain(const ChainArgs a) {
+  constexpr int VEC = VecT<T>::n;
+  __shared__ T W[1 << kMaxChain];
+  chain_weights<T>(a, W);
+  const int nx = 1 << a.m;
   __syncthreads();
   const uint64_t n_out = 1ull << a.out_rank;
   const T* A = static_cast<const T*>(a.A);
@@ -934,7 +1232,7 @@ __global__ void k_finalize(const ScalarRec* __restrict__ scal, int b, int e, con
 }
 
 // fixed pairwise tree over j (identical to the host tn_sum_partials)
-__global__ void k_pairwise(double* __restrict__ buf, uint64_t n, double* __restrict__ out) {
+static __global__ void k_pairwise(double* __restrict__ buf, uint64_t n, double* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (n == 0) { out[0] = out[1] = 0.0; return; }
   uint64_t m = n;

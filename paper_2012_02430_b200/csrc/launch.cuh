@@ -1,0 +1,106 @@
+// launch.cuh -- host-side launch helpers shared by the translation units of libtnb200.so:
+// shape classification of a bucket step / fused group and the per-kernel launch entry points
+// (launch_bucket.cu: k_bucket; launch_group_c64.cu / launch_group_c128.cu: k_group_t;
+// launch_pair.cu: k_pair; launch_gemm.cu: k_gemm).  Split so nvcc compiles them in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace tnb {
+
+// opt in to more than 48 KB of (static + dynamic) shared memory, once per kernel instantiation
+template <typename K>
+inline void allow_smem(K kernel, size_t dyn) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> granted;   // per kernel (per device is not needed: the
+                                                   // attribute is a function property)
+  if (dyn + 16 * 1024 <= 48 * 1024) return;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& g = granted[reinterpret_cast<const void*>(kernel)];
+  if (dyn > g) {
+    const size_t want = std::max<size_t>(dyn, 100 * 1024);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    g = want;
+  }
+}
+
+inline bool debug_checks() {
+  static const int on = [] {
+    const char* v = std::getenv("TNB_DEBUG");
+    return (v && v[0] == '1') ? 1 : 0;
+  }();
+  return on != 0;
+}
+inline int num_sms() {
+  static int g_num_sms = 0;
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+inline uint64_t host_pext(uint64_t x, uint64_t m) {
+  uint64_t r = 0;
+  int k = 0;
+  while (m) {
+    const uint64_t b = m & (~m + 1);
+    if (x & b) r |= 1ull << k;
+    ++k;
+    m ^= b;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------- k_group_t host side
+struct GIn {
+  const void* ptr;
+  uint64_t out_mask;   // output bits present (relative to the group output)
+  uint32_t pv;         // F_t(o) = ins0(pext(o, out_mask), pv)
+  uint32_t rank;       // bits of the input (for 32/64-bit offsets)
+  bool full;           // holds every output bit and every summed bit (read exactly once)
+  uint64_t gx[1 << kMaxGroup];
+};
+struct GDesc {
+  void* out;
+  int out_rank;
+  int M;
+  int n;
+  GIn in[kMaxIn];
+};
+
+inline uint64_t host_fmap(uint64_t o, uint64_t mask, uint32_t pv) {
+  const uint64_t r = host_pext(o, mask);
+  const uint64_t lo = r & ((1ull << pv) - 1);
+  return lo | ((r >> pv) << (pv + 1));
+}
+
+inline bool env_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && v[0] == '1';
+}
+inline bool gemm_disabled() {
+  static const bool off = env_flag("TNB_NO_GEMM");
+  return off;
+}
+
+
+// entry points (explicitly instantiated for float2 and double2 in their translation units);
+// each returns false when the shape has no instantiation / does not qualify
+template <typename T> bool try_launch_gemm(const GDesc& g, cudaStream_t st);
+template <typename T> bool try_launch_pair(const GDesc& g, cudaStream_t st);
+template <typename T> bool try_launch_group(const GDesc& g, cudaStream_t st);
+template <typename T> void launch_bucket_generic(const BigArgs& a, cudaStream_t st);   // k_bucket<T, n_in>
+
+}  // namespace tnb

@@ -13,10 +13,12 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/tn_b200.h"
 #include "kernels.cuh"
+#include "launch.cuh"
 #include "plan_format.h"
 #include "planner.h"
 
@@ -445,402 +447,6 @@ tn_status ensure_dev(tn_plan* pl, DevTables** out) {
   return TN_OK;
 }
 
-// opt in to more than 48 KB of (static + dynamic) shared memory, once per kernel instantiation
-template <typename K>
-void allow_smem(K kernel, size_t dyn) {
-  static std::mutex mu;
-  static std::map<const void*, size_t> granted;   // per kernel (per device is not needed: the
-                                                   // attribute is a function property)
-  if (dyn + 16 * 1024 <= 48 * 1024) return;
-  std::lock_guard<std::mutex> lk(mu);
-  size_t& g = granted[reinterpret_cast<const void*>(kernel)];
-  if (dyn > g) {
-    const size_t want = std::max<size_t>(dyn, 100 * 1024);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
-    g = want;
-  }
-}
-
-int g_num_sms = 0;
-bool debug_checks() {
-  static const int on = [] {
-    const char* v = std::getenv("TNB_DEBUG");
-    return (v && v[0] == '1') ? 1 : 0;
-  }();
-  return on != 0;
-}
-int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
-uint64_t host_pext(uint64_t x, uint64_t m) {
-  uint64_t r = 0;
-  int k = 0;
-  while (m) {
-    const uint64_t b = m & (~m + 1);
-    if (x & b) r |= 1ull << k;
-    ++k;
-    m ^= b;
-  }
-  return r;
-}
-
-// host side of the staging decision (see kernels.cuh): an input is staged in shared memory when
-// it holds some but not all of a tile's low output bits, those map to its lowest positions, and
-// the chunks fit the budget
-template <typename T>
-void plan_staging(BigArgs& a) {
-  constexpr int TB = TileBits<T>::v;
-  const uint64_t inner = (1ull << TB) - 1;
-  uint32_t off = 0;
-  for (int t = 0; t < a.n_in; ++t) {
-    a.flags[t] &= ~F_STAGED;
-    const uint64_t lowm = a.out_mask[t] & inner;
-    const int nlow = __builtin_popcountll(lowm);
-    if (a.out_rank <= TB || nlow == 0 || nlow >= TB || nlow > 10) continue;
-    // contiguity: the tile's low output bits must be the input's positions 0..nlow-1
-    uint64_t f = 0;
-    {
-      uint64_t m = a.out_mask[t], r = 0;
-      int k = 0;
-      for (int b = 0; b < 64 && m; ++b) {
-        if ((m >> b) & 1) {
-          if ((lowm >> b) & 1) r |= 1ull << k;
-          ++k;
-          m &= ~(1ull << b);
-        }
-      }
-      const uint64_t lo = r & ((1ull << a.pv[t]) - 1);
-      f = lo | ((r >> a.pv[t]) << (a.pv[t] + 1));
-    }
-    if (f != (1ull << nlow) - 1) continue;
-    const uint32_t need = 2u << nlow;  // both x
-    if ((off + need) * sizeof(T) * 2 > 48 * 1024) continue;
-    a.flags[t] |= F_STAGED;
-    a.nlow[t] = (uint32_t)nlow;
-    a.stage_off[t] = off;
-    off += need;
-  }
-  a.stage_elems = off;
-}
-
-// traversal order of the tile-index bits: bits absent from the largest input first (its chunk
-// is then reused by consecutive tiles), then bits absent from the second largest, then the rest
-// in ascending order.  Streaming (evict-first) loads only for inputs without reuse.
-template <typename T>
-void plan_order(BigArgs& a) {
-  constexpr int TB = TileBits<T>::v;
-  int big[2] = {-1, -1};
-  for (int t = 0; t < a.n_in; ++t) {
-    const int r = __builtin_popcountll(a.out_mask[t]);
-    if (big[0] < 0 || r > __builtin_popcountll(a.out_mask[big[0]])) { big[1] = big[0]; big[0] = t; }
-    else if (big[1] < 0 || r > __builtin_popcountll(a.out_mask[big[1]])) big[1] = t;
-  }
-  std::vector<int> bits;
-  for (int b = TB; b < 64; ++b) bits.push_back(b);
-  auto has = [&](int t, int b) { return t >= 0 && ((a.out_mask[t] >> b) & 1); };
-  std::stable_sort(bits.begin(), bits.end(), [&](int x, int y) {
-    if (has(big[0], x) != has(big[0], y)) return !has(big[0], x);
-    if (has(big[1], x) != has(big[1], y)) return !has(big[1], x);
-    return x < y;
-  });
-  // bits at or above out_rank never change within the grid; keep them last
-  std::stable_partition(bits.begin(), bits.end(), [&](int b) { return b < a.out_rank; });
-  for (int i = 0; i < 64 - TB; ++i) a.perm[i] = (uint8_t)(bits[i] - TB);
-  const uint64_t full = a.out_rank >= 64 ? ~0ull : ((1ull << a.out_rank) - 1);
-  for (int t = 0; t < a.n_in; ++t) {
-    if (a.out_mask[t] == full && a.out_rank >= 16) a.flags[t] |= F_STREAM;
-    else a.flags[t] &= ~F_STREAM;
-  }
-}
-
-template <typename T, int NIN>
-void launch_bucket_n(BigArgs a, cudaStream_t st) {
-  constexpr uint64_t TILE = 1ull << TileBits<T>::v;
-  plan_order<T>(a);
-  plan_staging<T>(a);
-  const uint64_t n_out = 1ull << a.out_rank;
-  const uint64_t tiles = (n_out + TILE - 1) / TILE;
-  const uint64_t cap = (uint64_t)num_sms() * 4;
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, cap);
-  const size_t smem = (size_t)a.stage_elems * sizeof(T) * 2;
-  bool wide = false;   // any input with more than 32 bits -> 64-bit offsets
-  for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
-  if (wide) {
-    allow_smem(k_bucket<T, NIN, uint64_t>, smem);
-    k_bucket<T, NIN, uint64_t><<<grid, kBucketThreads, smem, st>>>(a);
-  } else {
-    allow_smem(k_bucket<T, NIN, uint32_t>, smem);
-    k_bucket<T, NIN, uint32_t><<<grid, kBucketThreads, smem, st>>>(a);
-  }
-}
-
-// ---------------------------------------------------------------- k_group_t host side
-struct GIn {
-  const void* ptr;
-  uint64_t out_mask;   // output bits present (relative to the group output)
-  uint32_t pv;         // F_t(o) = ins0(pext(o, out_mask), pv)
-  uint32_t rank;       // bits of the input (for 32/64-bit offsets)
-  bool full;           // holds every output bit and every summed bit (read exactly once)
-  uint64_t gx[1 << kMaxGroup];
-};
-struct GDesc {
-  void* out;
-  int out_rank;
-  int M;
-  int n;
-  GIn in[kMaxIn];
-};
-
-uint64_t host_fmap(uint64_t o, uint64_t mask, uint32_t pv) {
-  const uint64_t r = host_pext(o, mask);
-  const uint64_t lo = r & ((1ull << pv) - 1);
-  return lo | ((r >> pv) << (pv + 1));
-}
-
-template <typename T, typename OffT, int NDIR, int NSTG, int M, int NDV>
-void launch_g(const GArgs& ga, unsigned grid, size_t smem, cudaStream_t st) {
-  allow_smem(k_group_t<T, OffT, NDIR, NSTG, M, NDV>, smem);
-  k_group_t<T, OffT, NDIR, NSTG, M, NDV><<<grid, kBucketThreads, smem, st>>>(ga);
-}
-
-template <typename T, typename OffT, int M>
-bool dispatch_g(const GArgs& ga, int nd, int ns, int ndv, unsigned grid, size_t smem, cudaStream_t st) {
-#define TN_G(D, S, V) \
-  if (nd == D && ns == S && ndv == V) { launch_g<T, OffT, D, S, M, V>(ga, grid, smem, st); return true; }
-  TN_G(1, 0, 1) TN_G(2, 0, 2) TN_G(0, 1, 0) TN_G(1, 1, 1) TN_G(0, 2, 0) TN_G(2, 1, 2) TN_G(1, 2, 1)
-  TN_G(1, 0, 0) TN_G(2, 0, 1) TN_G(1, 1, 0) TN_G(2, 1, 1)
-  if constexpr (M == 1) {
-    TN_G(3, 0, 3) TN_G(2, 2, 2) TN_G(0, 3, 0) TN_G(1, 3, 1) TN_G(0, 4, 0) TN_G(3, 0, 2) TN_G(2, 0, 0)
-  }
-#undef TN_G
-  return false;
-}
-
-// Classify the inputs (direct / staged / constant), build GArgs and launch k_group_t.  Returns
-// false when the shape has no instantiation (the caller then runs the generic path).
-template <typename T>
-bool try_launch_group(const GDesc& g, cudaStream_t st) {
-  constexpr int TB = TileBits<T>::v;
-  constexpr uint64_t TILE = 1ull << TB;
-  if (g.out_rank <= TB || g.M < 1 || g.M > kMaxGroup || g.n < 1 || g.n > kMaxIn) return false;
-  const uint64_t inner = TILE - 1;
-  const int NX = 1 << g.M;
-  // traversal order of the tile bits: bits absent from the two largest varying inputs first
-  int big[2] = {-1, -1};
-  for (int t = 0; t < g.n; ++t) {
-    const int r = __builtin_popcountll(g.in[t].out_mask);
-    if (big[0] < 0 || r > __builtin_popcountll(g.in[big[0]].out_mask)) { big[1] = big[0]; big[0] = t; }
-    else if (big[1] < 0 || r > __builtin_popcountll(g.in[big[1]].out_mask)) big[1] = t;
-  }
-  auto has = [&](int t, int b) { return t >= 0 && ((g.in[t].out_mask >> b) & 1); };
-  std::vector<int> bits;
-  for (int b = TB; b < 64; ++b) bits.push_back(b);
-  std::stable_sort(bits.begin(), bits.end(), [&](int x, int y) {
-    if (has(big[0], x) != has(big[0], y)) return !has(big[0], x);
-    if (has(big[1], x) != has(big[1], y)) return !has(big[1], x);
-    return x < y;
-  });
-  std::stable_partition(bits.begin(), bits.end(), [&](int b) { return b < g.out_rank; });
-
-  int dir[kMaxIn], dirs[kMaxIn], stg[kMaxIn], cst[kMaxIn], nd = 0, nds = 0, ns = 0, nc = 0;
-  int nlow_of[kMaxIn] = {0};
-  uint32_t nparts_of[kMaxIn] = {0};
-  uint32_t soff = 0;
-  for (int t = 0; t < g.n; ++t) {
-    const GIn& in = g.in[t];
-    const uint64_t lowm = in.out_mask & inner;
-    const int nlow = __builtin_popcountll(lowm);
-    if (nlow == 0) { cst[nc++] = t; continue; }
-    const bool vec_ok = (VecT<T>::n == 1) || ((in.out_mask & 1) && in.pv != 0);
-    // staging needs the tile's low output bits at the input's lowest positions
-    const bool contig = host_fmap(lowm, in.out_mask, in.pv) == (1ull << nlow) - 1;
-    std::vector<uint64_t> parts;
-    for (int x = 0; x < NX; ++x)
-      if (std::find(parts.begin(), parts.end(), in.gx[x]) == parts.end()) parts.push_back(in.gx[x]);
-    const uint32_t need = (uint32_t)parts.size() << nlow;
-    const bool stageable = contig && nlow < TB && (nlow <= TB - 3 || !vec_ok) &&
-                           (soff + need) * sizeof(T) * 2 <= 48 * 1024;
-    if (stageable) {
-      nlow_of[t] = nlow;
-      nparts_of[t] = (uint32_t)parts.size();
-      stg[ns++] = t;
-      soff += need;
-    } else if (vec_ok) {
-      dir[nd++] = t;
-    } else {
-      dirs[nds++] = t;   // direct, 8-byte loads
-    }
-  }
-  const int ndv = nd;
-  for (int i = 0; i < nds; ++i) dir[nd++] = dirs[i];
-  if (nd + ns == 0) return false;
-  GArgs ga;   // host copy; passed by value as the launch parameters
-  std::memset(&ga, 0, sizeof(ga));
-  ga.out = g.out;
-  ga.out_rank = g.out_rank;
-  ga.nc = nc;
-  for (int i = 0; i < 64 - TB; ++i) ga.perm[i] = (uint8_t)(bits[i] - TB);
-  const uint64_t full = (1ull << g.out_rank) - 1;
-  int k = 0;
-  uint32_t off = 0;
-  bool wide = false;
-  auto put = [&](int t) {
-    const GIn& in = g.in[t];
-    ga.in[k] = in.ptr;
-    ga.out_mask[k] = in.out_mask;
-    ga.pv[k] = in.pv;
-    ga.stream[k] = (in.full && in.out_mask == full && g.out_rank >= 16) ? 1u : 0u;
-    for (int x = 0; x < NX; ++x) ga.gx[k][x] = in.gx[x];
-    wide |= in.rank > 32;
-    ++k;
-  };
-  for (int i = 0; i < nd; ++i) put(dir[i]);
-  for (int i = 0; i < ns; ++i) {
-    const int t = stg[i];
-    std::vector<uint64_t> parts;
-    for (int x = 0; x < NX; ++x) {
-      auto it = std::find(parts.begin(), parts.end(), g.in[t].gx[x]);
-      uint32_t pi;
-      if (it == parts.end()) {
-        pi = (uint32_t)parts.size();
-        parts.push_back(g.in[t].gx[x]);
-        ga.rep[k][pi] = (uint8_t)x;
-      } else {
-        pi = (uint32_t)(it - parts.begin());
-      }
-      ga.sx[k][x] = off + (pi << nlow_of[t]);
-    }
-    ga.nlow[k] = (uint32_t)nlow_of[t];
-    ga.nparts[k] = nparts_of[t];
-    off += nparts_of[t] << nlow_of[t];
-    put(t);
-  }
-  for (int i = 0; i < nc; ++i) put(cst[i]);
-  ga.stage_elems = off;
-  const uint64_t tiles = ((1ull << g.out_rank) + TILE - 1) / TILE;
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 4);
-  const size_t smem = (size_t)off * sizeof(T) * 2;
-  if (wide) return g.M == 1 ? dispatch_g<T, uint64_t, 1>(ga, nd, ns, ndv, grid, smem, st) : false;
-  switch (g.M) {
-    case 1: return dispatch_g<T, uint32_t, 1>(ga, nd, ns, ndv, grid, smem, st);
-    case 2: return dispatch_g<T, uint32_t, 2>(ga, nd, ns, ndv, grid, smem, st);
-    case 3: return dispatch_g<T, uint32_t, 3>(ga, nd, ns, ndv, grid, smem, st);
-    case 4: return dispatch_g<T, uint32_t, 4>(ga, nd, ns, ndv, grid, smem, st);
-    case 5: return dispatch_g<T, uint32_t, 5>(ga, nd, ns, ndv, grid, smem, st);
-    default: return false;
-  }
-}
-
-// register-blocked pair kernel (k_pair) for groups with exactly two varying inputs
-template <typename T, typename OffT, int M>
-void launch_p(const PArgs& pa, unsigned grid, size_t smem, cudaStream_t st) {
-  allow_smem(k_pair<T, OffT, M>, smem);
-  k_pair<T, OffT, M><<<grid, kBucketThreads, smem, st>>>(pa);
-}
-
-template <typename T>
-bool try_launch_pair(const GDesc& g, cudaStream_t st) {
-  constexpr int TB = kPairTB;
-  constexpr uint64_t TILE = 1ull << TB;
-  if (g.out_rank < TB + 1 || g.M < 2 || g.M > kMaxGroup) return false;
-  const uint64_t inner = TILE - 1;
-  const int NX = 1 << g.M;
-  int var[2], nv = 0, cst[kMaxIn], nc = 0;
-  for (int t = 0; t < g.n; ++t) {
-    if ((g.in[t].out_mask & inner) == 0) { cst[nc++] = t; continue; }
-    if (nv == 2) return false;
-    var[nv++] = t;
-  }
-  if (nv != 2) return false;
-  PArgs pa;
-  std::memset(&pa, 0, sizeof(pa));
-  // staging layout: the tile bits of each input must be its lowest positions
-  uint32_t off = 0;
-  bool wide = false;
-  for (int u = 0; u < 2; ++u) {
-    const GIn& in = g.in[var[u]];
-    const uint64_t lowm = in.out_mask & inner;
-    const int nlow = __builtin_popcountll(lowm);
-    if (host_fmap(lowm, in.out_mask, in.pv) != (1ull << nlow) - 1) return false;
-    if ((1u << nlow) * sizeof(T) < 16) return false;
-    std::vector<uint64_t> parts;
-    for (int x = 0; x < NX; ++x) {
-      auto it = std::find(parts.begin(), parts.end(), in.gx[x]);
-      uint32_t pi;
-      if (it == parts.end()) {
-        pi = (uint32_t)parts.size();
-        parts.push_back(in.gx[x]);
-        pa.rep[u][pi] = (uint8_t)x;
-      } else {
-        pi = (uint32_t)(it - parts.begin());
-      }
-      pa.sx[u][x] = off + (pi << nlow);
-    }
-    pa.in[u] = in.ptr;
-    pa.mask[u] = in.out_mask;
-    pa.pv[u] = in.pv;
-    for (int x = 0; x < NX; ++x) pa.gx[u][x] = in.gx[x];
-    pa.nparts[u] = (uint32_t)parts.size();
-    pa.nlow[u] = (uint32_t)nlow;
-    off += (uint32_t)parts.size() << nlow;
-    wide |= in.rank > 32;
-  }
-  const size_t smem = (size_t)off * sizeof(T) * 2;
-  if (smem > 96 * 1024 || wide) return false;
-  pa.stage_elems = off;
-  // block bits: a tile bit in A only and one in B only, preferring bits >= 5 (lanes keep bits 0-4)
-  const uint64_t mA = g.in[var[0]].out_mask & inner, mB = g.in[var[1]].out_mask & inner;
-  int ra = -1, rb = -1;
-  for (int b = TB - 1; b >= 0; --b) {
-    if (ra < 0 && ((mA >> b) & 1) && !((mB >> b) & 1)) ra = b;
-    if (rb < 0 && ((mB >> b) & 1) && !((mA >> b) & 1)) rb = b;
-  }
-  if (ra < 0 || rb < 0) return false;
-  pa.ra = (uint32_t)ra;
-  pa.rb = (uint32_t)rb;
-  int k = 0;
-  for (int b = 0; b < TB; ++b)
-    if (b != ra && b != rb) pa.tbits[k++] = (uint32_t)b;
-  for (int i = 0; i < nc; ++i) {
-    const GIn& in = g.in[cst[i]];
-    pa.cin[i] = in.ptr;
-    pa.cmask[i] = in.out_mask;
-    pa.cpv[i] = in.pv;
-    for (int x = 0; x < NX; ++x) pa.cgx[i][x] = in.gx[x];
-  }
-  pa.nc = nc;
-  pa.out = g.out;
-  pa.out_rank = g.out_rank;
-  // traversal: tile bits absent from the larger input first
-  const int big = __builtin_popcountll(g.in[var[0]].out_mask) >= __builtin_popcountll(g.in[var[1]].out_mask) ? 0 : 1;
-  auto has = [&](int u, int b) { return (g.in[var[u]].out_mask >> b) & 1; };
-  std::vector<int> bits;
-  for (int b = TB; b < 64; ++b) bits.push_back(b);
-  std::stable_sort(bits.begin(), bits.end(), [&](int x, int y) {
-    if (has(big, x) != has(big, y)) return !has(big, x);
-    if (has(1 - big, x) != has(1 - big, y)) return !has(1 - big, x);
-    return x < y;
-  });
-  std::stable_partition(bits.begin(), bits.end(), [&](int b) { return b < g.out_rank; });
-  for (int i = 0; i < 64 - TB; ++i) pa.perm[i] = (uint8_t)(bits[i] - TB);
-  const uint64_t tiles = ((1ull << g.out_rank) + TILE - 1) / TILE;
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 2);
-  switch (g.M) {
-    case 2: launch_p<T, uint32_t, 2>(pa, grid, smem, st); return true;
-    case 3: launch_p<T, uint32_t, 3>(pa, grid, smem, st); return true;
-    case 4: launch_p<T, uint32_t, 4>(pa, grid, smem, st); return true;
-    case 5: launch_p<T, uint32_t, 5>(pa, grid, smem, st); return true;
-    default: return false;
-  }
-}
-
 // single bucket step as a group with M = 1 (G_t(x) = x << pv_t)
 template <typename T>
 bool try_launch_specialised(const BigArgs& a, cudaStream_t st) {
@@ -860,22 +466,13 @@ bool try_launch_specialised(const BigArgs& a, cudaStream_t st) {
     g.in[t].gx[0] = 0;
     g.in[t].gx[1] = 1ull << a.pv[t];
   }
-  return try_launch_group<T>(g, st);
+  return try_launch_gemm<T>(g, st) || try_launch_group<T>(g, st);
 }
 
 template <typename T>
 void launch_bucket(const BigArgs& a, cudaStream_t st) {
   if (try_launch_specialised<T>(a, st)) return;
-  switch (a.n_in) {
-    case 1: launch_bucket_n<T, 1>(a, st); break;
-    case 2: launch_bucket_n<T, 2>(a, st); break;
-    case 3: launch_bucket_n<T, 3>(a, st); break;
-    case 4: launch_bucket_n<T, 4>(a, st); break;
-    case 5: launch_bucket_n<T, 5>(a, st); break;
-    case 6: launch_bucket_n<T, 6>(a, st); break;
-    case 7: launch_bucket_n<T, 7>(a, st); break;
-    default: launch_bucket_n<T, 8>(a, st); break;
-  }
+  launch_bucket_generic<T>(a, st);
 }
 
 cudaEvent_t pool_event(tn_plan* pl) {
@@ -970,8 +567,15 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       constexpr int VEC = VecT<T>::n;
       const uint64_t work = ((1ull << c.out_rank) + VEC - 1) / VEC;
       const uint64_t blocks = (work + kBucketThreads - 1) / kBucketThreads;
-      const unsigned grid = (unsigned)std::min<uint64_t>(blocks, (uint64_t)num_sms() * 8);
-      k_chain<T><<<grid, kBucketThreads, 0, st>>>(c);
+      if (blocks < (uint64_t)num_sms() * 2 && c.m >= 3 && (1ull << c.out_rank) >= 32ull * VEC) {
+        // few outputs, many rows: split the rows over the warps of a CTA (k_chain_split)
+        const uint64_t nblk = (1ull << c.out_rank) / (32ull * VEC);
+        const unsigned g2 = (unsigned)std::min<uint64_t>(nblk, (uint64_t)num_sms() * 8);
+        k_chain_split<T><<<g2, kBucketThreads, 0, st>>>(c);
+      } else {
+        const unsigned grid = (unsigned)std::min<uint64_t>(blocks, (uint64_t)num_sms() * 8);
+        k_chain<T><<<grid, kBucketThreads, 0, st>>>(c);
+      }
     } else if (op.type == OP_GROUP) {
       // head step + (M-1) in-place reduce followers with rank-1 weights, summed in one pass
       const StepRec& h = pl->steps[op.begin];
@@ -1017,7 +621,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       bool launched = false;
       if (ok) {
         ProfScope ps(pl, st, bytes * sizeof(T), op.begin, op.end, 3, Rf);
-        launched = try_launch_pair<T>(g, st) || try_launch_group<T>(g, st);
+        launched = try_launch_gemm<T>(g, st) || try_launch_pair<T>(g, st) || try_launch_group<T>(g, st);
         ps.cancel = !launched;
       }
       if (!launched)   // no instantiation for this shape: run the steps one by one
@@ -1277,6 +881,62 @@ extern "C" tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* cons
     return TN_OK;
   }
   if (dtype == TN_C64) launch_bucket<float2>(a, st); else launch_bucket<double2>(a, st);
+  CU(cudaGetLastError());
+  return TN_OK;
+}
+
+extern "C" tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in, const void* const* in_dev,
+                                        const uint64_t* out_mask, const uint32_t* x_mask, void* out_dev,
+                                        int32_t out_rank, int32_t kernel, void* stream) {
+  if (M < 1 || M > kMaxGroup || n_in < 1 || n_in > kMaxIn || !in_dev || !out_mask || !x_mask || !out_dev)
+    return fail(TN_E_INVAL, "tn_eliminate_group: bad argument");
+  if (out_rank < 11 || out_rank > 40) return fail(TN_E_INVAL, "tn_eliminate_group: out_rank out of range");
+  if (dtype != TN_C64 && dtype != TN_C128) return fail(TN_E_DTYPE, "unsupported dtype");
+  if (kernel < 0 || kernel > 3) return fail(TN_E_INVAL, "tn_eliminate_group: unknown kernel");
+  GDesc g;
+  std::memset(&g, 0, sizeof(g));
+  g.out = out_dev;
+  g.out_rank = out_rank;
+  g.M = M;
+  g.n = n_in;
+  const uint64_t full = (1ull << out_rank) - 1;
+  for (int t = 0; t < n_in; ++t) {
+    if (!in_dev[t] || (out_mask[t] & ~full) || (x_mask[t] >> M) || x_mask[t] == 0)
+      return fail(TN_E_INVAL, "tn_eliminate_group: bad input " + std::to_string(t));
+    GIn& gi = g.in[t];
+    const int ro = __builtin_popcountll(out_mask[t]);
+    const int rx = __builtin_popcount(x_mask[t]);
+    gi.ptr = in_dev[t];
+    gi.out_mask = out_mask[t];
+    gi.pv = (uint32_t)ro;            // inserting a zero bit above every output bit: identity
+    gi.rank = (uint32_t)(ro + rx);
+    gi.full = out_mask[t] == full;
+    for (int x = 0; x < (1 << M); ++x) {
+      // held summed indices, x_0 most significant: x_i -> position ro + (number held above... )
+      uint64_t off = 0;
+      int pos = ro + rx - 1;
+      for (int i = 0; i < M; ++i) {
+        if (!((x_mask[t] >> i) & 1)) continue;
+        if ((x >> (M - 1 - i)) & 1) off += 1ull << pos;   // x's bit (M-1-i) is x_i (x_0 = MSB)
+        --pos;
+      }
+      gi.gx[x] = off;
+    }
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  bool ok;
+  if (dtype == TN_C64) {
+    ok = kernel == 1 ? try_launch_gemm<float2>(g, st)
+       : kernel == 2 ? try_launch_pair<float2>(g, st)
+       : kernel == 3 ? try_launch_group<float2>(g, st)
+       : (try_launch_gemm<float2>(g, st) || try_launch_pair<float2>(g, st) || try_launch_group<float2>(g, st));
+  } else {
+    ok = kernel == 1 ? try_launch_gemm<double2>(g, st)
+       : kernel == 2 ? try_launch_pair<double2>(g, st)
+       : kernel == 3 ? try_launch_group<double2>(g, st)
+       : (try_launch_pair<double2>(g, st) || try_launch_group<double2>(g, st));
+  }
+  if (!ok) return fail(TN_E_INVAL, "tn_eliminate_group: no kernel instantiation for this shape");
   CU(cudaGetLastError());
   return TN_OK;
 }

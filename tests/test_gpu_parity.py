@@ -120,6 +120,103 @@ def test_eliminate_specialised_vs_oracle(dtype, out_rank, kinds):
     assert np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30) < TOL[dtype] * 0.1
 
 
+# ------------------------------------------------------------------ fused groups (tn_eliminate_group)
+def _oracle_group(arrays, out_masks, x_masks, M, out_rank):
+    """The oracle's bucket elimination of x_0 .. x_{M-1} (labels 100 + i) over the caller tensors;
+    output bit b = label b.  Input positions: output bits low (ascending), held x_i on top with
+    x_0 the most significant; numpy axis 0 = the most significant position."""
+    ts = []
+    for a, m, xm in zip(arrays, out_masks, x_masks):
+        pos_labels = [b for b in range(out_rank) if (m >> b) & 1]
+        pos_labels += [100 + i for i in reversed(range(M)) if (xm >> i) & 1]
+        labs = tuple(reversed(pos_labels))
+        ts.append((a.reshape((2,) * len(labs)), labs))
+    rest, scalar = contract.partial_eliminate(ts, [100 + i for i in range(M)])
+    arr, labs = rest[0]
+    for a2, l2 in rest[1:]:          # inputs holding no summed index pass through: multiply in
+        arr, labs = contract._einsum_bucket([(arr, labs), (a2, l2), (np.full(2, 0.5), (999,))], 999)
+    arr = arr * scalar
+    want = tuple(reversed(range(out_rank)))
+    for l in want:
+        if l not in labs:
+            arr = np.stack([arr, arr], axis=-1)
+            labs = tuple(labs) + (l,)
+    arr = np.transpose(arr, [labs.index(l) for l in want])
+    return arr.reshape(-1)
+
+
+def _gemm_group(rng, out_rank, M, cls, xa=None, xb=None, cmask_hi=0, weights=True):
+    """A merge group as in a plan: A and B hold the output bits of classes a/c and b/c (cls[b] for
+    bit b), summed indices xa / xb (default: all); rank-1 weights on each x_i; optionally a constant
+    input holding high output bits `cmask_hi` and x_0."""
+    full_x = (1 << M) - 1
+    mA = sum(1 << b for b in range(out_rank) if cls[b] in "ac")
+    mB = sum(1 << b for b in range(out_rank) if cls[b] in "bc")
+    masks = [mA, mB]
+    xms = [full_x if xa is None else xa, full_x if xb is None else xb]
+    if weights:
+        for i in range(M):
+            masks.append(0)
+            xms.append(1 << i)
+    if cmask_hi:
+        masks.append(cmask_hi)
+        xms.append(1)
+    shapes = [bin(m).count("1") + bin(x).count("1") for m, x in zip(masks, xms)]
+    return masks, xms, shapes
+
+
+def _cls(rng, out_rank, low="abccc"):
+    c = list(low[::-1]) if low else []
+    while len(c) < out_rank:
+        c.append("abcc"[int(rng.integers(0, 4))])
+    if len(low) < 9:   # at least two a and two b bits above the lanes
+        for k, want in ((5, "a"), (6, "a"), (7, "b"), (8, "b")):
+            c[k] = want
+    return c
+
+
+GROUP_CASES = [
+    # (out_rank, M, low-bit classes (bit 4..0), xa, xb, cmask_hi)
+    (12, 1, "abccc", None, None, 0),
+    (14, 2, "ccbca", None, None, 0),
+    (16, 3, "abccc", None, None, 0),
+    (17, 3, "bbaac", 0b011, None, 0),       # A lacks x_2: chunk rows shared
+    (18, 4, "ccccb", None, 0b1010, 0),      # B lacks x_0, x_2
+    (17, 2, "aabbcbbbbb", None, None, 0),   # A's lowest bit (5, class c) outside the tile -> 8-byte copies
+    (15, 5, "cacab", None, None, 0),
+    (19, 3, "abccc", None, None, 1 << 18),  # tile-dependent constant factor
+    (20, 2, "caaab", None, None, 0),
+]
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3, 0])
+@pytest.mark.parametrize("case", range(len(GROUP_CASES)))
+def test_group_kernels_vs_oracle(case, kernel):
+    out_rank, M, low, xa, xb, chi = GROUP_CASES[case]
+    rng = np.random.default_rng(1000 + case)
+    cls = _cls(rng, out_rank, low)
+    masks, xms, shapes = _gemm_group(rng, out_rank, M, cls, xa, xb, chi)
+    for dtype in (T.TN_C64, T.TN_C128):
+        if kernel == 1 and dtype == T.TN_C128:
+            continue
+        arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+        dev = [torch.tensor(a, dtype=DT[dtype], device="cuda") for a in arrays]
+        out = torch.full((2 ** out_rank,), float("nan"), dtype=DT[dtype], device="cuda")
+        try:
+            B.tn_eliminate_group(dtype, M, [d.data_ptr() for d in dev], masks, xms, out.data_ptr(), out_rank,
+                                 kernel, torch.cuda.current_stream().cuda_stream)
+        except T.TnError:
+            # k_gemm stages all 2^M rows of a tile's chunks in shared memory: M >= 4 shapes whose
+            # chunks exceed the budget fall back to k_pair / k_group_t (kernel 0 never fails)
+            assert kernel in (2, 3) or (kernel == 1 and M >= 4), "k_gemm must take this GEMM-shaped group"
+            continue
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().astype(np.complex128)
+        ref = _oracle_group(arrays, masks, xms, M, out_rank)
+        assert np.all(np.isfinite(got)), "output element not written"
+        assert np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30) < TOL[dtype] * 0.1
+
+
 # ------------------------------------------------------------------ amplitudes, small/medium
 @pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
 @pytest.mark.parametrize("n,p,k,orderer", [(12, 1, 0, "min-fill"), (14, 2, 0, "min-degree"),
