@@ -60,6 +60,26 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def fp32_peak_tflops() -> float:
+    """FP32 FMA peak of the B200: 148 SMs x 128 FP32 lanes x 2 flops x the max SM clock."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:
+        mhz = 1965.0
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def load_traffic(kernel: str) -> dict:
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json, written by scripts/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel, {})
+    except Exception:
+        return {}
+
+
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -234,6 +254,7 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     plan.profile(False)
+    recs = plan.profile_records()
     prof = plan.profile_read()
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -267,21 +288,45 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = 1000.0 / float(te.item())
 
-    # ---- roofline of the dominant kernel (standalone bucket-step launches, k_bucket)
+    # ---- roofline of the dominant kernel family (by device time inside the timed region)
     peak, peak_src = load_peaks()
-    kb_ms = prof["ms"]
-    kb_bytes = prof["bytes"]
-    achieved = (kb_bytes / (kb_ms / 1e3)) / 1e9 if kb_ms > 0 else 0.0
+    fam = {}
+    for r in recs:
+        f = fam.setdefault(r["kernel"], {"ms": 0.0, "bytes": 0.0, "flops": 0.0, "launches": 0})
+        f["ms"] += r["ms"]
+        f["bytes"] += r["bytes"]
+        f["flops"] += r["flops"]
+        f["launches"] += 1
+    kb_ms = sum(f["ms"] for f in fam.values())
+    dom = max(fam, key=lambda k: fam[k]["ms"]) if fam else None
+    fp32_peak = fp32_peak_tflops()
+    roof = {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None, "traffic": None}
+    if dom is not None:
+        d = fam[dom]
+        achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        t_hbm = d["bytes"] / (peak * 1e9)
+        t_alu = d["flops"] / (fp32_peak * 1e12)
+        tr = load_traffic(dom)
+        roof = {"bound": "hbm" if t_hbm >= t_alu else "alu", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": tr.get("dram_bytes_per_launch"),
+                "kernel": dom, "launches": d["launches"],
+                "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
+                "avg_launch_ms": d["ms"] / d["launches"],
+                "kernel_share_of_step": (d["ms"] / args.steps) / ms_step if ms_step else None,
+                "flops_per_launch": d["flops"] / d["launches"],
+                "alu": {"achieved_tflops": d["flops"] / (d["ms"] / 1e3) / 1e12, "peak_tflops": fp32_peak,
+                        "frac": (d["flops"] / (d["ms"] / 1e3) / 1e12) / fp32_peak,
+                        "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md section 5)"},
+                "peak_source": peak_src,
+                "traffic_source": tr.get("source"),
+                "traffic_algorithmic_bytes_per_launch": tr.get("algorithmic_bytes_per_launch"),
+                "families": {k: {"ms_share_of_step": (v["ms"] / args.steps) / ms_step, "launches": v["launches"],
+                                 "GBps": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None}
+                             for k, v in sorted(fam.items(), key=lambda kv: -kv[1]["ms"])}}
+        if tr.get("dram_bytes_per_launch") is None:
+            roof["traffic"] = None
     gpu_launches = prof["all_launches"]
     algo_bytes_step = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
-    traffic, traffic_ratio = None, None
-    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path) and prof["launches"]:
-        try:
-            traffic_ratio = json.load(open(tr_path)).get("bytes_per_algorithmic_byte")
-            traffic = traffic_ratio * kb_bytes / prof["launches"]   # DRAM bytes per launch
-        except Exception:
-            traffic = None
 
     line = {
         "metric": METRIC,
@@ -311,13 +356,7 @@ def main():
             "algorithmic_GB_per_step": algo_bytes_step / 1e9,
             "step_GBps_algorithmic": algo_bytes_step / (ms_step / 1e3) / 1e9,
         },
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "traffic_per_algorithmic_byte": traffic_ratio,
-                     "algorithmic_bytes_per_launch": kb_bytes / prof["launches"] if prof["launches"] else None,
-                     "kernel": "k_bucket (standalone bucket steps)", "peak_source": peak_src,
-                     "kernel_share_of_step": (kb_ms / args.steps) / ms_step if ms_step else None,
-                     "launches": prof["launches"]},
+        "roofline": roof,
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "contractions/s",
                 "h2d_bytes_per_step": 2 * w.p * 8, "d2h_bytes_per_step": 16 * n},

@@ -207,12 +207,18 @@ tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms, d
                           uint64_t* all_launches);
 
 /* The per-launch records behind tn_profile_read (call it BEFORE tn_profile_read, which clears
- * them): one record per standalone launch (k_bucket / k_chain) with its plan step range, kind
- * (1 = k_bucket, 2 = k_chain, 3 = k_group), device milliseconds and algorithmic bytes.  out: host array of cap
- * records (may be NULL to query *n). */
+ * them): one record per standalone launch with its plan step range, op kind (1 = single bucket
+ * step, 2 = fused reduce chain, 3 = fused merge group, 4 = run of small steps in one CTA), the
+ * kernel that ran it (1 = k_bucket, 2 = k_chain, 3 = k_group_t, 4 = k_pair, 5 = k_gemm,
+ * 6 = k_chain_split, 7 = k_program), device milliseconds,
+ * algorithmic bytes (inputs read once + output written once) and flops (8 x 2^(out_rank + M): one
+ * complex multiply-add per output element and summed value).  out: host array of cap records
+ * (may be NULL to query *n). */
 typedef struct {
   int32_t step_begin, step_end, kind, out_rank;
   double ms, bytes;
+  int32_t kernel, pad;
+  double flops;
 } tn_prof_record_t;
 tn_status tn_profile_records(tn_plan* plan, tn_prof_record_t* out, int64_t cap, int64_t* n);
 

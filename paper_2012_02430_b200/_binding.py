@@ -70,7 +70,12 @@ class tn_step_info_t(C.Structure):
 
 class tn_prof_record_t(C.Structure):
     _fields_ = [("step_begin", C.c_int32), ("step_end", C.c_int32), ("kind", C.c_int32),
-                ("out_rank", C.c_int32), ("ms", C.c_double), ("bytes", C.c_double)]
+                ("out_rank", C.c_int32), ("ms", C.c_double), ("bytes", C.c_double),
+                ("kernel", C.c_int32), ("pad", C.c_int32), ("flops", C.c_double)]
+
+
+KERNEL_NAMES = {0: "?", 1: "k_bucket", 2: "k_chain", 3: "k_group_t", 4: "k_pair", 5: "k_gemm",
+                6: "k_chain_split", 7: "k_program"}
 
 
 _P = C.c_void_p
@@ -271,5 +276,6 @@ def tn_profile_records(h: int):
     _check(_lib.tn_profile_records(h, None, 0, C.byref(n)), "tn_profile_records")
     arr = (tn_prof_record_t * max(1, n.value))()
     _check(_lib.tn_profile_records(h, arr, n.value, C.byref(n)), "tn_profile_records")
-    return [{"step_begin": r.step_begin, "step_end": r.step_end, "kind": ("k_bucket", "k_chain", "k_group")[r.kind - 1],
-             "out_rank": r.out_rank, "ms": r.ms, "bytes": r.bytes} for r in arr[:n.value]]
+    return [{"step_begin": r.step_begin, "step_end": r.step_end, "kind": ("step", "chain", "group", "run")[r.kind - 1],
+             "kernel": KERNEL_NAMES.get(r.kernel, "?"), "out_rank": r.out_rank, "ms": r.ms, "bytes": r.bytes,
+             "flops": r.flops} for r in arr[:n.value]]

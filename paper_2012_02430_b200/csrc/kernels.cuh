@@ -426,7 +426,7 @@ struct GArgs {
 // 0), the remaining NDIR - NDV use two 8-byte loads (offsets p and p + F_t(1); F_t(1) = 0 when
 // they lack output bit 0, i.e. one value serves both elements)
 template <typename T, typename OffT, int NDIR, int NSTG, int M, int NDV>
-__global__ void __launch_bounds__(kBucketThreads, 4) k_group_t(const GArgs a) {
+__global__ void __launch_bounds__(kBucketThreads, (M >= 3 ? 2 : 4)) k_group_t(const GArgs a) {
   constexpr int VEC = VecT<T>::n;
   constexpr int TB = TileBits<T>::v;
   constexpr int STRIDE = kBucketThreads * VEC;
@@ -555,33 +555,44 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_group_t(const GArgs a) {
       if (o >= n_out) break;
       if constexpr (VEC == 2) {
         float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
+        // x-rows in batches of XB: every direct (global) load of a batch is issued before the math
+        // that consumes it, so up to NDIR x XB 16-byte loads per thread are in flight
+        constexpr int XB = NX < 8 ? NX : 8;
+#pragma unroll 1
+        for (int x0 = 0; x0 < NX; x0 += XB) {
+          float4 ld[NDIR > 0 ? NDIR : 1][XB];
 #pragma unroll
-        for (int x = 0; x < NX; ++x) {
+          for (int xb = 0; xb < XB; ++xb)
+#pragma unroll
+            for (int t = 0; t < NDIR; ++t) {
+              const float2* q = static_cast<const float2*>(a.in[t]) + (db[t] + kofs[t][kk] + (OffT)a.gx[t][x0 + xb]);
+              if (t < NDV) {
+                ld[t][xb] = a.stream[t] ? __ldcs(reinterpret_cast<const float4*>(q)) : __ldg(reinterpret_cast<const float4*>(q));
+              } else {
+                const float2 u0 = __ldg(q), u1 = __ldg(q + d1v[t]);
+                ld[t][xb] = make_float4(u0.x, u0.y, u1.x, u1.y);
+              }
+            }
+#pragma unroll
+          for (int xb = 0; xb < XB; ++xb) {
+          const int x = x0 + xb;
           float2 pa, pb;
 #pragma unroll
           for (int t = 0; t < NDIR; ++t) {
-            const float2* q = static_cast<const float2*>(a.in[t]) + (db[t] + kofs[t][kk] + (OffT)a.gx[t][x]);
-            float2 xa, xb;
-            if (t < NDV) {
-              const float4 u = __ldg(reinterpret_cast<const float4*>(q));
-              xa = make_float2(u.x, u.y);
-              xb = make_float2(u.z, u.w);
-            } else {
-              xa = __ldg(q);
-              xb = __ldg(q + d1v[t]);
-            }
-            if (t == 0) { pa = xa; pb = xb; } else { pa = cmul(pa, xa); pb = cmul(pb, xb); }
+            const float2 xa = make_float2(ld[t][xb].x, ld[t][xb].y), xb2 = make_float2(ld[t][xb].z, ld[t][xb].w);
+            if (t == 0) { pa = xa; pb = xb2; } else { pa = cmul(pa, xa); pb = cmul(pb, xb2); }
           }
 #pragma unroll
           for (int u = 0; u < NSTG; ++u) {
             const int t = NDIR + u;
             const float2* p = reinterpret_cast<const float2*>(sb + a.sx[t][x]) + (thr[t] + kofs[t][kk]);
-            const float2 xa = p[0], xb = p[s1v[u]];
-            if (NDIR == 0 && u == 0) { pa = xa; pb = xb; } else { pa = cmul(pa, xa); pb = cmul(pb, xb); }
+            const float2 xa = p[0], xb2 = p[s1v[u]];
+            if (NDIR == 0 && u == 0) { pa = xa; pb = xb2; } else { pa = cmul(pa, xa); pb = cmul(pb, xb2); }
           }
           const float2 c = reinterpret_cast<const float2&>(Cs[cb][x]);
           acc_a = cadd(acc_a, cmul(pa, c));
           acc_b = cadd(acc_b, cmul(pb, c));
+          }
         }
         __stcs(reinterpret_cast<float4*>(out + o), make_float4(acc_a.x, acc_a.y, acc_b.x, acc_b.y));
       } else {
@@ -813,8 +824,11 @@ struct MArgs {
   uint32_t posoff[2][kGemmMaxTB];      // element offset (within the input) of chunk bit k
   int8_t chbit[2][kGemmMaxTB];         // tile-local bit u -> chunk bit of A / B (-1: absent)
   uint8_t outbit[kGemmMaxTB];          // tile-local bit u -> output bit
-  uint32_t sm_in[2][2];                // dynamic smem element offset of buffer (input, buf)
-  uint32_t sm_dep[2];                  // dynamic smem uint32 offset of the chunk-piece offset table
+  uint32_t sm_in[2][4];                // dynamic smem element offset of ring slot (input, slot)
+  int32_t stages;                      // ring slots per input (2..4); lookahead = stages - 1 tiles
+  uint32_t sm_dep[2];                  // dynamic smem uint32 offset of the piece offset table (nrows << (nch - lv) entries)
+  uint32_t sm_bf_bytes;                // dynamic smem byte offset of the formatted B' chunk (2^M x 2^nch[1] float4)
+  int32_t c_tile_dep;                  // a constant input holds an output bit: C changes between tiles
   const void* cin[kMaxIn];             // constant inputs (no tile bit)
   uint64_t cmask[kMaxIn];
   uint32_t cpv[kMaxIn];
@@ -869,16 +883,18 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
     fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], mask_of(t), pv_of(t)) : 0u;
   }
   for (int b = tid; b < NB; b += kGemmThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
-  // chunk-piece offset tables: piece ip (2^lv elements) of a chunk row -> element offset
+  // piece offset tables: piece c (2^lv elements) of input u's chunk -> element offset from the
+  // tile's base offset (row part G_u(x) + in-row part), so a copy is one shared load + one add
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const uint32_t np = 1u << (a.nch[u] - a.lv[u]);
-    for (uint32_t ip = tid; ip < np; ip += kGemmThreads) {
-      const uint32_t ia = ip << a.lv[u];
-      uint32_t off = 0;
+    const uint32_t lp = a.nch[u] - a.lv[u];
+    const uint32_t np = a.nrows[u] << lp;
+    for (uint32_t c = tid; c < np; c += kGemmThreads) {
+      const uint32_t ia = (c & ((1u << lp) - 1u)) << a.lv[u];
+      uint32_t off = a.rowoff[u][c >> lp];
       for (uint32_t k = a.lv[u]; k < a.nch[u]; ++k)
         if ((ia >> k) & 1u) off += a.posoff[u][k];
-      smu[a.sm_dep[u] + ip] = off;
+      smu[a.sm_dep[u] + c] = off;
     }
   }
   __syncthreads();
@@ -936,50 +952,78 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
   __syncthreads();
 
   // cp.async of input u's chunk (all rows) at base offset `base` into buffer `buf`
-  auto prefetch = [&](int u, uint32_t base, int buf) {
+  auto prefetch = [&](int u, uint32_t base, int slot) {
     const float2* src = static_cast<const float2*>(a.in[u]) + base;
-    float2* dst = sm + a.sm_in[u][buf];
-    const uint32_t lp = a.nch[u] - a.lv[u];
-    const uint32_t np = a.nrows[u] << lp;
-    const uint32_t* dep = smu + a.sm_dep[u];
+    float2* dst = sm + a.sm_in[u][slot];
+    const uint32_t np = a.nrows[u] << (a.nch[u] - a.lv[u]);
+    const uint32_t* tab = smu + a.sm_dep[u];
     if (a.lv[u]) {
-      for (uint32_t c = tid; c < np; c += kGemmThreads) {
-        const uint32_t r = c >> lp, ip = c & ((1u << lp) - 1u);
-        cp_async16(dst + (c << 1), src + a.rowoff[u][r] + dep[ip]);
-      }
+      for (uint32_t c = tid; c < np; c += kGemmThreads) cp_async16(dst + (c << 1), src + tab[c]);
     } else {
-      for (uint32_t c = tid; c < np; c += kGemmThreads) {
-        const uint32_t r = c >> lp, ip = c & ((1u << lp) - 1u);
-        cp_async8(dst + c, src + a.rowoff[u][r] + dep[ip]);
-      }
+      for (uint32_t c = tid; c < np; c += kGemmThreads) cp_async8(dst + c, src + tab[c]);
     }
   };
-  int bA = 0, bB = 0;
-  if (t0 < t1) { prefetch(0, cur[0], 0); prefetch(1, cur[1], 0); }
+  // S-slot ring per input, lookahead D = S - 1 tiles.  An input's chunk version increments at
+  // every tile where its offset changes; version v lives in slot v % S.  At tile t the chunk of
+  // tile t + D is issued; the slot it overwrites held version <= ver(t) - 1 (finished).
+  const int S = a.stages, D = S - 1;
+  int ver[2] = {0, 0}, lver[2] = {0, 0};
+  int cslot[2] = {0, 0}, lslot[2] = {0, 0};   // ver % S and lver % S, kept incrementally
+  uint32_t lcur[2] = {cur[0], cur[1]};
+  uint64_t lt = t0;                     // the lookahead tile (last tile issued)
+  if (t0 < t1) { prefetch(0, lcur[0], 0); prefetch(1, lcur[1], 0); }
   cp_async_commit();
+  auto advance_lookahead = [&]() {      // issue the chunks of tile lt + 1 (if inside the range)
+    if (lt + 1 < t1) {
+      const int rr = __ffsll((long long)~lt) - 1;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (fbit[u][rr] != fcum[u][rr]) {
+          lcur[u] = lcur[u] + fbit[u][rr] - fcum[u][rr];
+          ++lver[u];
+          lslot[u] = lslot[u] + 1 == S ? 0 : lslot[u] + 1;
+          prefetch(u, lcur[u], lslot[u]);
+        }
+      }
+    }
+    ++lt;
+    cp_async_commit();
+  };
+  for (int d = 1; d < D; ++d) advance_lookahead();
+  float4* bf = reinterpret_cast<float4*>(dsm + a.sm_bf_bytes);   // C-scaled, pre-formatted B chunk
+  const uint32_t nB = 1u << a.nch[1];
 
+  int fixed_ver = -1;                   // version of B held (formatted) in bf
   for (uint64_t tile = t0; tile < t1; ++tile) {
     const int r = __ffsll((long long)~tile) - 1;
-    const bool has_next = tile + 1 < t1;
-    if (HASC && tid < (uint32_t)K) {
+    // B' is rebuilt only when B's chunk (or a tile-dependent constant factor) changes; the host
+    // orders the tile traversal so that consecutive tiles mostly share B
+    const bool refix = ver[1] != fixed_ver || a.c_tile_dep;
+    if (HASC && refix && tid < (uint32_t)K) {
       float2 c = make_float2(1.f, 0.f);
 #pragma unroll
       for (int t = 0; t < kMaxIn - 2; ++t)
         if (t < a.nc) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + curc[t] + a.cgx[t][tid]));
       Cs[tid] = c;
     }
-    bool chA = false, chB = false;
-    if (has_next) {
-      chA = fbit[0][r] != fcum[0][r];
-      chB = fbit[1][r] != fcum[1][r];
-      if (chA) prefetch(0, cur[0] + fbit[0][r] - fcum[0][r], bA ^ 1);
-      if (chB) prefetch(1, cur[1] + fbit[1][r] - fcum[1][r], bB ^ 1);
+    if (D <= 1) cp_async_wait<0>(); else if (D == 2) cp_async_wait<1>(); else cp_async_wait<2>();
+    __syncthreads();                    // chunks of this tile landed; every thread is past tile - 1
+    advance_lookahead();                // tile + D (its slot held a version <= this tile's - 1)
+    // B' [x][idx] = C[x] B[row(x)][idx], stored as (re, im, -im, re): a complex multiply-add is
+    // then two FFMA2 on operands read straight from shared memory (no register shuffles)
+    if (refix) {
+      const float2* sBraw = sm + a.sm_in[1][cslot[1]];
+      for (uint32_t e = tid; e < (uint32_t)K * nB; e += kGemmThreads) {
+        const uint32_t x = e >> a.nch[1], idx = e & (nB - 1u);
+        float2 b = sBraw[((uint32_t)a.row[1][x] << a.nch[1]) + idx];
+        if (HASC) b = cmul(b, Cs[x]);
+        bf[e] = make_float4(b.x, b.y, -b.y, b.x);
+      }
+      fixed_ver = ver[1];
+      __syncthreads();
     }
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const float2* sA = sm + a.sm_in[0][bA] + iathr;
-    const float2* sB = sm + a.sm_in[1][bB] + ibthr;
+    const float2* sA = sm + a.sm_in[0][cslot[0]] + iathr;
+    const float4* sB = bf + ibthr;
     uint64_t acc[RA][RB];
 #pragma unroll
     for (int i = 0; i < RA; ++i)
@@ -988,32 +1032,32 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
 #pragma unroll
     for (int x = 0; x < K; ++x) {
       const float2* pa = sA + ((uint32_t)a.row[0][x] << a.nch[0]);
-      const float2* pb = sB + ((uint32_t)a.row[1][x] << a.nch[1]);
-      float2 av[RA], bv[RB];
+      const float4* pb = sB + ((uint32_t)x << a.nch[1]);
+      float2 av[RA];
+      float4 bv[RB];
 #pragma unroll
       for (int i = 0; i < RA; ++i) av[i] = pa[iar[i]];
 #pragma unroll
       for (int j = 0; j < RB; ++j) bv[j] = pb[ibr[j]];
-      if (HASC) {
-        const float2 c = Cs[x];
-#pragma unroll
-        for (int j = 0; j < RB; ++j) bv[j] = cmul(bv[j], c);
-      }
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < RB; ++j) cmac2(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < RB; ++j) {
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].x, av[i].x)), "l"(f2_pack(bv[j].x, bv[j].y)));
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].y, av[i].y)), "l"(f2_pack(bv[j].z, bv[j].w)));
+        }
     }
     float2* ot = out + obase + othr;
 #pragma unroll
     for (int i = 0; i < RA; ++i)
 #pragma unroll
       for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(acc[i][j]));
-    __syncthreads();
-    if (chA) bA ^= 1;
-    if (chB) bB ^= 1;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) cur[u] = cur[u] + fbit[u][r] - fcum[u][r];
+    for (int u = 0; u < 2; ++u)
+      if (fbit[u][r] != fcum[u][r]) {
+        ++ver[u];
+        cslot[u] = cslot[u] + 1 == S ? 0 : cslot[u] + 1;
+      }
 #pragma unroll
     for (int t = 0; t < kMaxIn - 2; ++t)
       if (HASC && t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];

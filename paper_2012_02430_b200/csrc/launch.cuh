@@ -90,11 +90,27 @@ inline bool env_flag(const char* name) {
   const char* v = std::getenv(name);
   return v && v[0] == '1';
 }
+inline int gemm_stages() {   // TNB_GEMM_STAGES=2..4 (default 3)
+  static const int s = [] {
+    const char* v = std::getenv("TNB_GEMM_STAGES");
+    const int x = v ? std::atoi(v) : 3;
+    return x < 2 ? 2 : (x > 4 ? 4 : x);
+  }();
+  return s;
+}
 inline bool gemm_disabled() {
   static const bool off = env_flag("TNB_NO_GEMM");
   return off;
 }
 
+
+// which kernel the last launcher on this thread used (per-launch profile records)
+enum KernelId : int { KID_NONE = 0, KID_BUCKET = 1, KID_CHAIN = 2, KID_GROUP = 3, KID_PAIR = 4,
+                      KID_GEMM = 5, KID_CHAIN_SPLIT = 6, KID_PROGRAM = 7 };
+inline int& last_kernel() {
+  static thread_local int k = KID_NONE;
+  return k;
+}
 
 // entry points (explicitly instantiated for float2 and double2 in their translation units);
 // each returns false when the shape has no instantiation / does not qualify

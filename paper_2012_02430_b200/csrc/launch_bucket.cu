@@ -84,6 +84,7 @@ void launch_bucket_n(BigArgs a, cudaStream_t st) {
   const size_t smem = (size_t)a.stage_elems * sizeof(T) * 2;
   bool wide = false;   // any input with more than 32 bits -> 64-bit offsets
   for (int t = 0; t < a.n_in; ++t) wide |= (__builtin_popcountll(a.out_mask[t]) + 1 > 32);
+  last_kernel() = KID_BUCKET;
   if (wide) {
     allow_smem(k_bucket<T, NIN, uint64_t>, smem);
     k_bucket<T, NIN, uint64_t><<<grid, kBucketThreads, smem, st>>>(a);

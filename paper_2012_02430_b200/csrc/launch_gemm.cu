@@ -1,11 +1,17 @@
 // launch_gemm.cu: k_gemm (register-blocked batched complex GEMM groups, FFMA2) -- part of libtnb200.so (see launch.cuh)
 #include "launch.cuh"
 
+#include <cstdio>
+
 namespace tnb {
+
+// dynamic shared memory per CTA so that two CTAs (plus ~5 KB static each) fit the 228 KB of an SM
+constexpr size_t kGemmSmemBudget = 100 * 1024;
 
 template <int M, int RAB, int RBB>
 void launch_m(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
   allow_smem(k_gemm<M, RAB, RBB, true>, smem);
+  last_kernel() = KID_GEMM;
   k_gemm<M, RAB, RBB, true><<<grid, kGemmThreads, smem, st>>>(ma);
 }
 
@@ -37,12 +43,10 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
       if (ia < 0 || r > __builtin_popcountll(g.in[ia].out_mask)) { ib = ia; ia = t; }
       else if (ib < 0 || r > __builtin_popcountll(g.in[ib].out_mask)) ib = t;
     }
-    const GIn& A = g.in[ia];
-    const GIn& Bq = g.in[ib];
-    if (A.rank > 32 || Bq.rank > 32) return false;
+    if (g.in[ia].rank > 32 || g.in[ib].rank > 32) return false;
     const uint64_t full = (1ull << R) - 1;
-    const uint64_t ca = A.out_mask & ~Bq.out_mask, cb = Bq.out_mask & ~A.out_mask;
-    const uint64_t cc = A.out_mask & Bq.out_mask, cn = full & ~(A.out_mask | Bq.out_mask);
+    uint64_t ca = g.in[ia].out_mask & ~g.in[ib].out_mask, cb = g.in[ib].out_mask & ~g.in[ia].out_mask;
+    const uint64_t cc = g.in[ia].out_mask & g.in[ib].out_mask, cn = full & ~(g.in[ia].out_mask | g.in[ib].out_mask);
     if (cn & 31ull) return false;                       // lanes must be held by A or B
     int ra[2], rb[2], nra = 0, nrb = 0;
     for (int b = 5; b < R; ++b) {
@@ -60,6 +64,22 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
         if (!((used >> b) & 1) && ((cls >> b) & 1)) { wb[nw++] = b; used |= 1ull << b; }
       }
     if (nw < 3) return false;
+    // role of B (the operand formatted in shared memory, kept across consecutive tiles): the one
+    // whose chunk changes least often.  The tile is symmetric in the roles; the traversal flips
+    // A's exclusive non-tile bits first, so B stays for 2^(that count) tiles; ties -> B with fewer
+    // tile bits (smaller formatted chunk)
+    {
+      const int exa = __builtin_popcountll(ca & ~used), exb = __builtin_popcountll(cb & ~used);
+      const int ta = __builtin_popcountll(used & g.in[ia].out_mask), tb = __builtin_popcountll(used & g.in[ib].out_mask);
+      if (exb > exa || (exb == exa && ta < tb)) {
+        std::swap(ia, ib);
+        std::swap(ca, cb);
+        std::swap(ra, rb);
+        std::swap(nra, nrb);
+      }
+    }
+    const GIn& A = g.in[ia];
+    const GIn& Bq = g.in[ib];
     const int TB = 8 + nra + nrb;
     if (R < TB) return false;
     MArgs ma;
@@ -83,6 +103,8 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
       ++nc;
     }
     ma.nc = nc;
+    ma.c_tile_dep = 0;
+    for (int t = 0; t < nc; ++t) ma.c_tile_dep |= ma.cmask[t] != 0 ? 1 : 0;
     // chunks: tile bits held by each input, by ascending output bit (= ascending input position)
     uint32_t smem_elems = 0;
     uint32_t sz[2];
@@ -119,29 +141,46 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
       ma.pv[s] = in.pv;
       sz[s] = ma.nrows[s] << k;
     }
-    ma.sm_in[0][0] = 0;
-    ma.sm_in[0][1] = sz[0];
-    ma.sm_in[1][0] = 2 * sz[0];
-    ma.sm_in[1][1] = 2 * sz[0] + sz[1];
-    smem_elems = 2 * (sz[0] + sz[1]);
+    // ring slots: as many as fit the per-CTA budget (2 CTAs per SM), at most gemm_stages()
+    const uint32_t dep_u32 = (ma.nrows[0] << (ma.nch[0] - ma.lv[0])) + (ma.nrows[1] << (ma.nch[1] - ma.lv[1]));
+    const size_t bf_bytes = ((size_t)16 << g.M) << ma.nch[1];
+    int S = gemm_stages();
+    while (S > 2 && ((size_t)S * (sz[0] + sz[1]) * 8 + dep_u32 * 4 + bf_bytes + 16) > kGemmSmemBudget) --S;
+    ma.stages = S;
+    for (int k = 0; k < S; ++k) {
+      ma.sm_in[0][k] = k * sz[0];
+      ma.sm_in[1][k] = S * sz[0] + k * sz[1];
+    }
+    smem_elems = S * (sz[0] + sz[1]);
     uint32_t u32 = 2 * smem_elems;                       // uint32 units
     for (int s = 0; s < 2; ++s) {
       ma.sm_dep[s] = u32;
-      u32 += 1u << (ma.nch[s] - ma.lv[s]);
+      u32 += ma.nrows[s] << (ma.nch[s] - ma.lv[s]);
     }
-    const size_t smem = (size_t)u32 * 4;
-    if (smem > 110 * 1024) return false;
-    // traversal of the tile index: b-only bits first (A chunk unchanged), then a-only, then the rest
+    ma.sm_bf_bytes = (u32 * 4 + 15) / 16 * 16;
+    const size_t smem = ma.sm_bf_bytes + bf_bytes;
+    if (smem > kGemmSmemBudget) return false;
+    // traversal of the tile index: a-only bits first (B chunk and B' unchanged), then b-only, then
+    // the rest
     int np = 0;
     for (int pass = 0; pass < 3; ++pass)
       for (int b = 0; b < R; ++b) {
         if ((tmask >> b) & 1) continue;
-        const uint64_t cls = pass == 0 ? cb : pass == 1 ? ca : (cc | cn);
+        const uint64_t cls = pass == 0 ? ca : pass == 1 ? cb : (cc | cn);
         if ((cls >> b) & 1) ma.perm[np++] = (uint8_t)b;
       }
     if (np != R - TB) return false;
     ma.out = g.out;
     ma.out_rank = R;
+    if (env_flag("TNB_GEMM_DEBUG")) {
+      std::fprintf(stderr, "k_gemm R=%d M=%d TB=%d nra=%d nrb=%d nch=(%u,%u) lv=(%u,%u) rows=(%u,%u) S=%d smem=%zu nc=%d ctd=%d outbits=",
+                   R, g.M, TB, nra, nrb, ma.nch[0], ma.nch[1], ma.lv[0], ma.lv[1], ma.nrows[0], ma.nrows[1],
+                   ma.stages, smem, nc, ma.c_tile_dep);
+      for (int uu = 0; uu < TB; ++uu) std::fprintf(stderr, "%d%s", ma.outbit[uu], uu + 1 < TB ? "," : "");
+      std::fprintf(stderr, " perm=");
+      for (int b = 0; b < np && b < 8; ++b) std::fprintf(stderr, "%d,", ma.perm[b]);
+      std::fprintf(stderr, "\n");
+    }
     const uint64_t tiles = 1ull << (R - TB);
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 2);
     switch (g.M) {

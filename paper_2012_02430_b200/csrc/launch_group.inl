@@ -7,6 +7,7 @@ namespace tnb {
 template <typename T, typename OffT, int NDIR, int NSTG, int M, int NDV>
 void launch_g(const GArgs& ga, unsigned grid, size_t smem, cudaStream_t st) {
   allow_smem(k_group_t<T, OffT, NDIR, NSTG, M, NDV>, smem);
+  last_kernel() = KID_GROUP;
   k_group_t<T, OffT, NDIR, NSTG, M, NDV><<<grid, kBucketThreads, smem, st>>>(ga);
 }
 

@@ -7,6 +7,7 @@ namespace tnb {
 template <typename T, typename OffT, int M>
 void launch_p(const PArgs& pa, unsigned grid, size_t smem, cudaStream_t st) {
   allow_smem(k_pair<T, OffT, M>, smem);
+  last_kernel() = KID_PAIR;
   k_pair<T, OffT, M><<<grid, kBucketThreads, smem, st>>>(pa);
 }
 

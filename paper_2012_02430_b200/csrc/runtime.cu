@@ -48,7 +48,8 @@ struct DevTables {
 struct ProfRec {
   cudaEvent_t a, b;
   double bytes;
-  int32_t step_begin, step_end, kind, out_rank;
+  double flops;        // 8 x 2^(out_rank + M): one complex multiply-add per (output, summed value)
+  int32_t step_begin, step_end, kind, out_rank, kernel;
 };
 
 struct tn_plan {
@@ -504,6 +505,8 @@ struct ProfScope {
     pr.step_end = e;
     pr.kind = kind;
     pr.out_rank = out_rank;
+    pr.flops = kind == 4 ? 0.0 : 8.0 * std::ldexp(1.0, out_rank + (e - b));
+    last_kernel() = KID_NONE;
     cudaEventRecord(pr.a, st);
   }
   bool cancel = false;
@@ -515,6 +518,7 @@ struct ProfScope {
       return;
     }
     cudaEventRecord(pr.b, st);
+    pr.kernel = last_kernel();
     pl->prof.push_back(pr);
   }
 };
@@ -572,9 +576,11 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         const uint64_t nblk = (1ull << c.out_rank) / (32ull * VEC);
         const unsigned g2 = (unsigned)std::min<uint64_t>(nblk, (uint64_t)num_sms() * 8);
         k_chain_split<T><<<g2, kBucketThreads, 0, st>>>(c);
+        last_kernel() = KID_CHAIN_SPLIT;
       } else {
         const unsigned grid = (unsigned)std::min<uint64_t>(blocks, (uint64_t)num_sms() * 8);
         k_chain<T><<<grid, kBucketThreads, 0, st>>>(c);
+        last_kernel() = KID_CHAIN;
       }
     } else if (op.type == OP_GROUP) {
       // head step + (M-1) in-place reduce followers with rank-1 weights, summed in one pass
@@ -627,8 +633,16 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       if (!launched)   // no instantiation for this shape: run the steps one by one
         for (int si = op.begin; si < op.end; ++si) run_big<T>(pl, si, ws, j, st);
     } else {
+      double bytes = 0.0;
+      for (int si = op.begin; si < op.end; ++si) {
+        const StepRec& sk = pl->steps[si];
+        bytes += std::ldexp((double)sizeof(T), sk.out_rank);
+        for (int t = 0; t < sk.n_in; ++t) bytes += std::ldexp((double)sizeof(T), (int)sk.in[t].rank);
+      }
+      ProfScope ps(pl, st, bytes, op.begin, op.end, 4, pl->steps[op.end - 1].out_rank);
       k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
                                                   dt.scalars, nullptr, 0, 0, 0);
+      last_kernel() = KID_PROGRAM;
     }
     pl->all_launches++;
     if (debug_checks()) {
@@ -983,6 +997,9 @@ extern "C" tn_status tn_profile_records(tn_plan* plan, tn_prof_record_t* out, in
     out[i].out_rank = p.out_rank;
     out[i].ms = t;
     out[i].bytes = p.bytes;
+    out[i].kernel = p.kernel;
+    out[i].pad = 0;
+    out[i].flops = p.flops;
   }
   return TN_OK;
 }

@@ -1,0 +1,8 @@
+set -x; O=gpurun_out/${TAG:-r1e}; mkdir -p $O
+export PATH=/usr/local/cuda/bin:$PATH
+for S in 2 4; do TNB_GEMM_STAGES=$S timeout 600 python -m pytest tests/test_gpu_parity.py -k "group_kernels or fused" -x -q > $O/pytest_group_s$S.log 2>&1; echo "pytest group S=$S exit $?"; tail -2 $O/pytest_group_s$S.log; done
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 $O/pytest_gpu.log
+for S in 2 3 4; do TNB_GEMM_STAGES=$S timeout 600 python bench.py --no-cpu-baseline > $O/bench_s$S.log 2>&1; echo "bench S=$S exit $?"; python -c "import json;d=json.loads(open('$O/bench_s$S.log').read().strip().splitlines()[-1]);print(d['value'],d['e2e']['value'],d['roofline']['frac'])"; done
+timeout 600 python scripts/step_profile.py --out $O/steps.json > $O/steps.log 2>&1; echo "steps exit $?"; head -12 $O/steps.log
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_gemm<.int.3" -c 3 -o $O/prof_gemm3 python scripts/profile_c5a.py > $O/ncu_top.log 2>&1; echo "ncu top exit $?"; tail -3 $O/ncu_top.log
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_group_t<float2, unsigned int, .int.1, .int.1, .int.5" -c 1 -o $O/prof_group5 python scripts/profile_c5a.py > $O/ncu_g5.log 2>&1; echo "ncu g5 exit $?"; tail -3 $O/ncu_g5.log

@@ -3,6 +3,7 @@ once.  `--print-skip STEP` prints how many k_bucket launches precede the launch 
 STEP in the second call, for `ncu -k regex:k_bucket -s <skip> -c <n>`.  `--list` prints the
 standalone steps with their k_bucket ordinal and algorithmic bytes."""
 import argparse
+import json
 import os
 import sys
 
@@ -17,6 +18,7 @@ def main():
     ap.add_argument("--workload", default="C5a")
     ap.add_argument("--print-skip", type=int, default=None)
     ap.add_argument("--list", action="store_true")
+    ap.add_argument("--records", default=None, help="write the first call's per-launch records (JSON)")
     args = ap.parse_args()
     plan, g, ga, be, meta = bench.build_workload_plan(args.workload)
     steps = plan.steps()
@@ -40,9 +42,16 @@ def main():
 
     torch.cuda.set_device(0)
     partials = torch.zeros(2 * plan.n_slices, dtype=torch.float64, device="cuda")
+    plan.profile(True)                  # per-launch records of the first call (launch order)
     plan.contract_sliced(ga, be, 0, 1, partials, dtype=T.TN_C64)
+    torch.cuda.synchronize()
+    recs = plan.profile_records()
+    plan.profile(False)
+    plan.profile_read()
     plan.contract_sliced(ga, be, 1, 2, partials, dtype=T.TN_C64)
     torch.cuda.synchronize()
+    if args.records:
+        json.dump(recs, open(args.records, "w"), indent=1)
     print("ok", partials[:4].tolist())
 
 

@@ -38,8 +38,8 @@ def main():
         rows.append({**r, "n_in": s["n_in"], "in_rank": s["in_rank"], "GBps": r["bytes"] / r["ms"] / 1e6,
                      "share": r["ms"] / tot_ms})
     for x in rows[:20]:
-        print("%-8s steps %3d-%3d out %2d in %-16s %7.3f ms %6.0f GB/s share %.3f" % (
-            x["kind"], x["step_begin"], x["step_end"] - 1, x["out_rank"], x["in_rank"], x["ms"], x["GBps"], x["share"]))
+        print("%-13s %-5s steps %3d-%3d out %2d in %-16s %7.3f ms %6.0f GB/s share %.3f" % (
+            x["kernel"], x["kind"], x["step_begin"], x["step_end"] - 1, x["out_rank"], x["in_rank"], x["ms"], x["GBps"], x["share"]))
     print("total standalone ms per slice: %.2f, GB: %.1f" % (tot_ms, sum(r["bytes"] for r in recs) / 1e9))
     if args.out:
         json.dump({"workload": args.workload, "dtype": args.dtype, "records": rows}, open(args.out, "w"), indent=1)
