@@ -83,6 +83,35 @@ def bucket_eliminate(tensors: Sequence[Tensor], order: Sequence[int]) -> complex
     return scalar
 
 
+def contract_open(tensors: Sequence[Tensor], open_labels: Sequence[int], order: Sequence[int] | None = None,
+                  ) -> np.ndarray:
+    """Batch of amplitudes (§6): eliminate every label except `open_labels`
+    (bucket elimination along `order`, or the oracle's own min-degree order with the open labels
+    excluded) and multiply the remaining tensors -- which hold open labels only -- into one
+    tensor.  Returns the flat vector v[i], bit b of i = the value of open_labels[b]."""
+    opened = list(open_labels)
+    if order is None:
+        order, _ = greedy_min_degree(tensors, exclude=opened)
+    rest, scalar = partial_eliminate(tensors, order)
+    a = len(opened)
+    # rest tensors hold open labels only: one einsum over them (a library primitive), axes in
+    # the order opened[a-1] .. opened[0] so that the C-order flattening has bit b = opened[b]
+    local = {lab: i for i, lab in enumerate(opened)}
+    args = []
+    for arr, labs in rest:
+        if any(l not in local for l in labs):
+            raise ValueError("order misses live labels")
+        args.append(arr)
+        args.append([local[l] for l in labs])
+    args.append([local[l] for l in reversed(opened)])
+    if rest:
+        out = np.einsum(*args, optimize=False)
+    else:
+        out = np.ones((2,) * a, dtype=np.complex128)
+    # an open label held by no remaining tensor (cannot happen for a connected network)
+    return (np.asarray(out, dtype=np.complex128) * scalar).reshape(-1)
+
+
 def pairwise_sum(vals: Sequence[complex]) -> complex:
     """Fixed-order pairwise tree over the list index."""
     vals = list(vals)

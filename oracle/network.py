@@ -41,11 +41,16 @@ def fix_indices(tensors: Sequence[Tensor], fixed: Dict[int, int]) -> List[Tensor
 
 # ------------------------------------------------------------------ QAOA, fused gates
 def qaoa_amplitude_network(n: int, edges: Sequence[Tuple[int, int]], gammas, betas,
-                           out_bits: Sequence[int] | None = None) -> List[Tensor]:
+                           out_bits: Sequence[int] | None = None,
+                           open_qubits: Sequence[int] = ()) -> List[Tensor]:
     """Tensor expression of sigma = <out| U |0^N>, boundary fixed.
 
     U = prod_l [RX(2 beta_l)^{(x)N} prod_e ZZ(gamma_l)] H^{(x)N}  (Fig. 1 with the
     CNOT-Z-CNOT gadget fused into the diagonal ZZ(gamma); reading A1).
+
+    open_qubits: output wires w(q, p) = p*N + q left OPEN instead of fixed (PAPER.md:599-603,
+    §6 "if we decide to leave out some indices, the result will be a tensor indexed by those
+    indices"): the network then evaluates the batch of 2^a amplitudes <x_open 0_rest|U|0^N>.
     """
     p = len(gammas)
     assert len(betas) == p and p >= 1
@@ -68,8 +73,15 @@ def qaoa_amplitude_network(n: int, edges: Sequence[Tuple[int, int]], gammas, bet
             tens.append((m, (w(q, l), w(q, l - 1))))               # RX[out, in]
     out_bits = [0] * n if out_bits is None else list(out_bits)
     fixed = {inp(q): 0 for q in range(n)}
-    fixed.update({w(q, p): out_bits[q] for q in range(n)})
+    opened = set(open_qubits)
+    fixed.update({w(q, p): out_bits[q] for q in range(n) if q not in opened})
     return fix_indices(tens, fixed)
+
+
+def open_labels(n: int, p: int, open_qubits: Sequence[int]) -> List[int]:
+    """Labels of the open output wires, in ascending qubit order: bit b of a batch index is the
+    output bit of the b-th open qubit (ascending)."""
+    return [p * n + q for q in sorted(open_qubits)]
 
 
 def live_labels(tensors: Sequence[Tensor]) -> List[int]:

@@ -152,6 +152,39 @@ def test_norm_of_all_amplitudes():
     assert abs(tot - 1.0) < 1e-12
 
 
+# ------------------------------------------------------------------ amplitude batches (open indices)
+@pytest.mark.parametrize("n,p,seed,opened", [(10, 2, 3, (1, 4, 7)), (12, 1, 4, (0, 11)),
+                                             (8, 3, 5, (2, 3, 5, 6)), (14, 2, 6, (13,))])
+def test_amplitude_batch_vs_statevector(n, p, seed, opened):
+    """PAPER.md:599-603 (§6): leaving the output indices of `opened` open gives the batch
+    <x_open 0_rest|U|0^N>; bit b of the batch index = output bit of the b-th open qubit."""
+    g = random_regular_graph(n, 3, seed)
+    ga, be = qaoa_angles(p, seed + 7)
+    psi = sv.qaoa_state(n, g.edges, ga, be)
+    t = network.qaoa_amplitude_network(n, g.edges, ga, be, open_qubits=opened)
+    v = contract.contract_open(t, network.open_labels(n, p, opened))
+    assert v.shape == (1 << len(opened),)
+    qs = sorted(opened)
+    for i in range(1 << len(qs)):
+        bits = [0] * n
+        for b, q in enumerate(qs):
+            bits[q] = (i >> b) & 1
+        assert abs(v[i] - sv.amplitude(psi, bits)) < 1e-12
+    # entry 0 is the single amplitude (SURVEY §8 f1 pin)
+    assert abs(v[0] - contract.contract(network.qaoa_amplitude_network(n, g.edges, ga, be))) < 1e-12
+
+
+def test_amplitude_batch_all_qubits_norm():
+    # every output open: the whole state, sum |amp|^2 = 1 (SPEC.md:321-323)
+    n, p = 8, 2
+    g = random_regular_graph(n, 3, 21)
+    ga, be = qaoa_angles(p, 21)
+    opened = tuple(range(n))
+    v = contract.contract_open(network.qaoa_amplitude_network(n, g.edges, ga, be, open_qubits=opened),
+                               network.open_labels(n, p, opened))
+    assert abs(np.sum(np.abs(v) ** 2) - 1.0) < 1e-12
+
+
 # ------------------------------------------------------------------ closed forms, any N
 @pytest.mark.parametrize("n,p", [(16, 1), (40, 1), (60, 1), (24, 2), (30, 2), (12, 3)])
 def test_closed_forms_special_angles(n, p):
