@@ -65,7 +65,12 @@ typedef struct {
                              greedy run is always included, so the result is never worse */
   int32_t rg_tau_milli;   /* rgreedy: temperature tau x 1000 (0 -> tau = 0.5) */
   uint32_t rg_seed;       /* rgreedy: seed (runs are deterministic for a seed) */
-  int32_t reserved;       /* must be 0 */
+  int32_t n_open;         /* a: output wires left open (amplitude plans, §6): the
+                             result is the batch of 2^a amplitudes <x 0_rest|U|0^N>, bit b of the
+                             batch index x = output bit of the b-th open qubit (ascending).  The open
+                             indices form a clique in the line graph and are never eliminated or
+                             sliced.  0 <= a <= 20; 0 = single amplitude */
+  const int32_t* open_qubits; /* host int32[n_open]: distinct qubits in [0, n_qubits) (any order) */
 } tn_build_opts;
 
 typedef struct {
@@ -89,7 +94,7 @@ typedef struct {
   uint64_t big_launches_per_slice;    /* standalone bucket-kernel launches per slice */
   int32_t slices_batchable;  /* 1: every per-slice step runs in the interpreter, so slices run
                                 batched (one CTA per slice) when the workspace holds windows */
-  int32_t reserved_info;
+  int32_t n_open;            /* a: results are batches of 2^a amplitudes (tn_build_opts.n_open) */
 } tn_plan_info_t;
 
 /* ---------------------------------------------------------------- planning (host only) */
@@ -110,7 +115,8 @@ tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* out);
 
 /* The schedule as data (amplitude plans): host arrays sized by tn_plan_info:
  * prefix[slice_step] labels, sliced[k] labels (ascending: bit b of slice id j is the value of
- * sliced[b], reading A13), residual[n_labels - slice_step - k] labels, degrees[n_labels - k]
+ * sliced[b], reading A13), residual[n_labels - n_open - slice_step - k] labels,
+ * degrees[n_labels - n_open - k]
  * (N_{G_i}(v_i) of the executed steps).  Any pointer may be NULL. */
 tn_status tn_plan_schedule(const tn_plan* plan, int32_t* prefix, int32_t* sliced, int32_t* residual,
                            int32_t* degrees);
@@ -136,23 +142,30 @@ tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int64_t cap, i
 /* ---------------------------------------------------------------- contraction (device) */
 /* Unsliced amplitude (sliced plans: all 2^k slices summed locally).  gamma, beta: host double[p].
  * ws: device buffer of >= workspace_bytes[dtype] bytes (e.g. torch.empty).  stream: cudaStream_t
- * (NULL = legacy default stream).  out: host double[2] = {Re sigma, Im sigma}, 2^{-N/2} applied in
- * FP64 (reading A15).  Synchronous with respect to `stream` on return. */
+ * (NULL = legacy default stream).  out: host double[2 * 2^a] = {Re, Im} of batch entry x at
+ * out[2x], out[2x+1] (a = n_open; a = 0: the single amplitude sigma), 2^{-N/2} applied in FP64
+ * (reading A15).  Synchronous with respect to `stream` on return. */
 tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma, const double* beta,
                       int32_t p, void* ws, size_t ws_bytes, void* stream, double out[2]);
 
 /* Slices [begin, end) of a sliced plan, Eq. (1): runs the shared prefix once,
- * then every slice; writes the complex128 result of slice j into device double
- * partials_dev[2j], partials_dev[2j+1] (2^{-N/2} applied) and leaves other entries untouched.
+ * then every slice; writes the complex128 result of slice j, batch entry x (x < 2^a, a = n_open)
+ * into device double partials_dev[2(j 2^a + x)], partials_dev[2(j 2^a + x) + 1] (2^{-N/2}
+ * applied) and leaves other entries untouched.
  * Asynchronous on `stream`.  The caller zero-fills, all-reduces (torch.distributed / NCCL) and
- * sums with tn_sum_partials. */
+ * sums with tn_sum_partials.  When ws_bytes holds L >= 2 windows of per-slice tensors
+ * (tn_workspace_bytes(plan, dtype, L)), slice j of the range runs on lane (j - begin) mod L:
+ * lane 0 on `stream`, lane l >= 1 on a library-owned stream in window l, all forked from and
+ * joined back into `stream` (results identical to one lane).  Lanes = min(L, TNB_LANES
+ * environment variable, default 4; TNB_ONE_LANE=1 forces one). */
 tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, const double* gamma,
                              const double* beta, int32_t p, uint64_t begin, uint64_t end, void* ws,
                              size_t ws_bytes, void* stream, double* partials_dev);
 
-/* Fixed-order pairwise sum over j of partials_host[2j..2j+1], j < n_slices (host; bit-identical
- * for any partition of the slices across GPUs). out: host double[2]. */
-tn_status tn_sum_partials(const tn_plan* plan, const double* partials_host, double out[2]);
+/* Fixed-order pairwise sum over j of the per-slice results (host; bit-identical for any partition
+ * of the slices across GPUs), per batch entry x: partials_host as written by
+ * tn_contract_sliced (double[2 n_slices 2^a]); out: host double[2 * 2^a]. */
+tn_status tn_sum_partials(const tn_plan* plan, const double* partials_host, double* out);
 
 /* Energy plan: all E light-cone networks contracted in ONE batched launch.  zz: host double[E]
  * (Re <Z_u Z_v> per edge in the graph's edge order), zz_imag_max: host double (max |Im|, ~0),
@@ -172,7 +185,8 @@ tn_status tn_energy_batch(const tn_plan* plan, tn_dtype dtype, const double* gam
 /* Workspace bytes for `batch` windows: energy plans -- `batch` parameter sets (tn_energy_batch);
  * amplitude plans whose per-slice steps all run in the interpreter -- up to `batch` slices per
  * launch in tn_contract_sliced / tn_contract (slice batching; the library uses as
- * many windows as the given ws_bytes holds).  batch <= 1 gives workspace_bytes[dtype]. 0 on error. */
+ * many windows as the given ws_bytes holds); other amplitude plans -- two slice lanes when
+ * batch >= 2 (see tn_contract_sliced).  batch <= 1 gives workspace_bytes[dtype]. 0 on error. */
 size_t tn_workspace_bytes(const tn_plan* plan, tn_dtype dtype, uint64_t batch);
 
 /* One bucket step -- "elimination of vertex (index) v" (§4.2) -- on caller

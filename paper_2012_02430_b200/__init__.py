@@ -49,6 +49,11 @@ class Plan:
     def width(self) -> int:
         return int(self.info["width"])
 
+    @property
+    def batch(self) -> int:
+        """2^a amplitudes per result (a = open output indices; 1 for a single amplitude)."""
+        return 1 << int(self.info["n_open"])
+
     def schedule(self):
         """(prefix, sliced, residual, degrees) label lists (tn_plan_schedule)."""
         return B.tn_plan_schedule(self.handle)
@@ -63,11 +68,22 @@ class Plan:
     # slice batching: windows for up to this many bytes of per-slice tensors
     BATCH_WINDOW_BYTES = 4 << 30
 
+    # slice lanes (independent slices overlap on TNB_LANES streams, default 4) while the extra
+    # windows of per-slice tensors cost at most this many bytes in total
+    LANE_WINDOW_BYTES = 48 << 30
+
     def batch_windows(self, dtype: int) -> int:
-        """Slices run per launch when every per-slice step is an interpreter step."""
-        if not self.info["slices_batchable"] or self.n_slices <= 1:
+        """Windows of per-slice tensors in the default workspace: slices run per launch when every
+        per-slice step is an interpreter step (slice batching); otherwise two windows let
+        tn_contract_sliced run two slices concurrently (two slice lanes)."""
+        if self.n_slices <= 1:
             return 1
         one = B.tn_workspace_bytes(self.handle, dtype, 2) - B.tn_workspace_bytes(self.handle, dtype, 1)
+        if not self.info["slices_batchable"]:
+            import os
+            lanes = max(1, min(4, int(os.environ.get("TNB_LANES", "4"))))
+            lanes = 1 if os.environ.get("TNB_ONE_LANE") == "1" else lanes
+            return int(max(1, min(lanes, self.n_slices, self.LANE_WINDOW_BYTES // max(1, one))))
         return int(max(1, min(self.n_slices, self.BATCH_WINDOW_BYTES // max(1, one))))
 
     def workspace(self, dtype: int, device=None, batch: int = 0):
@@ -130,12 +146,13 @@ class Plan:
 
 def build_plan(graph, p: int, kind: str = "amplitude", orderer: str = "min-fill", n_sliced: int = 0,
                r: int = 0, max_width: int = 0, small_log2: int = -1, rg_q: int = 0, rg_tau: float = 0.0,
-               rg_seed: int = 0) -> Plan:
-    """Plan for a tn_inputs.Graph (or any object with .n and .edges)."""
+               rg_seed: int = 0, open_qubits=()) -> Plan:
+    """Plan for a tn_inputs.Graph (or any object with .n and .edges).  open_qubits: output wires
+    left open -- the plan then yields the batch of 2^a amplitudes (§6)."""
     k = TN_KIND_AMPLITUDE if kind == "amplitude" else TN_KIND_ENERGY
     buf = B.tn_plan_build(graph.n, graph.edges, p, kind=k, orderer=ORDERERS[orderer], n_sliced=n_sliced,
                           r=r, max_width=max_width, small_log2=small_log2, rg_q=rg_q, rg_tau=rg_tau,
-                          rg_seed=rg_seed)
+                          rg_seed=rg_seed, open_qubits=open_qubits)
     plan = Plan(buf)
     plan.orderer = orderer
     return plan

@@ -39,7 +39,8 @@ class TnError(RuntimeError):
 class tn_build_opts(C.Structure):
     _fields_ = [("kind", C.c_int32), ("orderer", C.c_int32), ("n_sliced", C.c_int32), ("r", C.c_int32),
                 ("max_width", C.c_int32), ("small_log2", C.c_int32), ("rg_q", C.c_int32),
-                ("rg_tau_milli", C.c_int32), ("rg_seed", C.c_uint32), ("reserved", C.c_int32)]
+                ("rg_tau_milli", C.c_int32), ("rg_seed", C.c_uint32), ("n_open", C.c_int32),
+                ("open_qubits", C.POINTER(C.c_int32))]
 
 
 class tn_plan_info_t(C.Structure):
@@ -51,7 +52,7 @@ class tn_plan_info_t(C.Structure):
                 ("workspace_bytes", C.c_size_t * 2), ("pred_bytes_per_slice", C.c_double * 2),
                 ("pred_bytes_prefix", C.c_double * 2), ("pred_bytes_big_per_slice", C.c_double * 2),
                 ("big_launches_per_slice", C.c_uint64), ("slices_batchable", C.c_int32),
-                ("reserved_info", C.c_int32)]
+                ("n_open", C.c_int32)]
 
     def as_dict(self):
         d = {}
@@ -134,13 +135,15 @@ def tn_version() -> int:
 def tn_plan_build(n_qubits: int, edges, p: int, kind: int = TN_KIND_AMPLITUDE,
                   orderer: int = TN_ORDER_MIN_FILL, n_sliced: int = 0, r: int = 0,
                   max_width: int = 0, small_log2: int = -1, rg_q: int = 0, rg_tau: float = 0.0,
-                  rg_seed: int = 0) -> bytes:
+                  rg_seed: int = 0, open_qubits=()) -> bytes:
     flat = []
     for e in edges:
         flat.extend((int(e[0]), int(e[1])))
     arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    oq = [int(q) for q in open_qubits]
+    oarr = (C.c_int32 * max(1, len(oq)))(*oq)
     opts = tn_build_opts(kind, orderer, n_sliced, r, max_width, small_log2, rg_q, int(round(rg_tau * 1000)),
-                         rg_seed, 0)
+                         rg_seed, len(oq), C.cast(oarr, C.POINTER(C.c_int32)))
     buf, ln = _P(), C.c_size_t()
     _check(_lib.tn_plan_build(n_qubits, len(flat) // 2, arr, p, C.byref(opts), C.byref(buf), C.byref(ln)),
            "tn_plan_build")
@@ -168,7 +171,7 @@ def tn_plan_info(h: int) -> dict:
 
 def tn_plan_schedule(h: int):
     info = tn_plan_info(h)
-    s, k, L = info["slice_step"], info["k"], info["n_labels"]
+    s, k, L = info["slice_step"], info["k"], info["n_labels"] - info["n_open"]
     pre = (C.c_int32 * max(1, s))()
     sl = (C.c_int32 * max(1, k))()
     res = (C.c_int32 * max(1, L - s - k))()
@@ -194,11 +197,18 @@ def tn_plan_steps(h: int):
     return out
 
 
-def tn_contract(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, stream: int) -> complex:
-    out = (C.c_double * 2)()
+def _unpack(out, A: int):
+    vals = [complex(out[2 * x], out[2 * x + 1]) for x in range(A)]
+    return vals[0] if A == 1 else vals
+
+
+def tn_contract(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, stream: int):
+    """sigma (complex) for a single-amplitude plan; the list of 2^a batch entries when n_open = a > 0."""
+    A = 1 << tn_plan_info(h)["n_open"]
+    out = (C.c_double * (2 * A))()
     _check(_lib.tn_contract(h, dtype, _dbl(gammas), _dbl(betas), len(gammas), ws_ptr, ws_bytes,
                             stream, out), "tn_contract")
-    return complex(out[0], out[1])
+    return _unpack(out, A)
 
 
 def tn_contract_sliced(h: int, dtype: int, gammas, betas, begin: int, end: int, ws_ptr: int,
@@ -207,12 +217,14 @@ def tn_contract_sliced(h: int, dtype: int, gammas, betas, begin: int, end: int, 
                                    ws_ptr, ws_bytes, stream, partials_ptr), "tn_contract_sliced")
 
 
-def tn_sum_partials(h: int, partials) -> complex:
-    """partials: flat float64 sequence [re0, im0, re1, im1, ...] (host)."""
+def tn_sum_partials(h: int, partials):
+    """partials: flat float64 sequence [re, im] per (slice j, batch entry x) at 2 (j 2^a + x)
+    (host).  Returns a complex (a = 0) or the list of 2^a batch entries."""
+    A = 1 << tn_plan_info(h)["n_open"]
     arr = _dbl(list(partials))
-    out = (C.c_double * 2)()
+    out = (C.c_double * (2 * A))()
     _check(_lib.tn_sum_partials(h, arr, out), "tn_sum_partials")
-    return complex(out[0], out[1])
+    return _unpack(out, A)
 
 
 def tn_energy(h: int, dtype: int, gammas, betas, ws_ptr: int, ws_bytes: int, stream: int):

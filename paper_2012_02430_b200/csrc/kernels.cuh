@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(kProgramThreads) k_program(const StepRec* __re
                                                              double2* results, int mode,
                                                              uint64_t win0, uint64_t win_elems) {
   int b = begin, e = end;
-  uint64_t rel = 0, jj = j;
+  uint64_t rel = mode == 0 ? win0 : 0ull, jj = j;   // mode 0: win0 = slice-window offset
   const ProgramRec* pr = nullptr;
   if (mode == 1) {
     pr = &progs[blockIdx.x];
@@ -1265,36 +1265,52 @@ __global__ void __launch_bounds__(kProgramThreads) k_program(const StepRec* __re
   }
 }
 
+// per slice: the product of the final factors in FP64 x 2^{log2_scale}; with open indices (§6)
+// thread o computes batch entry o (element pext(o, open_mask) of every factor)
 template <typename T>
 __global__ void k_finalize(const ScalarRec* __restrict__ scal, int b, int e, const T* ws,
-                           uint64_t j, double log2_scale, double* __restrict__ dst) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    const double2 v = final_product<T>(scal, b, e, ws, j, log2_scale, 0ull);
-    dst[0] = v.x;
-    dst[1] = v.y;
+                           uint64_t j, double log2_scale, double* __restrict__ dst, uint64_t rel,
+                           int n_open) {
+  const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= (1u << n_open)) return;
+  double re = 1.0, im = 0.0;
+  for (int i = b; i < e; ++i) {
+    const ScalarRec& r = scal[i];
+    const uint64_t off = r.off + ((r.flags & F_REL) ? rel : 0ull) +
+                         (r.slice_mask ? (pext_bits(j, r.slice_mask) << __popc(r.open_mask)) : 0ull) +
+                         pext_bits(o, r.open_mask);
+    const double2 v = to_d2(ws[off]);
+    const double nr = re * v.x - im * v.y, ni = re * v.y + im * v.x;
+    re = nr;
+    im = ni;
   }
+  const double sc = exp2(log2_scale);
+  dst[2 * o] = re * sc;
+  dst[2 * o + 1] = im * sc;
 }
 
-// fixed pairwise tree over j (identical to the host tn_sum_partials)
-static __global__ void k_pairwise(double* __restrict__ buf, uint64_t n, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (n == 0) { out[0] = out[1] = 0.0; return; }
+// fixed pairwise tree over j (identical to the host tn_sum_partials); buf[2 (j A + o)], one
+// thread per batch entry o
+static __global__ void k_pairwise(double* __restrict__ buf, uint64_t n, uint64_t A, double* __restrict__ out) {
+  const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= A) return;
+  if (n == 0) { out[2 * o] = out[2 * o + 1] = 0.0; return; }
   uint64_t m = n;
   while (m > 1) {
     uint64_t h = 0;
     for (uint64_t i = 0; i + 1 < m; i += 2, ++h) {
-      buf[2 * h] = buf[2 * i] + buf[2 * (i + 1)];
-      buf[2 * h + 1] = buf[2 * i + 1] + buf[2 * (i + 1) + 1];
+      buf[2 * (h * A + o)] = buf[2 * (i * A + o)] + buf[2 * ((i + 1) * A + o)];
+      buf[2 * (h * A + o) + 1] = buf[2 * (i * A + o) + 1] + buf[2 * ((i + 1) * A + o) + 1];
     }
     if (m & 1) {
-      buf[2 * h] = buf[2 * (m - 1)];
-      buf[2 * h + 1] = buf[2 * (m - 1) + 1];
+      buf[2 * (h * A + o)] = buf[2 * ((m - 1) * A + o)];
+      buf[2 * (h * A + o) + 1] = buf[2 * ((m - 1) * A + o) + 1];
       ++h;
     }
     m = h;
   }
-  out[0] = buf[0];
-  out[1] = buf[1];
+  out[2 * o] = buf[2 * o];
+  out[2 * o + 1] = buf[2 * o + 1];
 }
 
 }  // namespace tnb

@@ -98,6 +98,16 @@ inline int gemm_stages() {   // TNB_GEMM_STAGES=2..4 (default 3)
   }();
   return s;
 }
+constexpr int kMaxLanes = 4;
+inline int slice_lanes() {   // TNB_LANES=1..4 (default 4); TNB_ONE_LANE=1 == TNB_LANES=1
+  static const int n = [] {
+    if (env_flag("TNB_ONE_LANE")) return 1;
+    const char* v = std::getenv("TNB_LANES");
+    const int x = v ? std::atoi(v) : 4;
+    return x < 1 ? 1 : (x > kMaxLanes ? kMaxLanes : x);
+  }();
+  return n;
+}
 inline bool gemm_disabled() {
   static const bool off = env_flag("TNB_NO_GEMM");
   return off;

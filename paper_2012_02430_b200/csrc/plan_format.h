@@ -18,7 +18,7 @@
 namespace tnb {
 
 constexpr uint32_t kPlanMagic = 0x32424E54u;  // "TNB2"
-constexpr uint32_t kPlanVersion = 6;
+constexpr uint32_t kPlanVersion = 7;
 constexpr int kMaxIn = 8;     // inputs per bucket step
 constexpr int kMaxP = 16;     // QAOA depth supported by the materializer
 constexpr int kMaxFactors = 4;
@@ -83,12 +83,12 @@ struct OpRec {
   int32_t phase;
 };
 
-struct ScalarRec {       // per-slice final factors: rank-0 tensors and tensors of sliced indices only
-  uint64_t off;
-  uint32_t slice_mask;
+struct ScalarRec {       // per-slice final factors: tensors holding no eliminated index -- rank 0,
+  uint64_t off;          // or only sliced and open indices.  Element of batch entry o in slice j:
+  uint32_t slice_mask;   //   off + (pext(j, slice_mask) << popcount(open_mask)) + pext(o, open_mask)
   int32_t program;
   uint32_t flags;        // F_REL: produced per slice
-  uint32_t pad;
+  uint32_t open_mask;    // open indices held (bit b = the b-th open index, §6 amplitude batch)
 };
 
 struct ProgramRec {      // amplitude: one program; energy: one per edge (light cone)
@@ -115,7 +115,9 @@ struct PlanHeader {
   double pred_elems_big_slice; // part of pred_elems_slice in OP_BIG launches
   uint64_t big_launches_slice;
   uint64_t launches_prefix, launches_slice;
-  uint64_t reserved[4];
+  int32_t n_open;              // open output indices a: every result is a batch of 2^a amplitudes
+  int32_t pad0;
+  uint64_t reserved[3];
 };
 // Buffer = PlanHeader | ProgramRec[n_programs] | LeafRec[n_leaves] | StepRec[n_steps]
 //          | OpRec[n_ops] | ScalarRec[n_scalars] | int32 prefix[n_prefix] | int32 sliced[k]

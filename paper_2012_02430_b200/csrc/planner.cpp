@@ -58,8 +58,16 @@ void check_edges(int n, const std::vector<int>& edges) {
 
 }  // namespace
 
-Network build_amplitude_network(int n, const std::vector<int>& edges, int p) {
+Network build_amplitude_network(int n, const std::vector<int>& edges, int p,
+                                const std::vector<int>& open_qubits) {
   check_edges(n, edges);
+  std::vector<int> opened(open_qubits);
+  std::sort(opened.begin(), opened.end());
+  if (std::adjacent_find(opened.begin(), opened.end()) != opened.end() ||
+      (!opened.empty() && (opened.front() < 0 || opened.back() >= n)))
+    throw std::invalid_argument("bad open qubit list");
+  std::vector<int> open_rank(n, -1);
+  for (size_t b = 0; b < opened.size(); ++b) open_rank[opened[b]] = (int)b;
   NetBuilder b;
   auto w = [n](int q, int l) { return l * n + q; };
   for (int q = 0; q < n; ++q) b.add({w(q, 0)}, {LC_PLUS, 0, 0});
@@ -69,11 +77,14 @@ Network build_amplitude_network(int n, const std::vector<int>& edges, int p) {
     for (int q = 0; q < n; ++q) {
       if (l < p)
         b.add({w(q, l - 1), w(q, l)}, {LC_RX, (uint8_t)(l - 1), 0});
+      else if (open_rank[q] >= 0)  // open output wire (§6): e^{-i b X} between w(q, p-1) and it
+        b.add({w(q, p - 1), n * p + open_rank[q]}, {LC_RX, (uint8_t)(l - 1), 0});
       else  // output wire fixed to 0: <0| e^{-i b X} is a vector on w(q, p-1)
         b.add({w(q, p - 1)}, {LC_RXROW0, (uint8_t)(l - 1), 0});
     }
   }
-  b.net.n_labels = n * p;
+  b.net.n_labels = n * p + (int)opened.size();
+  for (size_t k = 0; k < opened.size(); ++k) b.net.open_labels.push_back(n * p + (int)k);
   b.net.log2_scale = -0.5 * b.n_plus;
   return b.net;
 }
@@ -153,7 +164,21 @@ BitGraph BitGraph::from_network(const Network& net) {
   for (const auto& t : net.tensors)
     for (size_t i = 0; i < t.labels.size(); ++i)
       for (size_t j = i + 1; j < t.labels.size(); ++j) g.add_edge(t.labels[i], t.labels[j]);
+  // the batch result is a tensor over the open indices: "a clique on left-out indices"
+  // (PAPER.md:603-605), and they are never eliminated
+  const auto& o = net.open_labels;
+  for (size_t i = 0; i < o.size(); ++i)
+    for (size_t j = i + 1; j < o.size(); ++j) g.add_edge(o[i], o[j]);
+  for (int v : o) g.keep(v);
   return g;
+}
+
+void BitGraph::keep(int v) {
+  if (keep_.empty()) keep_.assign(n_, 0);
+  if (!keep_[v]) {
+    keep_[v] = 1;
+    n_kept_++;
+  }
 }
 
 void BitGraph::add_edge(int a, int b) {
@@ -232,10 +257,10 @@ Ordering greedy_order(BitGraph g, int orderer) {
     for (int v = 0; v < n; ++v)
       if (g.alive(v)) fill[v] = g.fill_in(v);
   std::vector<char> dirty(n, 0);
-  while (g.n_alive() > 0) {
+  while (g.n_free() > 0) {
     int best = -1;
     for (int v = 0; v < n; ++v) {
-      if (!g.alive(v)) continue;
+      if (!g.alive(v) || g.kept(v)) continue;
       if (best < 0) { best = v; continue; }
       if (minfill) {
         if (fill[v] < fill[best] || (fill[v] == fill[best] && g.degree(v) < g.degree(best))) best = v;
@@ -292,23 +317,23 @@ Ordering boltzmann_run(BitGraph g, bool by_fill, double tau, uint64_t seed) {
   Ordering o;
   Rng rng{seed};
   std::vector<double> w(n);
-  while (g.n_alive() > 0) {
+  while (g.n_free() > 0) {
     int64_t kmin = INT64_MAX;
     std::vector<int64_t> key(n, 0);
     for (int v = 0; v < n; ++v) {
-      if (!g.alive(v)) continue;
+      if (!g.alive(v) || g.kept(v)) continue;
       key[v] = by_fill ? g.fill_in(v) : g.degree(v);
       kmin = std::min(kmin, key[v]);
     }
     double tot = 0.0;
     for (int v = 0; v < n; ++v) {
-      w[v] = g.alive(v) ? std::exp(-(double)(key[v] - kmin) / tau) : 0.0;
+      w[v] = (g.alive(v) && !g.kept(v)) ? std::exp(-(double)(key[v] - kmin) / tau) : 0.0;
       tot += w[v];
     }
     double u = rng.uniform() * tot;
     int pick = -1;
     for (int v = 0; v < n; ++v) {
-      if (!g.alive(v)) continue;
+      if (!g.alive(v) || g.kept(v)) continue;
       pick = v;
       u -= w[v];
       if (u <= 0.0) break;
@@ -348,7 +373,7 @@ Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec) {
     return sch;
   }
   if (r <= 0 || r > n) r = n;
-  if (n > g0.n_alive()) throw std::invalid_argument("n exceeds the live vertex count");
+  if (n > g0.n_free()) throw std::invalid_argument("n exceeds the live vertex count");
   BitGraph g = g0;
   int prefix_width = 0;
   double prefix_cost = 0.0;
@@ -375,11 +400,12 @@ Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec) {
         pcost += std::ldexp(1.0, full.degrees[s - 1]) * std::ldexp(1.0, n_done);
         gs.eliminate(full.order[s - 1]);
       }
-      if (gs.n_alive() < rr) break;
-      // the rr vertices with the most neighbours in G_s, ties -> smaller label (reading A9)
+      if (gs.n_free() < rr) break;
+      // the rr vertices with the most neighbours in G_s, ties -> smaller label (reading A9);
+      // open (kept) indices are never sliced
       std::vector<int> cand;
       for (int v = 0; v < gs.size(); ++v)
-        if (gs.alive(v)) cand.push_back(v);
+        if (gs.alive(v) && !gs.kept(v)) cand.push_back(v);
       std::stable_sort(cand.begin(), cand.end(),
                        [&](int a, int b) { return gs.degree(a) > gs.degree(b); });
       std::vector<int> S(cand.begin(), cand.begin() + rr);
@@ -497,12 +523,26 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   const int sA = (int)sch.prefix.size();
   for (int i = 0; i < sA; ++i) key[sch.prefix[i]] = i;
   for (size_t i = 0; i < sch.residual.size(); ++i) key[sch.residual[i]] = sA + (int64_t)i;
+  const int total_pos = sA + (int)sch.residual.size();
+  // open indices (§6): after every eliminated position; the b-th open label is bit b of every
+  // tensor holding open labels (b = 0 least significant), so a final tensor's element for batch
+  // index o is pext(o, its open mask)
+  const int n_open = (int)net.open_labels.size();
+  std::vector<int> open_bit(NL, -1);
+  for (int b = 0; b < n_open; ++b) {
+    const int l = net.open_labels[b];
+    if (key[l] != INT64_MIN) {
+      *err = "an open index is in the elimination order";
+      return out;
+    }
+    key[l] = total_pos + (n_open - 1 - b);
+    open_bit[l] = b;
+  }
   for (int l = 0; l < NL; ++l)
     if (key[l] == INT64_MIN) {
       *err = "order misses live label " + std::to_string(l);
       return out;
     }
-  const int total_pos = sA + (int)sch.residual.size();
   auto by_key = [&](int a, int b) { return key[a] < key[b]; };
 
   std::vector<Sym> syms;
@@ -513,9 +553,9 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     s.leaf = (int)t;
     syms.push_back(s);
   }
-  auto home = [&](const Sym& s) -> int64_t {  // min key over non-sliced indices, -1 if none
-    for (int l : s.idx)
-      if (slice_bit[l] < 0) return key[l];
+  auto home = [&](const Sym& s) -> int64_t {  // min key over eliminated (non-sliced, non-open)
+    for (int l : s.idx)                        // indices; -1 if none (a final factor)
+      if (slice_bit[l] < 0) return key[l] < total_pos ? key[l] : -1;
     return -1;
   };
   std::vector<std::vector<int>> bucket(total_pos);
@@ -711,9 +751,13 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     ScalarRec sr;
     std::memset(&sr, 0, sizeof(sr));
     sr.off = syms[id].off;
-    uint32_t m = 0;
-    for (int l : syms[id].idx) m |= 1u << slice_bit[l];
+    uint32_t m = 0, om = 0;
+    for (int l : syms[id].idx) {
+      if (slice_bit[l] >= 0) m |= 1u << slice_bit[l];
+      else if (open_bit[l] >= 0) om |= 1u << open_bit[l];
+    }
     sr.slice_mask = m;
+    sr.open_mask = om;
     sr.flags = syms[id].phaseB_born ? F_REL : 0u;
     out.scalars.push_back(sr);
   }

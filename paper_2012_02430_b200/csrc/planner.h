@@ -24,11 +24,16 @@ struct Network {
   std::vector<NetTensor> tensors;
   double log2_scale = 0.0;       // -(#|+> factors)/2
   int edge_u = -1, edge_v = -1;
+  std::vector<int> open_labels;  // never-eliminated output indices (§6 amplitude batch); bit b of
+                                 // a batch index <-> open_labels[b] (ascending qubit)
 };
 
 // PAPER.md:199-235 (§4.1) + Fig. 1 with the CNOT-Z-CNOT gadget fused into a
 // diagonal ZZ(gamma): live indices w(q,l) = l*N + q, l = 0..p-1 (reading A6).
-Network build_amplitude_network(int n, const std::vector<int>& edges, int p);
+// open_qubits: output wires left open (§6): the network evaluates the batch
+// <x_open 0_rest|U|0^N>; open wire of the b-th open qubit (ascending) -> label n*p + b.
+Network build_amplitude_network(int n, const std::vector<int>& edges, int p,
+                                const std::vector<int>& open_qubits = {});
 // <psi|Z_u Z_v|psi> restricted to the reverse light cone of edge (u, v).
 Network build_cone_network(int n, const std::vector<int>& edges, int p, int u, int v);
 
@@ -42,6 +47,11 @@ class BitGraph {
   bool alive(int v) const { return alive_[v] != 0; }
   int degree(int v) const { return deg_[v]; }
   int n_alive() const { return n_alive_; }
+  // kept vertices (open indices, §6) are never eliminated, sliced or chosen by an orderer
+  bool kept(int v) const { return !keep_.empty() && keep_[v] != 0; }
+  void keep(int v);
+  int n_kept() const { return n_kept_; }
+  int n_free() const { return n_alive_ - n_kept_; }   // vertices an orderer may still eliminate
   void add_edge(int a, int b);
   // elimination of vertex v: remove it and make its neighbourhood a clique
   void eliminate(int v);
@@ -55,9 +65,9 @@ class BitGraph {
 
  private:
   uint64_t* rowm(int v) { return &adj_[(size_t)v * W_]; }
-  int n_ = 0, W_ = 0, n_alive_ = 0;
+  int n_ = 0, W_ = 0, n_alive_ = 0, n_kept_ = 0;
   std::vector<uint64_t> adj_;
-  std::vector<uint8_t> alive_;
+  std::vector<uint8_t> alive_, keep_;
   std::vector<int> deg_;
 };
 

@@ -43,6 +43,8 @@ struct DevTables {
   LeafRec* leaves = nullptr;
   ScalarRec* scalars = nullptr;
   ProgramRec* progs = nullptr;
+  cudaStream_t side[kMaxLanes - 1] = {};   // slice lanes 1.. (tn_contract_sliced, one window each)
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes - 1] = {};
 };
 
 struct ProfRec {
@@ -74,6 +76,11 @@ struct tn_plan {
       cudaFree(kv.second.leaves);
       cudaFree(kv.second.scalars);
       cudaFree(kv.second.progs);
+      for (int l = 0; l < kMaxLanes - 1; ++l) {
+        if (kv.second.side[l]) cudaStreamDestroy(kv.second.side[l]);
+        if (kv.second.ev_join[l]) cudaEventDestroy(kv.second.ev_join[l]);
+      }
+      if (kv.second.ev_fork) cudaEventDestroy(kv.second.ev_fork);
     }
     for (auto& p : prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -105,8 +112,8 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 size_t ws_bytes_for(const PlanHeader& h, int dtype) {
   const size_t es = dtype == TN_C64 ? 8 : 16;
   const uint64_t nsl = 1ull << h.k;
-  const uint64_t nres = std::max<uint64_t>(nsl, (uint64_t)h.n_programs);
-  return align256(h.arena_elems * es) + align256(16 * nres) + 256;
+  const uint64_t nres = std::max<uint64_t>(nsl, (uint64_t)h.n_programs) << h.n_open;
+  return align256(h.arena_elems * es) + align256(16 * nres) + align256(16ull << h.n_open);
 }
 
 }  // namespace
@@ -136,8 +143,14 @@ extern "C" tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int3
   try {
     std::vector<int> ev(edges, edges + 2 * (size_t)n_edges);
     std::vector<Network> nets;
+    std::vector<int> opened;
+    if (opts->n_open < 0 || opts->n_open > 20 || (opts->n_open > 0 && !opts->open_qubits))
+      return fail(TN_E_INVAL, "tn_plan_build: n_open must be in [0, 20] with open_qubits given");
+    if (opts->n_open > 0 && opts->kind != TN_KIND_AMPLITUDE)
+      return fail(TN_E_INVAL, "tn_plan_build: open qubits need an amplitude plan");
+    for (int i = 0; i < opts->n_open; ++i) opened.push_back(opts->open_qubits[i]);
     if (opts->kind == TN_KIND_AMPLITUDE) {
-      nets.push_back(build_amplitude_network(n_qubits, ev, p));
+      nets.push_back(build_amplitude_network(n_qubits, ev, p, opened));
     } else {
       for (int e = 0; e < n_edges; ++e)
         nets.push_back(build_cone_network(n_qubits, ev, p, ev[2 * e], ev[2 * e + 1]));
@@ -204,6 +217,7 @@ extern "C" tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int3
         h.r = opts->r == 0 ? h.k : opts->r;
         h.slice_step = (int32_t)sch.prefix.size();
         h.persistent_elems = lp.persistent_elems;
+        h.n_open = (int32_t)net.open_labels.size();
       }
       h.pred_elems_slice += lp.elems_slice;
       h.pred_elems_prefix += lp.elems_prefix;
@@ -263,7 +277,7 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
   const PlanHeader& h = pl->h;
   if (h.magic != kPlanMagic || h.version != kPlanVersion)
     return fail(TN_E_PLAN, "tn_plan_load: bad magic or version");
-  if (h.k < 0 || h.k > 30 || h.p < 1 || h.p > kMaxP || h.n_programs < 1)
+  if (h.k < 0 || h.k > 30 || h.p < 1 || h.p > kMaxP || h.n_programs < 1 || h.n_open < 0 || h.n_open > 20)
     return fail(TN_E_PLAN, "tn_plan_load: bad header");
   if (!get(cur, end, pl->progs, h.n_programs) || !get(cur, end, pl->leaves, h.n_leaves) ||
       !get(cur, end, pl->steps, h.n_steps) || !get(cur, end, pl->ops, h.n_ops) ||
@@ -299,13 +313,14 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
         (o.type == OP_BIG && pl->steps[o.begin].out_rank < 1))
       return fail(TN_E_PLAN, "tn_plan_load: bad op record");
   for (const auto& s : pl->scalars)
-    if ((s.slice_mask >> h.k) != 0 || s.off + (1ull << __builtin_popcount(s.slice_mask)) > A)
+    if ((s.slice_mask >> h.k) != 0 || (s.open_mask >> h.n_open) != 0 ||
+        s.off + (1ull << (__builtin_popcount(s.slice_mask) + __builtin_popcount(s.open_mask))) > A)
       return fail(TN_E_PLAN, "tn_plan_load: bad scalar record");
   for (const auto& pr : pl->progs)
     if (pr.stepB_begin < 0 || pr.stepB_end > h.n_steps || pr.scal_begin < 0 || pr.scal_end > h.n_scalars ||
         pr.opA_begin < 0 || pr.opB_end > h.n_ops)
       return fail(TN_E_PLAN, "tn_plan_load: bad program record");
-  pl->batchable = pl->h.kind == TN_KIND_AMPLITUDE && pl->h.n_programs == 1;
+  pl->batchable = pl->h.kind == TN_KIND_AMPLITUDE && pl->h.n_programs == 1 && pl->h.n_open == 0;
   for (int oi = pl->progs[0].opB_begin; oi < pl->progs[0].opB_end; ++oi)
     if (pl->ops[oi].type != OP_RUN) pl->batchable = false;
   *out = pl.release();
@@ -357,6 +372,7 @@ extern "C" tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* o) {
   }
   o->big_launches_per_slice = h.big_launches_slice;
   o->slices_batchable = plan->batchable ? 1 : 0;
+  o->n_open = h.n_open;
   return TN_OK;
 }
 
@@ -400,26 +416,33 @@ extern "C" tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int
   return TN_OK;
 }
 
-extern "C" tn_status tn_sum_partials(const tn_plan* plan, const double* partials, double out[2]) {
+extern "C" tn_status tn_sum_partials(const tn_plan* plan, const double* partials, double* out) {
   if (!plan || !partials || !out) return fail(TN_E_INVAL, "tn_sum_partials: null argument");
   const uint64_t n = 1ull << plan->h.k;
-  std::vector<double> buf(partials, partials + 2 * n);
-  uint64_t m = n;
-  while (m > 1) {
-    uint64_t hh = 0;
-    for (uint64_t i = 0; i + 1 < m; i += 2, ++hh) {
-      buf[2 * hh] = buf[2 * i] + buf[2 * (i + 1)];
-      buf[2 * hh + 1] = buf[2 * i + 1] + buf[2 * (i + 1) + 1];
+  const uint64_t A = 1ull << plan->h.n_open;
+  std::vector<double> buf(2 * n);
+  for (uint64_t o = 0; o < A; ++o) {        // batch entry o: fixed pairwise tree over j
+    for (uint64_t j = 0; j < n; ++j) {
+      buf[2 * j] = partials[2 * (j * A + o)];
+      buf[2 * j + 1] = partials[2 * (j * A + o) + 1];
     }
-    if (m & 1) {
-      buf[2 * hh] = buf[2 * (m - 1)];
-      buf[2 * hh + 1] = buf[2 * (m - 1) + 1];
-      ++hh;
+    uint64_t m = n;
+    while (m > 1) {
+      uint64_t hh = 0;
+      for (uint64_t i = 0; i + 1 < m; i += 2, ++hh) {
+        buf[2 * hh] = buf[2 * i] + buf[2 * (i + 1)];
+        buf[2 * hh + 1] = buf[2 * i + 1] + buf[2 * (i + 1) + 1];
+      }
+      if (m & 1) {
+        buf[2 * hh] = buf[2 * (m - 1)];
+        buf[2 * hh + 1] = buf[2 * (m - 1) + 1];
+        ++hh;
+      }
+      m = hh;
     }
-    m = hh;
+    out[2 * o] = buf[0];
+    out[2 * o + 1] = buf[1];
   }
-  out[0] = buf[0];
-  out[1] = buf[1];
   return TN_OK;
 }
 
@@ -442,6 +465,11 @@ tn_status ensure_dev(tn_plan* pl, DevTables** out) {
     CU(up((void**)&t.leaves, pl->leaves.data(), pl->leaves.size() * sizeof(LeafRec)));
     CU(up((void**)&t.scalars, pl->scalars.data(), pl->scalars.size() * sizeof(ScalarRec)));
     CU(up((void**)&t.progs, pl->progs.data(), pl->progs.size() * sizeof(ProgramRec)));
+    for (int l = 0; l < kMaxLanes - 1; ++l) {
+      CU(cudaStreamCreateWithFlags(&t.side[l], cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&t.ev_join[l], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
     it = pl->dev.emplace(dev, t).first;
   }
   *out = &it->second;
@@ -492,6 +520,20 @@ uint64_t slice_off_of(const InRec& in, uint64_t j) {
   return in.slice_mask ? (host_pext(j, in.slice_mask) << in.rank) : 0ull;
 }
 
+// window b of the workspace (b >= 1): win0 + (b - 1) * arena elements (as k_program's window_rel)
+inline uint64_t window_rel_host(uint64_t b, uint64_t win0, uint64_t win_elems) {
+  return b == 0 ? 0ull : win0 + (b - 1) * win_elems;
+}
+
+// element offset of input `in` for slice j in the slice window at `rel` (per-slice tensors, F_REL,
+// live in the window; leaves and prefix outputs are shared)
+template <typename T>
+uint64_t in_off(const InRec& in, uint64_t j, uint64_t rel) {
+  return in.off + slice_off_of<T>(in, j) + ((in.flags & F_REL) ? rel : 0ull);
+}
+// output of a step: phase-B outputs are per-slice
+inline uint64_t out_off(const StepRec& s, uint64_t rel) { return s.out_off + (s.phase == 1 ? rel : 0ull); }
+
 struct ProfScope {
   tn_plan* pl;
   cudaStream_t st;
@@ -525,17 +567,17 @@ struct ProfScope {
 
 // one standalone bucket step (k_group_t with M = 1, else the generic k_bucket)
 template <typename T>
-void run_big(tn_plan* pl, int si, T* ws, uint64_t j, cudaStream_t st) {
+void run_big(tn_plan* pl, int si, T* ws, uint64_t j, cudaStream_t st, uint64_t rel) {
   const StepRec& s = pl->steps[si];
   BigArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.out = ws + s.out_off;
+  a.out = ws + out_off(s, rel);
   a.out_rank = s.out_rank;
   a.n_in = s.n_in;
   double bytes = std::ldexp((double)sizeof(T), s.out_rank);
   for (int t = 0; t < s.n_in; ++t) {
     const InRec& in = s.in[t];
-    a.in[t] = ws + in.off + slice_off_of<T>(in, j);
+    a.in[t] = ws + in_off<T>(in, j, rel);
     a.out_mask[t] = in.out_mask;
     a.pv[t] = in.pv;
     a.flags[t] = in.flags | ((t == 0 && s.inplace) ? 1u : 0u);
@@ -546,25 +588,25 @@ void run_big(tn_plan* pl, int si, T* ws, uint64_t j, cudaStream_t st) {
 }
 
 template <typename T>
-tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, uint64_t j,
+tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, uint64_t j, uint64_t rel,
                   cudaStream_t st) {
   for (int oi = op_b; oi < op_e; ++oi) {
     const OpRec& op = pl->ops[oi];
     if (op.type == OP_BIG) {
-      run_big<T>(pl, op.begin, ws, j, st);
+      run_big<T>(pl, op.begin, ws, j, st, rel);
     } else if (op.type == OP_CHAIN) {
       const StepRec& h = pl->steps[op.begin];
       const StepRec& last = pl->steps[op.end - 1];
       ChainArgs c;
       std::memset(&c, 0, sizeof(c));
       c.m = op.end - op.begin;
-      c.out = ws + last.out_off;
+      c.out = ws + out_off(last, rel);
       c.out_rank = last.out_rank;
-      c.A = ws + h.in[0].off + slice_off_of<T>(h.in[0], j);
+      c.A = ws + in_off<T>(h.in[0], j, rel);
       for (int i = 0; i < c.m; ++i) {
         const StepRec& sk = pl->steps[op.begin + i];
         c.nw[i] = sk.n_in - 1;
-        for (int k = 1; k < sk.n_in; ++k) c.w[i][k - 1] = ws + sk.in[k].off + slice_off_of<T>(sk.in[k], j);
+        for (int k = 1; k < sk.n_in; ++k) c.w[i][k - 1] = ws + in_off<T>(sk.in[k], j, rel);
       }
       const double bytes = (std::ldexp(1.0, (int)h.in[0].rank) + std::ldexp(1.0, c.out_rank)) * sizeof(T);
       ProfScope ps(pl, st, bytes, op.begin, op.end, 2, c.out_rank);
@@ -592,7 +634,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       const int Rf = last.out_rank;
       const uint64_t low = (1ull << Rf) - 1, xrest = (1ull << (M - 1)) - 1;
       const uint64_t hfull = (1ull << h.out_rank) - 1;
-      g.out = ws + last.out_off;
+      g.out = ws + out_off(last, rel);
       g.out_rank = Rf;
       g.M = M;
       double bytes = std::ldexp(1.0, Rf);
@@ -600,7 +642,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       for (int t = 0; t < h.n_in && ok; ++t) {
         const InRec& in = h.in[t];
         GIn& gi = g.in[g.n++];
-        gi.ptr = ws + in.off + slice_off_of<T>(in, j);
+        gi.ptr = ws + in_off<T>(in, j, rel);
         gi.out_mask = in.out_mask & low;
         gi.pv = in.pv;
         gi.rank = in.rank;
@@ -615,7 +657,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         for (int k = 1; k < sk.n_in; ++k) {
           if (g.n >= kMaxIn) { ok = false; break; }
           GIn& gi = g.in[g.n++];
-          gi.ptr = ws + sk.in[k].off + slice_off_of<T>(sk.in[k], j);
+          gi.ptr = ws + in_off<T>(sk.in[k], j, rel);
           gi.out_mask = 0;
           gi.pv = 0;
           gi.rank = 1;
@@ -631,7 +673,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         ps.cancel = !launched;
       }
       if (!launched)   // no instantiation for this shape: run the steps one by one
-        for (int si = op.begin; si < op.end; ++si) run_big<T>(pl, si, ws, j, st);
+        for (int si = op.begin; si < op.end; ++si) run_big<T>(pl, si, ws, j, st, rel);
     } else {
       double bytes = 0.0;
       for (int si = op.begin; si < op.end; ++si) {
@@ -641,7 +683,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       }
       ProfScope ps(pl, st, bytes, op.begin, op.end, 4, pl->steps[op.end - 1].out_rank);
       k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
-                                                  dt.scalars, nullptr, 0, 0, 0);
+                                                  dt.scalars, nullptr, 0, rel, 0);
       last_kernel() = KID_PROGRAM;
     }
     pl->all_launches++;
@@ -694,15 +736,14 @@ tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int 
   T* ws = static_cast<T*>(wsv);
   if ((s = materialize<T>(pl, *dt, gamma, beta, p, ws, st)) != TN_OK) return s;
   const ProgramRec& pr = pl->progs[0];
-  if ((s = run_ops<T>(pl, *dt, pr.opA_begin, pr.opA_end, ws, 0, st)) != TN_OK) return s;
+  if ((s = run_ops<T>(pl, *dt, pr.opA_begin, pr.opA_end, ws, 0, 0, st)) != TN_OK) return s;
   // batched slices: every per-slice step runs in the interpreter -> one launch
   // runs up to nb slices, each CTA in its own window for the per-slice tensors
   const size_t es = sizeof(T);
   const size_t base_bytes = ws_bytes_for(pl->h, es == 8 ? TN_C64 : TN_C128);
   const uint64_t win_bytes = pl->h.arena_elems * es;
   uint64_t nb = 1;
-  if (pl->batchable && win_bytes > 0 && ws_bytes > base_bytes)
-    nb = 1 + (ws_bytes - base_bytes) / win_bytes;
+  if (win_bytes > 0 && ws_bytes > base_bytes) nb = 1 + (ws_bytes - base_bytes) / win_bytes;
   if (pl->batchable && nb >= 2) {
     const uint64_t win0 = base_bytes / es;
     for (uint64_t j = begin; j < end; j += nb) {
@@ -715,11 +756,30 @@ tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int 
     CU(cudaGetLastError());
     return TN_OK;
   }
+  // L slice lanes when the workspace holds L windows of per-slice tensors: slice j runs on lane
+  // (j - begin) % L -- lane 0 on the caller's stream in the base arena, lane l >= 1 on a
+  // library-owned stream in window l.  The latency-bound small steps, launch gaps and partial
+  // waves of one slice overlap the kernels of the others (slices are independent, Eq. 1).
+  const uint64_t L = std::min<uint64_t>({nb, (uint64_t)slice_lanes(), end - begin});
+  if (L >= 2) {
+    CU(cudaEventRecord(dt->ev_fork, st));
+    for (uint64_t l = 1; l < L; ++l) CU(cudaStreamWaitEvent(dt->side[l - 1], dt->ev_fork, 0));
+  }
   for (uint64_t j = begin; j < end; ++j) {
-    if ((s = run_ops<T>(pl, *dt, pr.opB_begin, pr.opB_end, ws, j, st)) != TN_OK) return s;
-    k_finalize<T><<<1, 32, 0, st>>>(dt->scalars, pr.scal_begin, pr.scal_end, ws, j, pr.log2_scale,
-                                   partials_dev + 2 * j);
+    const uint64_t lane = L >= 2 ? (j - begin) % L : 0;
+    cudaStream_t sj = lane ? dt->side[lane - 1] : st;
+    const uint64_t rel = lane ? window_rel_host(lane, base_bytes / es, pl->h.arena_elems) : 0ull;
+    if ((s = run_ops<T>(pl, *dt, pr.opB_begin, pr.opB_end, ws, j, rel, sj)) != TN_OK) return s;
+    {
+      const uint32_t A = 1u << pl->h.n_open;
+      k_finalize<T><<<(A + 127) / 128, 128, 0, sj>>>(dt->scalars, pr.scal_begin, pr.scal_end, ws, j, pr.log2_scale,
+                                                    partials_dev + 2 * (j << pl->h.n_open), rel, pl->h.n_open);
+    }
     pl->all_launches++;
+  }
+  for (uint64_t l = 1; l < L; ++l) {
+    CU(cudaEventRecord(dt->ev_join[l - 1], dt->side[l - 1]));
+    CU(cudaStreamWaitEvent(st, dt->ev_join[l - 1], 0));
   }
   CU(cudaGetLastError());
   return TN_OK;
@@ -761,11 +821,13 @@ extern "C" tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const doub
   if (s != TN_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // scratch: 2*max(n, E) doubles of partials, then the pairwise result in the trailing pad
-  double* res = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(scratch) + align256(16 * std::max<uint64_t>(n, plan->h.n_programs)));
-  k_pairwise<<<1, 32, 0, st>>>(scratch, n, res);
+  const uint64_t A = 1ull << plan->h.n_open;
+  double* res = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(scratch) +
+                                          align256(16 * (std::max<uint64_t>(n, plan->h.n_programs) * A)));
+  k_pairwise<<<(unsigned)((A + 127) / 128), 128, 0, st>>>(scratch, n, A, res);
   const_cast<tn_plan*>(plan)->all_launches++;
   CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(out, res, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out, res, 2 * A * sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return TN_OK;
 }

@@ -24,7 +24,8 @@ def run_sliced(plan, gammas, betas, dtype: int = 0, group=None, device=None,
                compute: Optional[Callable] = None, stream=None):
     """Whole-job sliced amplitude; returns (sigma, partials_host).
 
-    compute(begin, end, partials) fills partials[2j:2j+2] for j in [begin, end); the default is
+    compute(begin, end, partials) fills partials[2(j A + x) : 2(j A + x) + 2] for j in [begin, end)
+    and batch entries x < A = plan.batch (A = 1: a single amplitude); the default is
     the CUDA path (tn_contract_sliced).  Tests on CPU inject their own compute (gloo backend).
     """
     import torch
@@ -38,12 +39,12 @@ def run_sliced(plan, gammas, betas, dtype: int = 0, group=None, device=None,
     begin, end = slice_block(n, rank, world)
     if compute is None:
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        partials = torch.zeros(2 * n, dtype=torch.float64, device=dev)
+        partials = torch.zeros(2 * n * getattr(plan, "batch", 1), dtype=torch.float64, device=dev)
         if end > begin:
             plan.contract_sliced(gammas, betas, begin, end, partials, dtype=dtype, stream=stream)
     else:
         dev = torch.device("cpu") if device is None else torch.device(device)
-        partials = torch.zeros(2 * n, dtype=torch.float64, device=dev)
+        partials = torch.zeros(2 * n * getattr(plan, "batch", 1), dtype=torch.float64, device=dev)
         if end > begin:
             compute(begin, end, partials)
     if world > 1:

@@ -380,3 +380,87 @@ def test_energy_batch_matches_single_and_oracle(dtype):
         assert zz1 == zzs[b] and e1 == ens[b]                                   # same arithmetic
         Eref, _ = energy.maxcut_energy(n, g.edges, ga, be)
         assert abs(ens[b] - Eref) < TOL[dtype] * len(g.edges)
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+def test_two_slice_lanes_match_one_lane_and_oracle(dtype):
+    """Odd slices on the side stream in window 1 (workspace with two windows) give the same
+    partials, bit for bit, as one lane (one window), and match the oracle."""
+    n, p = 44, 2
+    g = random_regular_graph(n, 3, 23)
+    ga, be = qaoa_angles(p, 23)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=3, small_log2=6)
+    assert plan.info["slices_batchable"] == 0
+    outs = []
+    for windows in (1, 2):
+        ws = plan.workspace(dtype, batch=windows)
+        part = torch.zeros(2 * plan.n_slices, dtype=torch.float64, device="cuda")
+        B.tn_contract_sliced(plan.handle, dtype, ga, be, 0, plan.n_slices, ws.data_ptr(), ws.numel(),
+                             torch.cuda.current_stream().cuda_stream, part.data_ptr())
+        torch.cuda.synchronize()
+        outs.append(part.cpu())
+    assert torch.equal(outs[0], outs[1])
+    pre, sl, res, _ = plan.schedule()
+    ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
+    assert rel(plan.sum_partials(outs[1].tolist()), ref) < TOL[dtype]
+
+
+# ------------------------------------------------------------------ amplitude batches (SURVEY §8 f1)
+def _oracle_batch(n, edges, ga, be, opened, pre, sl, res):
+    """Oracle batch with the plan's schedule as data: prefix once, Eq. (1) over the slices, the
+    open indices left open; entries summed over slices in the fixed pairwise
+    order (SPEC.md:414)."""
+    p = len(ga)
+    tens = network.qaoa_amplitude_network(n, edges, ga, be, open_qubits=opened)
+    ol = network.open_labels(n, p, opened)
+    rest, ps = contract.partial_eliminate(tens, pre)
+    parts = []
+    for j in range(1 << len(sl)):
+        fixed = network.fix_indices(rest, contract.slice_assignment(sl, j))
+        parts.append(ps * contract.contract_open(fixed, ol, order=res))
+    return np.array([contract.pairwise_sum([v[x] for v in parts]) for x in range(1 << len(opened))])
+
+
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+@pytest.mark.parametrize("n,p,k,opened,small", [(12, 2, 0, (0, 3, 7), 4), (16, 1, 2, (2, 9), 4),
+                                                (30, 2, 3, (1, 4, 8, 17), 6), (40, 1, 2, (0, 39), 0),
+                                                (24, 3, 2, (5,), 30)])
+def test_amplitude_batch_vs_oracle(dtype, n, p, k, opened, small):
+    """A batch of 2^a amplitudes (open output indices) vs the oracle; entry 0 vs the
+    single-amplitude plan; the state vector where N <= 16."""
+    g = random_regular_graph(n, 3, 3 * n + p)
+    ga, be = qaoa_angles(p, n + 5)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=k, small_log2=small, open_qubits=opened)
+    got = np.array(plan.contract(ga, be, dtype=dtype))
+    pre, sl, res, _ = plan.schedule()
+    ref = _oracle_batch(n, g.edges, ga, be, opened, pre, sl, res)
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(got - ref)) / scale < TOL[dtype]
+    single = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=k, small_log2=small)
+    assert abs(got[0] - single.contract(ga, be, dtype=dtype)) / scale < TOL[dtype]
+    if n <= 16:
+        psi = sv.qaoa_state(n, g.edges, ga, be)
+        qs = sorted(opened)
+        for x in range(1 << len(qs)):
+            bits = [0] * n
+            for b, q in enumerate(qs):
+                bits[q] = (x >> b) & 1
+            assert abs(got[x] - sv.amplitude(psi, bits)) / scale < TOL[dtype]
+
+
+def test_amplitude_batch_sliced_partition_bit_identical():
+    n, p = 30, 1
+    g = random_regular_graph(n, 3, 77)
+    ga, be = qaoa_angles(p, 77)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=3, small_log2=6, open_qubits=(3, 11, 20))
+    A = plan.batch
+    full = torch.zeros(2 * plan.n_slices * A, dtype=torch.float64, device="cuda")
+    plan.contract_sliced(ga, be, 0, plan.n_slices, full, dtype=T.TN_C64)
+    parts = torch.zeros_like(full)
+    for a0, b0 in ((0, 3), (3, 5), (5, 8)):
+        plan.contract_sliced(ga, be, a0, b0, parts, dtype=T.TN_C64)
+    torch.cuda.synchronize()
+    assert torch.equal(full, parts)
+    s1 = plan.sum_partials(full.cpu().tolist())
+    s2, _ = run_sliced(plan, ga, be, dtype=T.TN_C64)
+    assert s1 == s2 and len(s1) == A

@@ -187,3 +187,36 @@ def test_select_sliced_plan_rule_a11():
     best = min(t["pred_bytes_c64"] for t in feas)                  # fewest predicted bytes
     mine = [t for t in feas if t["orderer"] == plan.orderer and t["k"] == plan.info["k"]][0]
     assert mine["pred_bytes_c64"] == best
+
+
+# ------------------------------------------------------------------ amplitude batches (open indices)
+@pytest.mark.parametrize("n,p,k,opened", [(20, 1, 0, (0, 5)), (30, 2, 3, (1, 2, 29)), (60, 1, 4, (7,))])
+def test_open_batch_plan_schedule_and_width(n, p, k, opened):
+    """PAPER.md:599-607 (§6): the open indices are never eliminated nor sliced; the schedule
+    covers every other live label; the result clique of size a does not raise the width while
+    a < c (reported; the replay with the clique added matches the planner's degrees)."""
+    g = random_regular_graph(n, 3, n + 1)
+    ga, be = qaoa_angles(p, n)
+    plan = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=k, open_qubits=opened)
+    assert plan.info["n_open"] == len(opened) and plan.batch == 1 << len(opened)
+    assert plan.info["n_labels"] == n * p + len(opened)
+    pre, sl, res, degs = plan.schedule()
+    assert set(pre) | set(sl) | set(res) == set(range(n * p))
+    assert len(pre) + len(sl) + len(res) == n * p
+    # independent replay: oracle network with the open wires (labels p*N+q) plus their clique
+    tens = network.qaoa_amplitude_network(n, g.edges, ga, be, open_qubits=opened)
+    ol = network.open_labels(n, p, opened)
+    clique = [(np.ones((2, 2)), (ol[i], ol[j])) for i in range(len(ol)) for j in range(i + 1, len(ol))]
+    rep = _replay(tens + clique, pre, sl, res)
+    assert rep == degs
+    single = T.build_plan(g, p, "amplitude", "min-fill", n_sliced=k)
+    assert plan.width <= single.width + len(opened)
+
+
+def test_open_batch_bad_arguments():
+    g = random_regular_graph(10, 3, 1)
+    for bad in ((10,), (-1,), (3, 3)):
+        with pytest.raises(B.TnError):
+            T.build_plan(g, 1, "amplitude", "min-fill", open_qubits=bad)
+    with pytest.raises(B.TnError):
+        T.build_plan(g, 1, "energy", "min-fill", open_qubits=(1,))
