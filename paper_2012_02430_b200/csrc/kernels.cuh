@@ -1227,6 +1227,7 @@ __device__ __forceinline__ uint64_t window_rel(uint32_t b, uint64_t win0, uint64
 }
 
 // mode 0: CTA 0 runs steps [begin, end) of the plan (slice j).
+// mode 3: CTA i runs step begin + i (the independent steps of one prefix level).
 // mode 1: CTA (b, y) runs program b's phase-B steps in window y (parameter set y of a batched
 //         energy), then writes its final value to results[y * gridDim.x + b].
 // mode 2: CTA b runs program 0's phase-B steps for slice j + b in window b (batched slices) and
@@ -1239,7 +1240,11 @@ __global__ void __launch_bounds__(kProgramThreads) k_program(const StepRec* __re
                                                              double2* results, int mode,
                                                              uint64_t win0, uint64_t win_elems) {
   int b = begin, e = end;
-  uint64_t rel = mode == 0 ? win0 : 0ull, jj = j;   // mode 0: win0 = slice-window offset
+  uint64_t rel = (mode == 0 || mode == 3) ? win0 : 0ull, jj = j;   // modes 0, 3: win0 = window offset
+  if (mode == 3) {   // CTA i runs step begin + i (independent steps of one level)
+    b = begin + (int)blockIdx.x;
+    e = b + 1;
+  }
   const ProgramRec* pr = nullptr;
   if (mode == 1) {
     pr = &progs[blockIdx.x];

@@ -18,7 +18,7 @@
 namespace tnb {
 
 constexpr uint32_t kPlanMagic = 0x32424E54u;  // "TNB2"
-constexpr uint32_t kPlanVersion = 7;
+constexpr uint32_t kPlanVersion = 8;
 constexpr int kMaxIn = 8;     // inputs per bucket step
 constexpr int kMaxP = 16;     // QAOA depth supported by the materializer
 constexpr int kMaxFactors = 4;
@@ -66,7 +66,7 @@ struct StepRec {
   InRec in[kMaxIn];
 };
 
-enum OpType : int32_t { OP_BIG = 0, OP_RUN = 1, OP_CHAIN = 2, OP_GROUP = 3 };
+enum OpType : int32_t { OP_BIG = 0, OP_RUN = 1, OP_CHAIN = 2, OP_GROUP = 3, OP_PRUN = 4 };
 constexpr int kMaxGroupPlan = 5;    // summed indices of one fused merge group (k_group_t, M <= 5)
 constexpr int kMaxChain = 8;        // summed indices of one fused reduce chain (W table 2^8)
 constexpr int kMaxChainW = 3;       // x-only weights per chained step
@@ -77,7 +77,9 @@ struct OpRec {
                   //   inputs are rank-1 weights on the summed index -- as ONE streaming pass
                   //   out[o] = sum_{x < 2^m} W[x] A[o + x 2^{R_A - m}] (exact re-association);
                   // OP_GROUP: steps [begin, end) -- any step followed by in-place reduce steps with
-                  //   rank-1 weights -- as ONE k_group_t launch summing M = end-begin indices
+                  //   rank-1 weights -- as ONE k_group_t launch summing M = end-begin indices;
+                  // OP_PRUN: steps [begin, end) -- independent small steps of one dependency level
+                  //   of the prefix -- in one interpreter launch, one CTA per step
   int32_t begin;
   int32_t end;
   int32_t phase;

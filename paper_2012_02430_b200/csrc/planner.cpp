@@ -575,6 +575,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     StepRec rec;
     std::vector<int> ins;
     int outsym;
+    int orig = 0;    // position in the elimination order (before the level sort of phase A)
   };
   std::vector<PendingStep> pend;
   for (int pos = 0; pos < total_pos; ++pos) {
@@ -667,7 +668,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     for (int id : ins) syms[id].death = t_now;
     const int oid = (int)syms.size();
     syms.push_back(o);
-    pend.push_back(PendingStep{rec, ins, oid});
+    pend.push_back(PendingStep{rec, ins, oid, (int)pend.size()});
     route(oid);
   }
   for (size_t i = 0; i < syms.size(); ++i) {
@@ -681,6 +682,48 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   int nA = 0;
   for (auto& ps : pend)
     if (ps.rec.phase == 0) nA++;
+  // ---- the prefix (phase A) in dependency levels: its buckets form a shallow DAG (C5a: 143
+  // steps, depth 5), so the steps of one level run side by side, one CTA each (OP_PRUN).  Phase A
+  // is stably sorted by (level, big step); the memory a level frees is released only when the
+  // level ends, so no output of a level overwrites an input another step of the level still reads.
+  std::vector<int> lend(nsteps + 1, 0);   // per step (new order): time at which its level ends
+  std::vector<int> level(nsteps, 0);
+  {
+    std::vector<int> producer(syms.size(), -1);
+    for (int si = 0; si < nsteps; ++si) producer[pend[si].outsym] = si;
+    std::vector<int> lev(nsteps, 0);
+    for (int si = 0; si < nsteps; ++si) {
+      int l = 0;
+      for (int id : pend[si].ins)
+        if (producer[id] >= 0) l = std::max(l, lev[producer[id]]);
+      lev[si] = l + 1;
+    }
+    std::vector<int> idx(nA);
+    for (int i = 0; i < nA; ++i) idx[i] = i;
+    auto big = [&](int si) { return pend[si].rec.out_rank > small_log2 ? 1 : 0; };
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+      if (lev[a] != lev[b]) return lev[a] < lev[b];
+      return big(a) < big(b);
+    });
+    std::vector<PendingStep> re;
+    re.reserve(nsteps);
+    for (int i = 0; i < nA; ++i) { re.push_back(pend[idx[i]]); level[i] = lev[idx[i]]; }
+    for (int si = nA; si < nsteps; ++si) { re.push_back(pend[si]); level[si] = 0; }
+    pend.swap(re);
+    for (auto& sy : syms) sy.death = -1;
+    for (int si = 0; si < nsteps; ++si) {
+      for (int id : pend[si].ins) syms[id].death = si + 1;
+      syms[pend[si].outsym].birth = si + 1;
+    }
+    for (int si = 0; si < nsteps; ++si) {
+      int e = si;
+      if (si < nA)
+        while (e + 1 < nA && level[e + 1] == level[si]) ++e;
+      lend[si + 1] = e + 1;
+    }
+    for (auto& sy : syms)   // phase-A inputs live until their consumer's level ends
+      if (sy.death >= 1 && sy.death <= nA) sy.death = lend[sy.death];
+  }
   // lifetimes: tensors used in phase B but born before it persist across slices
   for (auto& s : syms) {
     if (s.scalar_ref) s.death = T_end;
@@ -699,6 +742,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   std::vector<std::vector<int>> dies(T_end + 2);
   for (size_t i = 0; i < syms.size(); ++i)
     if (syms[i].death <= T_end) dies[syms[i].death].push_back((int)i);
+  std::vector<std::vector<std::pair<uint64_t, uint64_t>>> deferred(T_end + 2);
   for (int si = 0; si < nsteps; ++si) {
     const int t = si + 1;
     PendingStep& ps = pend[si];
@@ -706,11 +750,12 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     if (ps.rec.inplace) {
       Sym& a = syms[ps.ins[0]];
       o.off = a.off;
-      ar.release(a.off + o.size, a.size - o.size);
+      deferred[lend[t]].push_back({a.off + o.size, a.size - o.size});   // the upper half
       a.size = 0;  // its lower part now belongs to the output
     } else {
       o.off = ar.alloc(o.size);
     }
+    for (auto& d : deferred[t]) ar.release(d.first, d.second);
     for (int id : dies[t]) {
       if (syms[id].persistent) continue;
       ar.release(syms[id].off, syms[id].size);
@@ -737,13 +782,14 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     }
     out.leaves.push_back(lr);
   }
+  out.degrees.assign(nsteps, 0);
   for (int si = 0; si < nsteps; ++si) {
     PendingStep& ps = pend[si];
     ps.rec.out_off = syms[ps.outsym].off;
     for (int t = 0; t < ps.rec.n_in; ++t) ps.rec.in[t].off = syms[ps.ins[t]].off;
     const Sym& o = syms[ps.outsym];
     ps.rec.degree = (int)o.idx.size();
-    out.degrees.push_back(ps.rec.degree);
+    out.degrees[ps.orig] = ps.rec.degree;    // reported in elimination order (tn_plan_schedule)
     out.width = std::max(out.width, ps.rec.degree);
     out.steps.push_back(ps.rec);
   }
@@ -777,7 +823,8 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
         continue;
       }
       int j = i;
-      while (j < nsteps && out.steps[j].phase == phase && out.steps[j].out_rank <= small_log2) {
+      while (j < nsteps && out.steps[j].phase == phase && out.steps[j].out_rank <= small_log2 &&
+             (phase == 1 || level[j] == level[i])) {
         if (j > i) {
           const StepRec& s2 = out.steps[j];
           double e2 = std::ldexp(1.0, s2.out_rank);
@@ -786,7 +833,8 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
         }
         ++j;
       }
-      out.ops.push_back(OpRec{OP_RUN, i, j, phase});
+      // a phase-A run lies inside one dependency level: its steps are independent (OP_PRUN)
+      out.ops.push_back(OpRec{phase == 0 ? OP_PRUN : OP_RUN, i, j, phase});
       i = j;
     }
   }

@@ -307,7 +307,7 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
   }
   for (const auto& o : pl->ops)
     if (o.begin < 0 || o.end > h.n_steps || o.begin >= o.end ||
-        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN && o.type != OP_GROUP) ||
+        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN && o.type != OP_GROUP && o.type != OP_PRUN) ||
         (o.type == OP_GROUP && (o.end - o.begin > kMaxGroupPlan || o.end - o.begin < 2)) ||
         (o.type == OP_CHAIN && (o.end - o.begin > kMaxChain || pl->steps[o.end - 1].out_rank < 1)) ||
         (o.type == OP_BIG && pl->steps[o.begin].out_rank < 1))
@@ -682,8 +682,12 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         for (int t = 0; t < sk.n_in; ++t) bytes += std::ldexp((double)sizeof(T), (int)sk.in[t].rank);
       }
       ProfScope ps(pl, st, bytes, op.begin, op.end, 4, pl->steps[op.end - 1].out_rank);
-      k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
-                                                  dt.scalars, nullptr, 0, rel, 0);
+      if (op.type == OP_PRUN)   // independent steps of one prefix level: one CTA each
+        k_program<T><<<(unsigned)(op.end - op.begin), kProgramThreads, 0, st>>>(
+            dt.steps, op.begin, op.end, ws, j, dt.progs, dt.scalars, nullptr, 3, rel, 0);
+      else
+        k_program<T><<<1, kProgramThreads, 0, st>>>(dt.steps, op.begin, op.end, ws, j, dt.progs,
+                                                    dt.scalars, nullptr, 0, rel, 0);
       last_kernel() = KID_PROGRAM;
     }
     pl->all_launches++;
