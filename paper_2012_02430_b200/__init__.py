@@ -190,8 +190,10 @@ def select_sliced_plan(graph, p: int, max_width: int, k_min: int = 0, k_max: int
         results = list(ex.map(run, jobs))
     tried, cands = [], []
     for k, idx, pl, total in results:
+        o, q, tau, seed = orderers[idx] if len(orderers[idx]) == 4 else (*orderers[idx], 0)
         tried.append({"k": k, "orderer": pl.orderer, "width": pl.width, "pred_bytes_c64": total,
-                      "unsliced_width": pl.info["unsliced_width"], "slice_step": pl.info["slice_step"]})
+                      "unsliced_width": pl.info["unsliced_width"], "slice_step": pl.info["slice_step"],
+                      "recipe": {"orderer": o, "n_sliced": k, "rg_q": q, "rg_tau": tau, "rg_seed": seed}})
         if pl.width <= max_width:
             cands.append((total, k, idx, pl))
     if not cands:
