@@ -799,9 +799,9 @@ __global__ void __launch_bounds__(kBucketThreads, 2) k_pair(const PArgs a) {
 // batched complex GEMM with K = 2^M:
 //     out[o] = sum_{x < K} C[x] A[F_A(o) + G_A(x)] B[F_B(o) + G_B(x)]
 // Output bits are of class a (in A only), b (in B only), c (in both: the batch).  A CTA tile is a
-// set of TB = 8 + RAB + RBB output bits chosen by the host (runtime.cu try_launch_gemm):
+// set of TB = 5 + WB + RAB + RBB output bits chosen by the host (launch_gemm.cu try_launch_gemm):
 //   tile-local bits 0..4  = output bits 0..4 (lanes: every warp store is 256 contiguous bytes),
-//   tile-local bits 5..7  = three more output bits (warps), preferably of class a / b,
+//   tile-local bits 5..   = WB more output bits (the 2^WB warps), preferably of class a / b,
 //   tile-local bits 8..   = RAB a-bits and RBB b-bits: each thread owns a 2^RAB x 2^RBB register
 //                           block, so every A value feeds 2^RBB outputs and every B value 2^RAB.
 // Per tile the A and B chunks (every x-row, every tile bit the input holds) are copied to shared
@@ -809,8 +809,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) k_pair(const PArgs a) {
 // between consecutive tiles is not reloaded).  The tile-constant factor C[x] (inputs without tile
 // bits) multiplies the B values.  Complex multiply-adds use packed FP32x2 FMAs (FFMA2: one complex
 // MAC = 2 instructions).  Output written once with streaming stores.
-constexpr int kGemmThreads = 256;
-constexpr int kGemmMaxTB = 12;
+constexpr int kGemmMaxTB = 16;
 struct MArgs {
   void* out;
   const void* in[2];                   // A, B
@@ -860,10 +859,12 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 
-template <int M, int RAB, int RBB, bool HASC>
-__global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
+template <int M, int RAB, int RBB, bool HASC, int WB>
+__global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArgs a) {
+  constexpr int kGemmThreads = 32 << WB;   // 2^WB warps; tile-local bits 5 .. 5+WB-1 on the warps
+  constexpr int TL = 5 + WB;               // thread bits of the tile
   constexpr int K = 1 << M, RA = 1 << RAB, RB = 1 << RBB;
-  constexpr int TB = 8 + RAB + RBB;
+  constexpr int TB = TL + RAB + RBB;
   constexpr int NB = 64 - TB;
   const uint32_t tid = threadIdx.x;
   const uint64_t n_tiles = 1ull << (a.out_rank - TB);
@@ -919,7 +920,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
   uint64_t othr = 0;
   uint32_t iathr = 0, ibthr = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < TL; ++k) {
     if ((tid >> k) & 1u) {
       othr += 1ull << a.outbit[k];
       if (a.chbit[0][k] >= 0) iathr += 1u << a.chbit[0][k];
@@ -933,14 +934,14 @@ __global__ void __launch_bounds__(kGemmThreads, 2) k_gemm(const MArgs a) {
     ora[i] = 0; iar[i] = 0;
 #pragma unroll
     for (int k = 0; k < RAB; ++k)
-      if ((i >> k) & 1) { ora[i] += 1ull << a.outbit[8 + k]; iar[i] += 1u << a.chbit[0][8 + k]; }
+      if ((i >> k) & 1) { ora[i] += 1ull << a.outbit[TL + k]; iar[i] += 1u << a.chbit[0][TL + k]; }
   }
 #pragma unroll
   for (int j = 0; j < RB; ++j) {
     orb[j] = 0; ibr[j] = 0;
 #pragma unroll
     for (int k = 0; k < RBB; ++k)
-      if ((j >> k) & 1) { orb[j] += 1ull << a.outbit[8 + RAB + k]; ibr[j] += 1u << a.chbit[1][8 + RAB + k]; }
+      if ((j >> k) & 1) { orb[j] += 1ull << a.outbit[TL + RAB + k]; ibr[j] += 1u << a.chbit[1][TL + RAB + k]; }
   }
   uint32_t cur[2], curc[kMaxIn - 2];
 #pragma unroll

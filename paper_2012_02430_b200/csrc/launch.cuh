@@ -98,8 +98,8 @@ inline int gemm_stages() {   // TNB_GEMM_STAGES=2..4 (default 3)
   }();
   return s;
 }
-constexpr int kMaxLanes = 4;
-inline int slice_lanes() {   // TNB_LANES=1..4 (default 4); TNB_ONE_LANE=1 == TNB_LANES=1
+constexpr int kMaxLanes = 8;
+inline int slice_lanes() {   // TNB_LANES=1..8 (default 4); TNB_ONE_LANE=1 == TNB_LANES=1
   static const int n = [] {
     if (env_flag("TNB_ONE_LANE")) return 1;
     const char* v = std::getenv("TNB_LANES");

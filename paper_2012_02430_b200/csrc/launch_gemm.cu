@@ -8,20 +8,39 @@ namespace tnb {
 // dynamic shared memory per CTA so that two CTAs (plus ~5 KB static each) fit the 228 KB of an SM
 constexpr size_t kGemmSmemBudget = 100 * 1024;
 
-template <int M, int RAB, int RBB>
+template <int M, int RAB, int RBB, int WB>
 void launch_m(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
-  allow_smem(k_gemm<M, RAB, RBB, true>, smem);
+  allow_smem(k_gemm<M, RAB, RBB, true, WB>, smem);
   last_kernel() = KID_GEMM;
-  k_gemm<M, RAB, RBB, true><<<grid, kGemmThreads, smem, st>>>(ma);
+  k_gemm<M, RAB, RBB, true, WB><<<grid, 32 << WB, smem, st>>>(ma);
 }
 
-template <int M>
+template <int M, int WB>
 bool dispatch_m(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
-  if (rab == 2 && rbb == 2) { launch_m<M, 2, 2>(ma, grid, smem, st); return true; }
-  if (rab == 2 && rbb == 1) { launch_m<M, 2, 1>(ma, grid, smem, st); return true; }
-  if (rab == 1 && rbb == 2) { launch_m<M, 1, 2>(ma, grid, smem, st); return true; }
-  if (rab == 1 && rbb == 1) { launch_m<M, 1, 1>(ma, grid, smem, st); return true; }
+  if (rab == 3 && rbb == 2) { launch_m<M, 3, 2, WB>(ma, grid, smem, st); return true; }
+  if (rab == 2 && rbb == 2) { launch_m<M, 2, 2, WB>(ma, grid, smem, st); return true; }
+  if (rab == 2 && rbb == 1) { launch_m<M, 2, 1, WB>(ma, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 2) { launch_m<M, 1, 2, WB>(ma, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 1) { launch_m<M, 1, 1, WB>(ma, grid, smem, st); return true; }
   return false;
+}
+
+inline bool gemm_ra3() {
+  static const bool on = [] {
+    const char* v = std::getenv("TNB_GEMM_RA3");   // measured slower on C5a (61 vs 66 /s): off
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+// CTA size: 2^WB warps (TNB_GEMM_WB = 2 or 3); 4-warp CTAs run 4 per SM, 8-warp CTAs 2 per SM
+inline int gemm_wb() {
+  static const int wb = [] {
+    const char* v = std::getenv("TNB_GEMM_WB");
+    const int x = v ? std::atoi(v) : 3;
+    return x == 2 ? 2 : 3;
+  }();
+  return wb;
 }
 
 // A group whose varying inputs are two tensors holding a-only and b-only output bits runs as a
@@ -48,7 +67,7 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     uint64_t ca = g.in[ia].out_mask & ~g.in[ib].out_mask, cb = g.in[ib].out_mask & ~g.in[ia].out_mask;
     const uint64_t cc = g.in[ia].out_mask & g.in[ib].out_mask, cn = full & ~(g.in[ia].out_mask | g.in[ib].out_mask);
     if (cn & 31ull) return false;                       // lanes must be held by A or B
-    int ra[2], rb[2], nra = 0, nrb = 0;
+    int ra[3], rb[3], nra = 0, nrb = 0;
     for (int b = 5; b < R; ++b) {
       if (((ca >> b) & 1) && nra < 2) ra[nra++] = b;
       if (((cb >> b) & 1) && nrb < 2) rb[nrb++] = b;
@@ -57,13 +76,14 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     uint64_t used = 31ull;
     for (int i = 0; i < nra; ++i) used |= 1ull << ra[i];
     for (int i = 0; i < nrb; ++i) used |= 1ull << rb[i];
+    const int WB = gemm_wb();
     int wb[3], nw = 0;
-    for (int pass = 0; pass < 2 && nw < 3; ++pass)
-      for (int b = 5; b < R && nw < 3; ++b) {
+    for (int pass = 0; pass < 2 && nw < WB; ++pass)
+      for (int b = 5; b < R && nw < WB; ++b) {
         const uint64_t cls = pass == 0 ? (ca | cb) : cc;
         if (!((used >> b) & 1) && ((cls >> b) & 1)) { wb[nw++] = b; used |= 1ull << b; }
       }
-    if (nw < 3) return false;
+    if (nw < WB) return false;
     // role of B (the operand formatted in shared memory, kept across consecutive tiles): the one
     // whose chunk changes least often.  The tile is symmetric in the roles; the traversal flips
     // A's exclusive non-tile bits first, so B stays for 2^(that count) tiles; ties -> B with fewer
@@ -78,15 +98,36 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
         std::swap(nra, nrb);
       }
     }
+    // an 8 x 4 register block when A has a third exclusive bit to spare (TNB_GEMM_RA3=1; off by
+    // default -- 128 registers, measured slower):
+    // half the shared loads per FFMA2 and the per-tile overhead spread over twice the outputs
+    if (nra == 2 && nrb == 2 && gemm_ra3()) {
+      for (int b = 5; b < R; ++b)
+        if (((ca >> b) & 1) && !((used >> b) & 1)) { ra[nra++] = b; used |= 1ull << b; break; }
+      bool ok3 = nra == 3 && R >= 5 + WB + nra + nrb;
+      if (ok3) {   // shared memory of the larger tile at two ring slots must fit the budget
+        auto rows = [&](const GIn& in) {
+          std::vector<uint64_t> parts;
+          for (int x = 0; x < (1 << g.M); ++x)
+            if (std::find(parts.begin(), parts.end(), in.gx[x]) == parts.end()) parts.push_back(in.gx[x]);
+          return (uint64_t)parts.size();
+        };
+        const uint64_t na = rows(g.in[ia]) << __builtin_popcountll(used & g.in[ia].out_mask);
+        const uint64_t nb = rows(g.in[ib]) << __builtin_popcountll(used & g.in[ib].out_mask);
+        const uint64_t need = 2 * (na + nb) * 8 + (na + nb) * 4 + ((16ull << g.M) << __builtin_popcountll(used & g.in[ib].out_mask)) + 16;
+        ok3 = need <= (WB == 3 ? kGemmSmemBudget : kGemmSmemBudget / 2);
+      }
+      if (nra == 3 && !ok3) { used &= ~(1ull << ra[2]); --nra; }
+    }
     const GIn& A = g.in[ia];
     const GIn& Bq = g.in[ib];
-    const int TB = 8 + nra + nrb;
-    if (R < TB) return false;
+    const int TB = 5 + WB + nra + nrb;
+    if (R < TB || TB > kGemmMaxTB) return false;
     MArgs ma;
     std::memset(&ma, 0, sizeof(ma));
     int u = 0;
     for (int b = 0; b < 5; ++b) ma.outbit[u++] = (uint8_t)b;
-    for (int i = 0; i < 3; ++i) ma.outbit[u++] = (uint8_t)wb[i];
+    for (int i = 0; i < WB; ++i) ma.outbit[u++] = (uint8_t)wb[i];
     for (int i = 0; i < nra; ++i) ma.outbit[u++] = (uint8_t)ra[i];
     for (int i = 0; i < nrb; ++i) ma.outbit[u++] = (uint8_t)rb[i];
     const uint64_t tmask = used;
@@ -145,7 +186,8 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     const uint32_t dep_u32 = (ma.nrows[0] << (ma.nch[0] - ma.lv[0])) + (ma.nrows[1] << (ma.nch[1] - ma.lv[1]));
     const size_t bf_bytes = ((size_t)16 << g.M) << ma.nch[1];
     int S = gemm_stages();
-    while (S > 2 && ((size_t)S * (sz[0] + sz[1]) * 8 + dep_u32 * 4 + bf_bytes + 16) > kGemmSmemBudget) --S;
+    const size_t budget = WB == 3 ? kGemmSmemBudget : kGemmSmemBudget / 2;   // 2 or 4 CTAs per SM
+    while (S > 2 && ((size_t)S * (sz[0] + sz[1]) * 8 + dep_u32 * 4 + bf_bytes + 16) > budget) --S;
     ma.stages = S;
     for (int k = 0; k < S; ++k) {
       ma.sm_in[0][k] = k * sz[0];
@@ -159,7 +201,7 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     }
     ma.sm_bf_bytes = (u32 * 4 + 15) / 16 * 16;
     const size_t smem = ma.sm_bf_bytes + bf_bytes;
-    if (smem > kGemmSmemBudget) return false;
+    if (smem > budget) return false;
     // traversal of the tile index: a-only bits first (B chunk and B' unchanged), then b-only, then
     // the rest
     int np = 0;
@@ -182,13 +224,23 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
       std::fprintf(stderr, "\n");
     }
     const uint64_t tiles = 1ull << (R - TB);
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 2);
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * (WB == 3 ? 2 : 4));
+    if (WB == 2) {
+      switch (g.M) {
+        case 1: return dispatch_m<1, 2>(ma, nra, nrb, grid, smem, st);
+        case 2: return dispatch_m<2, 2>(ma, nra, nrb, grid, smem, st);
+        case 3: return dispatch_m<3, 2>(ma, nra, nrb, grid, smem, st);
+        case 4: return dispatch_m<4, 2>(ma, nra, nrb, grid, smem, st);
+        case 5: return dispatch_m<5, 2>(ma, nra, nrb, grid, smem, st);
+        default: return false;
+      }
+    }
     switch (g.M) {
-      case 1: return dispatch_m<1>(ma, nra, nrb, grid, smem, st);
-      case 2: return dispatch_m<2>(ma, nra, nrb, grid, smem, st);
-      case 3: return dispatch_m<3>(ma, nra, nrb, grid, smem, st);
-      case 4: return dispatch_m<4>(ma, nra, nrb, grid, smem, st);
-      case 5: return dispatch_m<5>(ma, nra, nrb, grid, smem, st);
+      case 1: return dispatch_m<1, 3>(ma, nra, nrb, grid, smem, st);
+      case 2: return dispatch_m<2, 3>(ma, nra, nrb, grid, smem, st);
+      case 3: return dispatch_m<3, 3>(ma, nra, nrb, grid, smem, st);
+      case 4: return dispatch_m<4, 3>(ma, nra, nrb, grid, smem, st);
+      case 5: return dispatch_m<5, 3>(ma, nra, nrb, grid, smem, st);
       default: return false;
     }
   }

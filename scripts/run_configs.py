@@ -79,11 +79,17 @@ def run_amplitude(name, k_range, max_width, sample_slices=3, batched=False, time
     ga, be = qaoa_angles(w.p, 0)
     t0 = time.perf_counter()
     small = 30 if batched else -1
-    try:
-        plan, tried = T.select_sliced_plan(g, w.p, max_width, k_min=k_range[0], k_max=k_range[1], small_log2=small)
-    except T.TnError:
-        # this seed's instance is wider than the survey's: take the narrowest plan found
-        plan, tried = T.select_sliced_plan(g, w.p, 64, k_min=k_range[1], k_max=k_range[1], small_log2=small)
+    recipes = json.load(open(bench.RECIPES)) if os.path.exists(bench.RECIPES) else {}
+    if name in recipes and not batched:
+        # the offline search's pick (scripts/plan_search.py, reading A11), as bench.py uses it
+        plan, _, _, _, meta = bench.build_workload_plan(name)
+        tried = meta["tried"]
+    else:
+        try:
+            plan, tried = T.select_sliced_plan(g, w.p, max_width, k_min=k_range[0], k_max=k_range[1], small_log2=small)
+        except T.TnError:
+            # this seed's instance is wider than the survey's: take the narrowest plan found
+            plan, tried = T.select_sliced_plan(g, w.p, 64, k_min=k_range[1], k_max=k_range[1], small_log2=small)
     plan_s = time.perf_counter() - t0
     info = plan.info
     rec = {"config": name, "kind": "amplitude", "n": w.n, "p": w.p, "plan_s": plan_s, "orderer": plan.orderer,
@@ -180,7 +186,7 @@ def main():
             ("C2", lambda: run_amplitude("C2", (0, 0), 62)),
             ("C4a", lambda: run_amplitude("C4a", (8, 12), 30, batched=True)),
             ("C4b", lambda: run_amplitude("C4b", (8, 12), 30)),
-            ("C5a", lambda: run_amplitude("C5a", (3, 8), 32)),
+            ("C5a", lambda: run_amplitude("C5a", (5, 8), 32)),
             ("C5b", lambda: run_amplitude("C5b", (8, 16), 32, time_slices=4, sample_slices=1))]
     for name, fn in jobs:
         if not want(name):
