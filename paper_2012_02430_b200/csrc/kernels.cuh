@@ -826,7 +826,7 @@ struct MArgs {
   uint32_t sm_in[2][4];                // dynamic smem element offset of ring slot (input, slot)
   int32_t stages;                      // ring slots per input (2..4); lookahead = stages - 1 tiles
   uint32_t sm_dep[2];                  // dynamic smem uint32 offset of the piece offset table (nrows << (nch - lv) entries)
-  uint32_t sm_bf_bytes;                // dynamic smem byte offset of the formatted B' chunk (2^nch[1] x (2^M + 1) float4)
+  uint32_t sm_bf_bytes;                // dynamic smem byte offset of the formatted B' chunk (2^M x 2^nch[1] float4)
   int32_t c_tile_dep;                  // a constant input holds an output bit: C changes between tiles
   const void* cin[kMaxIn];             // constant inputs (no tile bit)
   uint64_t cmask[kMaxIn];
@@ -886,24 +886,16 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
   for (int b = tid; b < NB; b += kGemmThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
   // piece offset tables: piece c (2^lv elements) of input u's chunk -> element offset from the
   // tile's base offset (row part G_u(x) + in-row part), so a copy is one shared load + one add
-  // A: one 8-byte piece per (x, ia) (its shared layout is x-innermost, below); B: 2^lv-element
-  // pieces of each distinct row
-  for (uint32_t c = tid; c < ((uint32_t)K << a.nch[0]); c += kGemmThreads) {
-    const uint32_t ia = c & ((1u << a.nch[0]) - 1u), x = c >> a.nch[0];
-    uint32_t off = a.rowoff[0][a.row[0][x]];
-    for (uint32_t k = 0; k < a.nch[0]; ++k)
-      if ((ia >> k) & 1u) off += a.posoff[0][k];
-    smu[a.sm_dep[0] + c] = off;
-  }
-  {
-    const uint32_t lp = a.nch[1] - a.lv[1];
-    const uint32_t np = a.nrows[1] << lp;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t lp = a.nch[u] - a.lv[u];
+    const uint32_t np = a.nrows[u] << lp;
     for (uint32_t c = tid; c < np; c += kGemmThreads) {
-      const uint32_t ib = (c & ((1u << lp) - 1u)) << a.lv[1];
-      uint32_t off = a.rowoff[1][c >> lp];
-      for (uint32_t k = a.lv[1]; k < a.nch[1]; ++k)
-        if ((ib >> k) & 1u) off += a.posoff[1][k];
-      smu[a.sm_dep[1] + c] = off;
+      const uint32_t ia = (c & ((1u << lp) - 1u)) << a.lv[u];
+      uint32_t off = a.rowoff[u][c >> lp];
+      for (uint32_t k = a.lv[u]; k < a.nch[u]; ++k)
+        if ((ia >> k) & 1u) off += a.posoff[u][k];
+      smu[a.sm_dep[u] + c] = off;
     }
   }
   __syncthreads();
@@ -961,21 +953,12 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
   __syncthreads();
 
   // cp.async of input u's chunk (all rows) at base offset `base` into buffer `buf`
-  // A's chunk is stored x-innermost with a padded row: element (ia, x) at ia * (K + 1) + x, so a
-  // thread's operands for every x are at immediate offsets from one base, and lanes with distinct
-  // ia hit distinct banks (odd word stride)
   auto prefetch = [&](int u, uint32_t base, int slot) {
     const float2* src = static_cast<const float2*>(a.in[u]) + base;
     float2* dst = sm + a.sm_in[u][slot];
+    const uint32_t np = a.nrows[u] << (a.nch[u] - a.lv[u]);
     const uint32_t* tab = smu + a.sm_dep[u];
-    if (u == 0) {
-      const uint32_t mA = (1u << a.nch[0]) - 1u;
-      for (uint32_t c = tid; c < ((uint32_t)K << a.nch[0]); c += kGemmThreads)
-        cp_async8(dst + (c & mA) * (K + 1) + (c >> a.nch[0]), src + tab[c]);
-      return;
-    }
-    const uint32_t np = a.nrows[1] << (a.nch[1] - a.lv[1]);
-    if (a.lv[1]) {
+    if (a.lv[u]) {
       for (uint32_t c = tid; c < np; c += kGemmThreads) cp_async16(dst + (c << 1), src + tab[c]);
     } else {
       for (uint32_t c = tid; c < np; c += kGemmThreads) cp_async8(dst + c, src + tab[c]);
@@ -1035,18 +1018,13 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
         const uint32_t x = e >> a.nch[1], idx = e & (nB - 1u);
         float2 b = sBraw[((uint32_t)a.row[1][x] << a.nch[1]) + idx];
         if (HASC) b = cmul(b, Cs[x]);
-        bf[idx * (K + 1) + x] = make_float4(b.x, b.y, -b.y, b.x);   // x-innermost, padded row
+        bf[e] = make_float4(b.x, b.y, -b.y, b.x);
       }
       fixed_ver = ver[1];
       __syncthreads();
     }
-    const float2* sA = sm + a.sm_in[0][cslot[0]];
-    const float2* pa[RA];
-    const float4* pb[RB];
-#pragma unroll
-    for (int i = 0; i < RA; ++i) pa[i] = sA + (iathr + iar[i]) * (K + 1);
-#pragma unroll
-    for (int j = 0; j < RB; ++j) pb[j] = bf + (ibthr + ibr[j]) * (K + 1);
+    const float2* sA = sm + a.sm_in[0][cslot[0]] + iathr;
+    const float4* sB = bf + ibthr;
     uint64_t acc[RA][RB];
 #pragma unroll
     for (int i = 0; i < RA; ++i)
@@ -1054,12 +1032,14 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
       for (int j = 0; j < RB; ++j) acc[i][j] = 0ull;
 #pragma unroll
     for (int x = 0; x < K; ++x) {
+      const float2* pa = sA + ((uint32_t)a.row[0][x] << a.nch[0]);
+      const float4* pb = sB + ((uint32_t)x << a.nch[1]);
       float2 av[RA];
       float4 bv[RB];
 #pragma unroll
-      for (int i = 0; i < RA; ++i) av[i] = pa[i][x];
+      for (int i = 0; i < RA; ++i) av[i] = pa[iar[i]];
 #pragma unroll
-      for (int j = 0; j < RB; ++j) bv[j] = pb[j][x];
+      for (int j = 0; j < RB; ++j) bv[j] = pb[ibr[j]];
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll

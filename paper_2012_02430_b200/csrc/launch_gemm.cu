@@ -114,7 +114,7 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
         };
         const uint64_t na = rows(g.in[ia]) << __builtin_popcountll(used & g.in[ia].out_mask);
         const uint64_t nb = rows(g.in[ib]) << __builtin_popcountll(used & g.in[ib].out_mask);
-        const uint64_t need = 2 * (na + nb) * 8 * 2 + (na + nb) * 4 * 2 + ((32ull << g.M) << __builtin_popcountll(used & g.in[ib].out_mask)) + 16;
+        const uint64_t need = 2 * (na + nb) * 8 + (na + nb) * 4 + ((16ull << g.M) << __builtin_popcountll(used & g.in[ib].out_mask)) + 16;
         ok3 = need <= (WB == 3 ? kGemmSmemBudget : kGemmSmemBudget / 2);
       }
       if (nra == 3 && !ok3) { used &= ~(1ull << ra[2]); --nra; }
@@ -180,12 +180,11 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
       ma.in[s] = in.ptr;
       ma.mask[s] = in.out_mask;
       ma.pv[s] = in.pv;
-      sz[s] = s == 0 ? ((1u << g.M) + 1) << k : ma.nrows[s] << k;   // A: x-innermost padded rows
+      sz[s] = ma.nrows[s] << k;
     }
-    ma.lv[0] = 0;   // A is copied in 8-byte pieces (one per (x, ia))
     // ring slots: as many as fit the per-CTA budget (2 CTAs per SM), at most gemm_stages()
-    const uint32_t dep_u32 = ((1u << g.M) << ma.nch[0]) + (ma.nrows[1] << (ma.nch[1] - ma.lv[1]));
-    const size_t bf_bytes = ((size_t)16 * ((1u << g.M) + 1)) << ma.nch[1];
+    const uint32_t dep_u32 = (ma.nrows[0] << (ma.nch[0] - ma.lv[0])) + (ma.nrows[1] << (ma.nch[1] - ma.lv[1]));
+    const size_t bf_bytes = ((size_t)16 << g.M) << ma.nch[1];
     int S = gemm_stages();
     const size_t budget = WB == 3 ? kGemmSmemBudget : kGemmSmemBudget / 2;   // 2 or 4 CTAs per SM
     while (S > 2 && ((size_t)S * (sz[0] + sz[1]) * 8 + dep_u32 * 4 + bf_bytes + 16) > budget) --S;
@@ -196,10 +195,10 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     }
     smem_elems = S * (sz[0] + sz[1]);
     uint32_t u32 = 2 * smem_elems;                       // uint32 units
-    ma.sm_dep[0] = u32;
-    u32 += (1u << g.M) << ma.nch[0];
-    ma.sm_dep[1] = u32;
-    u32 += ma.nrows[1] << (ma.nch[1] - ma.lv[1]);
+    for (int s = 0; s < 2; ++s) {
+      ma.sm_dep[s] = u32;
+      u32 += ma.nrows[s] << (ma.nch[s] - ma.lv[s]);
+    }
     ma.sm_bf_bytes = (u32 * 4 + 15) / 16 * 16;
     const size_t smem = ma.sm_bf_bytes + bf_bytes;
     if (smem > budget) return false;
