@@ -15,6 +15,31 @@ void launch_m(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
   k_gemm<M, RAB, RBB, true, WB><<<grid, 32 << WB, smem, st>>>(ma);
 }
 
+template <int M, int RAB, int RBB>
+void launch_ws(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
+  allow_smem(k_gemm_ws<M, RAB, RBB>, smem);
+  last_kernel() = KID_GEMM;
+  k_gemm_ws<M, RAB, RBB><<<grid, kGemmWsThreads, smem, st>>>(ma);
+}
+
+template <int M>
+bool dispatch_ws(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
+  if (rab == 2 && rbb == 2) { launch_ws<M, 2, 2>(ma, grid, smem, st); return true; }
+  if (rab == 2 && rbb == 1) { launch_ws<M, 2, 1>(ma, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 2) { launch_ws<M, 1, 2>(ma, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 1) { launch_ws<M, 1, 1>(ma, grid, smem, st); return true; }
+  return false;
+}
+
+// warp-specialised k_gemm (producer warp + mbarriers) for tile-independent C: TNB_GEMM_WS=0 off
+inline bool gemm_ws() {
+  static const bool on = [] {
+    const char* v = std::getenv("TNB_GEMM_WS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 template <int M, int WB>
 bool dispatch_m(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
   if (rab == 3 && rbb == 2) { launch_m<M, 3, 2, WB>(ma, grid, smem, st); return true; }
@@ -47,9 +72,18 @@ inline int gemm_wb() {
 // register-blocked batched complex GEMM (k_gemm, c64).  Returns false when the shape does not
 // qualify (the caller then tries k_pair / k_group_t).
 template <typename T>
+bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig);
+
+template <typename T>
 bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
+  static const bool contig = env_flag("TNB_GEMM_CONTIG");
+  return (contig && try_launch_gemm_impl<T>(g, st, true)) || try_launch_gemm_impl<T>(g, st, false);
+}
+
+template <typename T>
+bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig) {
   if constexpr (!std::is_same<T, float2>::value) {
-    (void)g; (void)st;
+    (void)g; (void)st; (void)contig;
     return false;
   } else {
     if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) return false;
@@ -78,9 +112,11 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     for (int i = 0; i < nrb; ++i) used |= 1ull << rb[i];
     const int WB = gemm_wb();
     int wb[3], nw = 0;
-    for (int pass = 0; pass < 2 && nw < WB; ++pass)
+    // warp bits: the lowest free a/b bits (reuse), or with TNB_GEMM_CONTIG=1 the lowest free bits of
+    // any class (a more contiguous tile: its 256-byte store segments closer together in HBM)
+    for (int pass = contig ? 1 : 0; pass < 2 && nw < WB; ++pass)
       for (int b = 5; b < R && nw < WB; ++b) {
-        const uint64_t cls = pass == 0 ? (ca | cb) : cc;
+        const uint64_t cls = pass == 0 ? (ca | cb) : (contig ? (ca | cb | cc) : cc);
         if (!((used >> b) & 1) && ((cls >> b) & 1)) { wb[nw++] = b; used |= 1ull << b; }
       }
     if (nw < WB) return false;
@@ -225,6 +261,16 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
     }
     const uint64_t tiles = 1ull << (R - TB);
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * (WB == 3 ? 2 : 4));
+    if (WB == 3 && !ma.c_tile_dep && gemm_ws() && nra <= 2 && nrb <= 2 && ma.stages <= kGemmMaxSlots) {
+      switch (g.M) {
+        case 1: return dispatch_ws<1>(ma, nra, nrb, grid, smem, st);
+        case 2: return dispatch_ws<2>(ma, nra, nrb, grid, smem, st);
+        case 3: return dispatch_ws<3>(ma, nra, nrb, grid, smem, st);
+        case 4: return dispatch_ws<4>(ma, nra, nrb, grid, smem, st);
+        case 5: return dispatch_ws<5>(ma, nra, nrb, grid, smem, st);
+        default: break;
+      }
+    }
     if (WB == 2) {
       switch (g.M) {
         case 1: return dispatch_m<1, 2>(ma, nra, nrb, grid, smem, st);

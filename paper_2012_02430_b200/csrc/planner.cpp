@@ -945,6 +945,39 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       oi += best_g;
     }
     out.ops.swap(fused);
+    // reduce chains among the small steps of phase-B interpreter runs (e.g. the final reduction of
+    // a slice to its scalar) run as streaming chain launches too -- unless every per-slice op is
+    // an interpreter run (then slices run batched, one CTA each, and stay that way)
+    bool all_runs = true;
+    for (const auto& op : out.ops)
+      if (op.phase == 1 && op.type != OP_RUN) all_runs = false;
+    if (!all_runs) {
+      std::vector<OpRec> ops2;
+      for (const auto& op : out.ops) {
+        if (op.phase != 1 || op.type != OP_RUN) {
+          ops2.push_back(op);
+          continue;
+        }
+        int i = op.begin, run_start = op.begin;
+        while (i < op.end) {
+          if (is_reduce(out.steps[i])) {
+            int j = i + 1;
+            while (j < op.end && j - i < kMaxChain && out.steps[j].inplace && is_reduce(out.steps[j]) &&
+                   out.steps[j].in[0].off == out.steps[j - 1].out_off)
+              ++j;
+            if (j - i >= 2) {
+              if (run_start < i) ops2.push_back(OpRec{OP_RUN, run_start, i, 1});
+              ops2.push_back(OpRec{OP_CHAIN, i, j, 1});
+              run_start = i = j;
+              continue;
+            }
+          }
+          ++i;
+        }
+        if (run_start < op.end) ops2.push_back(OpRec{OP_RUN, run_start, op.end, 1});
+      }
+      out.ops.swap(ops2);
+    }
   }
   for (auto& op : out.ops) (op.phase == 0 ? out.launches_prefix : out.launches_slice)++;
   out.launches_slice += 1;  // per-slice finalize

@@ -613,9 +613,9 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       constexpr int VEC = VecT<T>::n;
       const uint64_t work = ((1ull << c.out_rank) + VEC - 1) / VEC;
       const uint64_t blocks = (work + kBucketThreads - 1) / kBucketThreads;
-      if (blocks < (uint64_t)num_sms() * 2 && c.m >= 3 && (1ull << c.out_rank) >= 32ull * VEC) {
-        // few outputs, many rows: split the rows over the warps of a CTA (k_chain_split)
-        const uint64_t nblk = (1ull << c.out_rank) / (32ull * VEC);
+      if (blocks < (uint64_t)num_sms() * 2 && c.m >= 3) {
+        // few outputs, many rows: split the rows over the threads of a CTA (k_chain_split)
+        const uint64_t nblk = std::max<uint64_t>(1, (1ull << c.out_rank) / (32ull * VEC));
         const unsigned g2 = (unsigned)std::min<uint64_t>(nblk, (uint64_t)num_sms() * 8);
         k_chain_split<T><<<g2, kBucketThreads, 0, st>>>(c);
         last_kernel() = KID_CHAIN_SPLIT;

@@ -1,0 +1,5 @@
+set -x; O=gpurun_out/${TAG:-r1u}; mkdir -p $O
+export PATH=/usr/local/cuda/bin:$PATH
+timeout 600 python -m pytest tests/test_gpu_parity.py -k "group_kernels or fused" -x -q > $O/pytest_group.log 2>&1; echo "pytest group exit $?"; tail -2 $O/pytest_group.log
+timeout 900 python bench.py --no-cpu-baseline > $O/bench.log 2>&1; echo "bench exit $?"; python -c "import json;d=json.loads(open('$O/bench.log').read().strip().splitlines()[-1]);r=d['roofline'];print(d['value'],d['e2e']['value'],r['kernel'],r['frac'],r['path']['frac'],{k:(round(v['ms_share_of_step'],3),round(v['GBps'])) for k,v in r['families'].items()},d['clocks'])"
+timeout 600 python scripts/step_profile.py --out $O/steps.json > $O/steps.log 2>&1; head -6 $O/steps.log
