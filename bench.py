@@ -58,7 +58,7 @@ def build_workload_plan(name: str = "C5a", seed: int = 0, search: bool = False):
     if rec is not None:
         r = rec["recipe"]
         plan = T.build_plan(g, w.p, "amplitude", r["orderer"], n_sliced=r["n_sliced"], rg_q=r["rg_q"],
-                            rg_tau=r["rg_tau"], rg_seed=r["rg_seed"])
+                            rg_tau=r["rg_tau"], rg_seed=r["rg_seed"], r=r.get("r", 0))
         if plan.width > cap:
             raise RuntimeError(f"recipe for {name} gives width {plan.width} > {cap}")
         plan.orderer = rec["orderer"]

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--k-max", type=int, default=None)
     ap.add_argument("--seeds", type=int, default=6)
     ap.add_argument("--q", type=int, default=16)
+    ap.add_argument("--r", type=int, default=0, help="indices sliced per round (0: r = n, one round)")
+    ap.add_argument("--dry", action="store_true", help="print only, do not update the recipe file")
     args = ap.parse_args()
     import bench
     import paper_2012_02430_b200 as T
@@ -39,11 +41,15 @@ def main():
     orderers += [("rgreedy", args.q, tau, s) for tau in (0.3, 0.5) for s in range(min(3, args.seeds))]
     t0 = time.time()
     _, tried = T.select_sliced_plan(g, w.p, bench.MAX_WIDTH.get(args.workload, 32), k_min=kmin, k_max=kmax,
-                                    orderers=orderers)
+                                    orderers=orderers, r=args.r)
+    for t in tried:
+        t["recipe"]["r"] = args.r
     ok = sorted([t for t in tried if t["width"] <= bench.MAX_WIDTH.get(args.workload, 32)],
                 key=lambda t: (t["pred_bytes_c64"], t["k"]))
     for t in ok[:10]:
         print(t)
+    if args.dry:
+        return
     try:
         cur = json.load(open(RECIPES))
     except Exception:
