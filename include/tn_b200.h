@@ -207,8 +207,11 @@ tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* const* in_dev,
  * elimination-order layout).  Input t has popcount(out_mask[t]) + popcount(x_mask[t]) bits;
  * every input must hold at least one summed index.  1 <= M <= 5, 1 <= n_in <= 8,
  * 11 <= out_rank <= 40.  kernel: 0 = the library's choice (as in a plan), 1 = k_gemm
- * (register-blocked batched complex GEMM, c64 only), 2 = k_pair, 3 = k_group_t; TN_E_INVAL when
- * the requested kernel does not take this shape.  Asynchronous on `stream`. */
+ * (register-blocked batched complex GEMM on the FP32 pipes, c64 only), 2 = k_pair, 3 = k_group_t,
+ * 4 = k_gemm_tc (the same GEMM on the tensor cores: tcgen05.mma kind::tf32 with a 3xTF32 split,
+ * accumulators in TMEM; c64 only; needs >= 7 output bits held by one operand only, >= 3 by the
+ * other only, 2 <= ... <= 32 summed values per tile row fitting shared memory); TN_E_INVAL when the
+ * requested kernel does not take this shape.  Asynchronous on `stream`. */
 tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in, const void* const* in_dev,
                              const uint64_t* out_mask, const uint32_t* x_mask, void* out_dev,
                              int32_t out_rank, int32_t kernel, void* stream);

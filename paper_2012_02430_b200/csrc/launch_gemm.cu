@@ -77,6 +77,13 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig);
 template <typename T>
 bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   static const bool contig = env_flag("TNB_GEMM_CONTIG");
+  if (std::is_same<T, float2>::value && gemm_tc_enabled() && try_launch_gemm_tc(g, st)) return true;
+  return (contig && try_launch_gemm_impl<T>(g, st, true)) || try_launch_gemm_impl<T>(g, st, false);
+}
+
+template <typename T>
+bool try_launch_gemm_simt(const GDesc& g, cudaStream_t st) {
+  static const bool contig = env_flag("TNB_GEMM_CONTIG");
   return (contig && try_launch_gemm_impl<T>(g, st, true)) || try_launch_gemm_impl<T>(g, st, false);
 }
 
@@ -294,5 +301,7 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig) {
 
 template bool try_launch_gemm<float2>(const GDesc&, cudaStream_t);
 template bool try_launch_gemm<double2>(const GDesc&, cudaStream_t);
+template bool try_launch_gemm_simt<float2>(const GDesc&, cudaStream_t);
+template bool try_launch_gemm_simt<double2>(const GDesc&, cudaStream_t);
 
 }  // namespace tnb

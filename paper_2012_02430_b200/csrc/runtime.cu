@@ -972,7 +972,7 @@ extern "C" tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in,
     return fail(TN_E_INVAL, "tn_eliminate_group: bad argument");
   if (out_rank < 11 || out_rank > 40) return fail(TN_E_INVAL, "tn_eliminate_group: out_rank out of range");
   if (dtype != TN_C64 && dtype != TN_C128) return fail(TN_E_DTYPE, "unsupported dtype");
-  if (kernel < 0 || kernel > 3) return fail(TN_E_INVAL, "tn_eliminate_group: unknown kernel");
+  if (kernel < 0 || kernel > 4) return fail(TN_E_INVAL, "tn_eliminate_group: unknown kernel");
   GDesc g;
   std::memset(&g, 0, sizeof(g));
   g.out = out_dev;
@@ -1006,7 +1006,8 @@ extern "C" tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   bool ok;
   if (dtype == TN_C64) {
-    ok = kernel == 1 ? try_launch_gemm<float2>(g, st)
+    ok = kernel == 1 ? try_launch_gemm_simt<float2>(g, st)
+       : kernel == 4 ? try_launch_gemm_tc(g, st)
        : kernel == 2 ? try_launch_pair<float2>(g, st)
        : kernel == 3 ? try_launch_group<float2>(g, st)
        : (try_launch_gemm<float2>(g, st) || try_launch_pair<float2>(g, st) || try_launch_group<float2>(g, st));

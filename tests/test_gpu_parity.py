@@ -217,6 +217,40 @@ def test_group_kernels_vs_oracle(case, kernel):
         assert np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30) < TOL[dtype] * 0.1
 
 
+TC_CASES = [
+    # (out_rank, M, classes from bit 0 up (a: A only, b: B only, c: both), xa, xb, cmask_hi)
+    (18, 3, "abccabcaabcbabaaac", None, None, 0),          # the bit pattern of C5a's top group
+    (17, 3, "bacbbcabbabbbcbbb", None, None, 0),           # B holds the most exclusive bits (swap)
+    (16, 1, "aaaacaaabbbbbccc", None, None, 0),            # K' = 4 zero-padded to one K-chunk
+    (17, 2, "ccaaaaaaabbbbbcbb", 0b01, None, 0),           # A lacks x_1; low diag bits
+    (18, 5, "aabbcaaaaabbbcccab", None, 0b10110, 0),       # K = 32, B lacks x_0 and x_3
+    (19, 3, "abcabcaaaabbbcccaab", None, None, 1 << 18),   # tile-dependent constant factor
+    (20, 4, "acbcacbcaaaaabbbbccc", None, None, 0),
+]
+
+
+@pytest.mark.parametrize("case", range(len(TC_CASES)))
+def test_gemm_tc_vs_oracle(case):
+    """k_gemm_tc (tcgen05 kind::tf32, 3xTF32 split) on GEMM-shaped merge groups vs the oracle at
+    the complex64 tolerance; several tiles per CTA, ragged diag / col splits."""
+    out_rank, M, cls_s, xa, xb, chi = TC_CASES[case]
+    rng = np.random.default_rng(5000 + case)
+    cls = list(cls_s)
+    assert len(cls) == out_rank
+    masks, xms, shapes = _gemm_group(rng, out_rank, M, cls, xa, xb, chi)
+    arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+    dev = [torch.tensor(a, dtype=torch.complex64, device="cuda") for a in arrays]
+    out = torch.full((2 ** out_rank,), float("nan"), dtype=torch.complex64, device="cuda")
+    B.tn_eliminate_group(T.TN_C64, M, [d.data_ptr() for d in dev], masks, xms, out.data_ptr(), out_rank,
+                         4, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.complex128)
+    ref = _oracle_group(arrays, masks, xms, M, out_rank)
+    assert np.all(np.isfinite(got)), "output element not written"
+    err = np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30)
+    assert err < TOL[T.TN_C64] * 0.1, err
+
+
 # ------------------------------------------------------------------ amplitudes, small/medium
 @pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
 @pytest.mark.parametrize("n,p,k,orderer", [(12, 1, 0, "min-fill"), (14, 2, 0, "min-degree"),
