@@ -117,7 +117,7 @@ inline bool gemm_disabled() {
 // which kernel the last launcher on this thread used (per-launch profile records)
 enum KernelId : int { KID_NONE = 0, KID_BUCKET = 1, KID_CHAIN = 2, KID_GROUP = 3, KID_PAIR = 4,
                       KID_GEMM = 5, KID_CHAIN_SPLIT = 6, KID_PROGRAM = 7,
-                      KID_GEMM_TC = 8 };
+                      KID_GEMM_TC = 8, KID_GEMM_FC = 9 };
 inline int& last_kernel() {
   static thread_local int k = KID_NONE;
   return k;
@@ -128,6 +128,9 @@ inline int& last_kernel() {
 template <typename T> bool try_launch_gemm(const GDesc& g, cudaStream_t st);   // k_gemm_tc first (c64), else k_gemm
 bool try_launch_gemm_tc(const GDesc& g, cudaStream_t st);
 bool gemm_tc_enabled();                                                          // TNB_GEMM_TC=1
+// producer group g (GEMM-shaped) computed tile by tile and consumed by group g3 (its input tin)
+template <typename T> bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
+bool fc_enabled();                                                               // TNB_NO_FC=1 off
 template <typename T> bool try_launch_gemm_simt(const GDesc& g, cudaStream_t st);   // k_gemm / k_gemm_ws only                        // tcgen05 kind::tf32, c64
 template <typename T> bool try_launch_pair(const GDesc& g, cudaStream_t st);
 template <typename T> bool try_launch_group(const GDesc& g, cudaStream_t st);

@@ -66,7 +66,7 @@ struct StepRec {
   InRec in[kMaxIn];
 };
 
-enum OpType : int32_t { OP_BIG = 0, OP_RUN = 1, OP_CHAIN = 2, OP_GROUP = 3, OP_PRUN = 4 };
+enum OpType : int32_t { OP_BIG = 0, OP_RUN = 1, OP_CHAIN = 2, OP_GROUP = 3, OP_PRUN = 4, OP_GROUP_FEED = 5 };
 constexpr int kMaxGroupPlan = 5;    // summed indices of one fused merge group (k_group_t, M <= 5)
 constexpr int kMaxChain = 8;        // summed indices of one fused reduce chain (W table 2^8)
 constexpr int kMaxChainW = 3;       // x-only weights per chained step
@@ -79,7 +79,11 @@ struct OpRec {
                   // OP_GROUP: steps [begin, end) -- any step followed by in-place reduce steps with
                   //   rank-1 weights -- as ONE k_group_t launch summing M = end-begin indices;
                   // OP_PRUN: steps [begin, end) -- independent small steps of one dependency level
-                  //   of the prefix -- in one interpreter launch, one CTA per step
+                  //   of the prefix -- in one interpreter launch, one CTA per step;
+                  // OP_GROUP_FEED: an OP_GROUP whose output is a full input of the next op (an
+                  //   OP_GROUP) and read by nothing else: the two may run as ONE launch that computes
+                  //   the output tile by tile and consumes it without writing it (k_gemm_fc), else
+                  //   as the two groups
   int32_t begin;
   int32_t end;
   int32_t phase;

@@ -12,7 +12,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <stdexcept>
 
@@ -686,6 +689,67 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   // steps, depth 5), so the steps of one level run side by side, one CTA each (OP_PRUN).  Phase A
   // is stably sorted by (level, big step); the memory a level frees is released only when the
   // level ends, so no output of a level overwrites an input another step of the level still reads.
+  // ---- phase B: a merge block (a merge step and the in-place reduce steps after it) whose output
+  // is a full input of a later merge step c (it holds every output bit of c and c's summed index)
+  // moves down to just before c, so that the runtime can compute the block's output tile by tile
+  // inside c's launch instead of writing and re-reading it (OP_GROUP_FEED, k_gemm_fc).  Legal: the
+  // block's inputs exist before it, its output has exactly one consumer (c), and the steps it
+  // moves past neither read its output nor produce its inputs -- the arithmetic is unchanged; only
+  // the block's inputs live longer.  TNB_NO_FEED=1 keeps the elimination order.
+  if (!(std::getenv("TNB_NO_FEED") && std::getenv("TNB_NO_FEED")[0] == '1')) {
+    std::vector<int> consumer(syms.size(), -1);
+    for (int si = nA; si < nsteps; ++si)
+      for (int id : pend[si].ins) consumer[id] = si;
+    std::vector<std::vector<std::pair<int, int>>> attach(nsteps);   // blocks emitted right before c
+    std::vector<char> moved(nsteps, 0);
+    int si = nA;
+    while (si < nsteps) {
+      if (pend[si].rec.inplace) { ++si; continue; }
+      int e = si + 1;
+      while (e < nsteps && pend[e].rec.inplace && pend[e].ins[0] == pend[e - 1].outsym) ++e;
+      const int T = pend[e - 1].outsym;
+      const int c = consumer[T];
+      bool ok = c > e && e - si >= 2 && e - si <= kMaxGroupPlan && pend[c].rec.out_rank > small_log2 &&
+                pend[e - 1].rec.out_rank > small_log2;
+      if (ok) {
+        const StepRec& cr = pend[c].rec;
+        int t = -1;
+        for (size_t k2 = 0; k2 < pend[c].ins.size(); ++k2)
+          if (pend[c].ins[k2] == T) t = (int)k2;
+        const uint64_t full = (1ull << cr.out_rank) - 1;
+        ok = t >= 0 && cr.in[t].out_mask == full && cr.in[t].pv == (uint32_t)cr.out_rank &&
+             cr.in[t].slice_mask == 0;
+      }
+      if (std::getenv("TNB_PLAN_DEBUG"))
+        std::fprintf(stderr, "feed? block [%d,%d) R=%d -> consumer %d (inplace %d R %d) ok=%d\n", si, e,
+                     pend[e - 1].rec.out_rank, c, c >= 0 ? pend[c].rec.inplace : -1, c >= 0 ? pend[c].rec.out_rank : -1, (int)ok);
+      if (ok) {
+        attach[c].push_back({si, e});
+        for (int k2 = si; k2 < e; ++k2) moved[k2] = 1;
+      }
+      si = e;
+    }
+    std::vector<PendingStep> re(pend.begin(), pend.begin() + nA);
+    re.reserve(nsteps);
+    std::vector<int> stack;
+    std::function<void(int)> emit = [&](int s2) {
+      for (const auto& b : attach[s2])
+        for (int k2 = b.first; k2 < b.second; ++k2) emit(k2);
+      re.push_back(pend[s2]);
+    };
+    for (int s2 = nA; s2 < nsteps; ++s2)
+      if (!moved[s2]) emit(s2);
+    if ((int)re.size() != nsteps) {
+      *err = "internal: phase-B reorder lost steps";
+      return out;
+    }
+    pend.swap(re);
+    for (auto& sy : syms) sy.death = -1;
+    for (int s2 = 0; s2 < nsteps; ++s2) {
+      for (int id : pend[s2].ins) syms[id].death = s2 + 1;
+      syms[pend[s2].outsym].birth = s2 + 1;
+    }
+  }
   std::vector<int> lend(nsteps + 1, 0);   // per step (new order): time at which its level ends
   std::vector<int> level(nsteps, 0);
   {
@@ -978,6 +1042,28 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       }
       out.ops.swap(ops2);
     }
+  }
+  // ---- producer -> consumer pairs (phase B): an OP_GROUP whose output is a full input of the
+  // next op's head (an OP_GROUP) becomes OP_GROUP_FEED; its output is then never written or read
+  // when the fused launch takes the pair (predicted bytes / launches assume it does)
+  for (size_t oi = 0; oi + 1 < out.ops.size(); ++oi) {
+    OpRec& a = out.ops[oi];
+    const OpRec& b = out.ops[oi + 1];
+    if (a.phase != 1 || b.phase != 1 || a.type != OP_GROUP || (b.type != OP_GROUP && b.type != OP_GROUP_FEED)) continue;
+    const StepRec& last = out.steps[a.end - 1];
+    const StepRec& head = out.steps[b.begin];
+    const uint64_t full = (1ull << head.out_rank) - 1;
+    bool feed = false;
+    for (int t = 0; t < head.n_in; ++t)
+      if (head.in[t].off == last.out_off && head.in[t].out_mask == full && head.in[t].pv == (uint32_t)head.out_rank &&
+          head.in[t].rank == (uint32_t)last.out_rank && (head.in[t].flags & F_REL))
+        feed = true;
+    if (!feed) continue;
+    a.type = OP_GROUP_FEED;
+    const double t_elems = 2.0 * std::ldexp(1.0, last.out_rank);
+    out.elems_slice -= t_elems;
+    out.elems_big_slice -= t_elems;
+    out.big_launches_slice -= 1;
   }
   for (auto& op : out.ops) (op.phase == 0 ? out.launches_prefix : out.launches_slice)++;
   out.launches_slice += 1;  // per-slice finalize

@@ -305,13 +305,18 @@ extern "C" tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out) {
         return fail(TN_E_PLAN, "tn_plan_load: bad step input record");
     }
   }
-  for (const auto& o : pl->ops)
+  const int n_ops = (int)pl->ops.size();
+  for (int oi = 0; oi < n_ops; ++oi) {
+    const OpRec& o = pl->ops[oi];
     if (o.begin < 0 || o.end > h.n_steps || o.begin >= o.end ||
-        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN && o.type != OP_GROUP && o.type != OP_PRUN) ||
-        (o.type == OP_GROUP && (o.end - o.begin > kMaxGroupPlan || o.end - o.begin < 2)) ||
+        (o.type != OP_BIG && o.type != OP_RUN && o.type != OP_CHAIN && o.type != OP_GROUP && o.type != OP_PRUN &&
+         o.type != OP_GROUP_FEED) ||
+        ((o.type == OP_GROUP || o.type == OP_GROUP_FEED) && (o.end - o.begin > kMaxGroupPlan || o.end - o.begin < 2)) ||
+        (o.type == OP_GROUP_FEED && (oi + 1 >= n_ops || (pl->ops[oi + 1].type != OP_GROUP && pl->ops[oi + 1].type != OP_GROUP_FEED))) ||
         (o.type == OP_CHAIN && (o.end - o.begin > kMaxChain || pl->steps[o.end - 1].out_rank < 1)) ||
         (o.type == OP_BIG && pl->steps[o.begin].out_rank < 1))
       return fail(TN_E_PLAN, "tn_plan_load: bad op record");
+  }
   for (const auto& s : pl->scalars)
     if ((s.slice_mask >> h.k) != 0 || (s.open_mask >> h.n_open) != 0 ||
         s.off + (1ull << (__builtin_popcount(s.slice_mask) + __builtin_popcount(s.open_mask))) > A)
@@ -391,7 +396,7 @@ extern "C" tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int
   *n = (int64_t)plan->steps.size();
   std::vector<char> big(plan->steps.size(), 0);
   for (const auto& op : plan->ops)
-    if (op.type == OP_BIG || op.type == OP_CHAIN || op.type == OP_GROUP)
+    if (op.type == OP_BIG || op.type == OP_CHAIN || op.type == OP_GROUP || op.type == OP_GROUP_FEED)
       for (int i = op.begin; i < op.end; ++i) big[i] = op.type == OP_BIG ? 1 : (op.type == OP_CHAIN ? 2 : 3);
   for (int64_t i = 0; out && i < cap && i < *n; ++i) {
     const StepRec& s = plan->steps[i];
@@ -587,6 +592,51 @@ void run_big(tn_plan* pl, int si, T* ws, uint64_t j, cudaStream_t st, uint64_t r
   launch_bucket<T>(a, st);
 }
 
+// the GDesc of a fused merge group (OP_GROUP / OP_GROUP_FEED): head step + (M-1) in-place reduce
+// followers whose other inputs are rank-1 weights on their summed index
+template <typename T>
+bool group_desc(const tn_plan* pl, const OpRec& op, T* ws, uint64_t j, uint64_t rel, GDesc& g, double& bytes) {
+  const StepRec& h = pl->steps[op.begin];
+  const StepRec& last = pl->steps[op.end - 1];
+  std::memset(&g, 0, sizeof(g));
+  const int M = op.end - op.begin;
+  const int Rf = last.out_rank;
+  const uint64_t low = (1ull << Rf) - 1, xrest = (1ull << (M - 1)) - 1;
+  const uint64_t hfull = (1ull << h.out_rank) - 1;
+  g.out = ws + out_off(last, rel);
+  g.out_rank = Rf;
+  g.M = M;
+  bytes = std::ldexp(1.0, Rf);
+  for (int t = 0; t < h.n_in; ++t) {
+    const InRec& in = h.in[t];
+    GIn& gi = g.in[g.n++];
+    gi.ptr = ws + in_off<T>(in, j, rel);
+    gi.out_mask = in.out_mask & low;
+    gi.pv = in.pv;
+    gi.rank = in.rank;
+    gi.full = in.out_mask == hfull;
+    for (int x = 0; x < (1 << M); ++x)
+      gi.gx[x] = host_fmap(((uint64_t)x & xrest) << Rf, in.out_mask, in.pv) +
+                 ((uint64_t)((x >> (M - 1)) & 1) << in.pv);
+    bytes += std::ldexp(1.0, (int)in.rank);
+  }
+  for (int i = 1; i < M; ++i) {
+    const StepRec& sk = pl->steps[op.begin + i];
+    for (int k = 1; k < sk.n_in; ++k) {
+      if (g.n >= kMaxIn) return false;
+      GIn& gi = g.in[g.n++];
+      gi.ptr = ws + in_off<T>(sk.in[k], j, rel);
+      gi.out_mask = 0;
+      gi.pv = 0;
+      gi.rank = 1;
+      gi.full = false;
+      for (int x = 0; x < (1 << M); ++x) gi.gx[x] = (uint64_t)((x >> (M - 1 - i)) & 1);
+      bytes += 2.0;
+    }
+  }
+  return true;
+}
+
 template <typename T>
 tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, uint64_t j, uint64_t rel,
                   cudaStream_t st) {
@@ -624,51 +674,38 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         k_chain<T><<<grid, kBucketThreads, 0, st>>>(c);
         last_kernel() = KID_CHAIN;
       }
-    } else if (op.type == OP_GROUP) {
+    } else if (op.type == OP_GROUP || op.type == OP_GROUP_FEED) {
       // head step + (M-1) in-place reduce followers with rank-1 weights, summed in one pass
-      const StepRec& h = pl->steps[op.begin];
-      const StepRec& last = pl->steps[op.end - 1];
       GDesc g;
-      std::memset(&g, 0, sizeof(g));
-      const int M = op.end - op.begin;
-      const int Rf = last.out_rank;
-      const uint64_t low = (1ull << Rf) - 1, xrest = (1ull << (M - 1)) - 1;
-      const uint64_t hfull = (1ull << h.out_rank) - 1;
-      g.out = ws + out_off(last, rel);
-      g.out_rank = Rf;
-      g.M = M;
-      double bytes = std::ldexp(1.0, Rf);
-      bool ok = true;
-      for (int t = 0; t < h.n_in && ok; ++t) {
-        const InRec& in = h.in[t];
-        GIn& gi = g.in[g.n++];
-        gi.ptr = ws + in_off<T>(in, j, rel);
-        gi.out_mask = in.out_mask & low;
-        gi.pv = in.pv;
-        gi.rank = in.rank;
-        gi.full = in.out_mask == hfull;
-        for (int x = 0; x < (1 << M); ++x)
-          gi.gx[x] = host_fmap(((uint64_t)x & xrest) << Rf, in.out_mask, in.pv) +
-                     ((uint64_t)((x >> (M - 1)) & 1) << in.pv);
-        bytes += std::ldexp(1.0, (int)in.rank);
-      }
-      for (int i = 1; i < M && ok; ++i) {
-        const StepRec& sk = pl->steps[op.begin + i];
-        for (int k = 1; k < sk.n_in; ++k) {
-          if (g.n >= kMaxIn) { ok = false; break; }
-          GIn& gi = g.in[g.n++];
-          gi.ptr = ws + in_off<T>(sk.in[k], j, rel);
-          gi.out_mask = 0;
-          gi.pv = 0;
-          gi.rank = 1;
-          gi.full = false;
-          for (int x = 0; x < (1 << M); ++x) gi.gx[x] = (uint64_t)((x >> (M - 1 - i)) & 1);
-          bytes += 2.0;
+      double bytes = 0.0;
+      const bool ok = group_desc<T>(pl, op, ws, j, rel, g, bytes);
+      if (ok && op.type == OP_GROUP_FEED && fc_enabled()) {
+        // producer -> consumer: the next group reads this group's output as a full input; one
+        // launch computes it tile by tile and consumes it in registers (k_gemm_fc)
+        const OpRec& nx = pl->ops[oi + 1];
+        GDesc g3;
+        double bytes3 = 0.0;
+        if (group_desc<T>(pl, nx, ws, j, rel, g3, bytes3)) {
+          int tin = -1;
+          for (int t = 0; t < g3.n; ++t)
+            if (g3.in[t].ptr == g.out) tin = t;
+          if (tin >= 0) {
+            const double tb = std::ldexp(1.0, g.out_rank);   // the never-written intermediate
+            ProfScope ps(pl, st, (bytes - tb + bytes3 - tb) * sizeof(T), op.begin, nx.end, 3, g3.out_rank);
+            ps.pr.flops = 8.0 * (std::ldexp(1.0, g.out_rank + g.M) + std::ldexp(1.0, g3.out_rank + g3.M));
+            const bool fused = try_launch_gemm_fc<T>(g, g3, tin, st);
+            ps.cancel = !fused;
+            if (fused) {
+              ++oi;
+              pl->all_launches++;
+              continue;
+            }
+          }
         }
       }
       bool launched = false;
       if (ok) {
-        ProfScope ps(pl, st, bytes * sizeof(T), op.begin, op.end, 3, Rf);
+        ProfScope ps(pl, st, bytes * sizeof(T), op.begin, op.end, 3, g.out_rank);
         launched = try_launch_gemm<T>(g, st) || try_launch_pair<T>(g, st) || try_launch_group<T>(g, st);
         ps.cancel = !launched;
       }

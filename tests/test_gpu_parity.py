@@ -280,7 +280,7 @@ def test_interpreter_only_and_big_only_agree(dtype):
 
 @pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
 @pytest.mark.parametrize("n,p,k,orderer", [(50, 2, 2, "min-fill"), (36, 3, 3, "rgreedy-fill"),
-                                           (90, 1, 2, "rgreedy-fill")])
+                                           (90, 1, 2, "rgreedy-fill"), (70, 2, 3, "rgreedy-fill")])
 def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
     # every step standalone (small_log2 = 0): reduce chains (k_chain), merge groups (k_group_t,
     # k_pair) and single steps all run at moderate widths, checked against the oracle
@@ -292,6 +292,25 @@ def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
     pre, sl, res, _ = plan.schedule()
     ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
     assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
+
+
+@pytest.mark.parametrize("n,p,k", [(36, 3, 3), (70, 2, 3)])
+def test_feed_pairs_run_fused_and_match_oracle(n, p, k):
+    """OP_GROUP_FEED: a GEMM-shaped group whose output is a full input of the next group runs as ONE
+    k_gemm_fc launch (the intermediate is never written); the contraction still matches the
+    oracle (c64 tolerance), and the fused launch is the one that ran (profile records)."""
+    g = random_regular_graph(n, 3, 7 * n + p)
+    ga, be = qaoa_angles(p, n + 1)
+    plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
+    plan.profile(True)
+    got = plan.contract(ga, be, dtype=T.TN_C64)
+    recs = plan.profile_records()
+    plan.profile(False)
+    assert any(r["kernel"] == "k_gemm_fc" for r in recs), sorted({r["kernel"] for r in recs})
+    pre, sl, res, _ = plan.schedule()
+    ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
+    assert rel(got, ref) < TOL[T.TN_C64]
+
 
 
 def test_slice_partials_vs_oracle_per_slice():
