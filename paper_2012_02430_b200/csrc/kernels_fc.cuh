@@ -15,6 +15,10 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef FC_OCC
+#define FC_OCC 2
+#endif
+
 namespace tnb {
 
 constexpr int kFcMaxV = 1;   // consumer inputs (besides T) that hold output bits
@@ -34,7 +38,7 @@ struct FArgs {
 };
 
 template <int M, int RAB, int RBB>
-__global__ void __launch_bounds__(256, (RAB + RBB >= 4 ? 1 : 2)) k_gemm_fc(const MArgs a, const FArgs f) {
+__global__ void __launch_bounds__(256, FC_OCC) k_gemm_fc(const MArgs a, const FArgs f) {
   constexpr int kThreads = 256;
   constexpr int TL = 8;                    // 5 lane bits + 3 warp bits
   constexpr int K = 1 << M, RA = 1 << RAB, RB = 1 << RBB;
@@ -92,31 +96,31 @@ __global__ void __launch_bounds__(256, (RAB + RBB >= 4 ? 1 : 2)) k_gemm_fc(const
   uint64_t obase = 0;
   for (int b = 0; b < nperm && (t0 >> b); ++b)
     if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
-  uint64_t othr = 0;
+  uint32_t othr = 0;                       // tile bits are consumer output bits (< 2^32 elements)
   uint32_t iathr = 0, ibthr = 0;
 #pragma unroll
   for (int k = 0; k < TL; ++k) {
     if ((tid >> k) & 1u) {
-      othr += 1ull << a.outbit[k];
+      othr += 1u << a.outbit[k];
       if (a.chbit[0][k] >= 0) iathr += 1u << a.chbit[0][k];
       if (a.chbit[1][k] >= 0) ibthr += 1u << a.chbit[1][k];
     }
   }
-  uint64_t ora[RA], orb[RB];
+  uint32_t ora[RA], orb[RB];
   uint32_t iar[RA], ibr[RB];
 #pragma unroll
   for (int i = 0; i < RA; ++i) {
     ora[i] = 0; iar[i] = 0;
 #pragma unroll
     for (int k = 0; k < RAB; ++k)
-      if ((i >> k) & 1) { ora[i] += 1ull << a.outbit[TL + k]; iar[i] += 1u << a.chbit[0][TL + k]; }
+      if ((i >> k) & 1) { ora[i] += 1u << a.outbit[TL + k]; iar[i] += 1u << a.chbit[0][TL + k]; }
   }
 #pragma unroll
   for (int j = 0; j < RB; ++j) {
     orb[j] = 0; ibr[j] = 0;
 #pragma unroll
     for (int k = 0; k < RBB; ++k)
-      if ((j >> k) & 1) { orb[j] += 1ull << a.outbit[TL + RAB + k]; ibr[j] += 1u << a.chbit[1][TL + RAB + k]; }
+      if ((j >> k) & 1) { orb[j] += 1u << a.outbit[TL + RAB + k]; ibr[j] += 1u << a.chbit[1][TL + RAB + k]; }
   }
   // consumer offsets of this thread's outputs (F_v additive over disjoint bits)
   uint32_t vthr[kFcMaxV], va[kFcMaxV][RA], vb[kFcMaxV][RB];
@@ -198,17 +202,6 @@ __global__ void __launch_bounds__(256, (RAB + RBB >= 4 ? 1 : 2)) k_gemm_fc(const
 #pragma unroll
       for (int v = 0; v < kFcMaxV; ++v) vcur[v] = v < f.nv ? (uint32_t)fmap(obo, f.vmask[v], f.vpv[v]) : 0u;
     }
-    // consumer factors of this tile: issued now, used after the GEMM (latency overlaps the math)
-    float2 xv[kFcMaxV][RA][RB];
-#pragma unroll
-    for (int v = 0; v < kFcMaxV; ++v)
-      if (v < f.nv) {
-        const float2* src = static_cast<const float2*>(f.vin[v]) + vcur[v] + vthr[v] + f.vgx[v][y];
-#pragma unroll
-        for (int i = 0; i < RA; ++i)
-#pragma unroll
-          for (int j = 0; j < RB; ++j) xv[v][i][j] = __ldg(src + va[v][i] + vb[v][j]);
-      }
     const float2 c3 = C3s[y];
     const bool refix = ver[1] != fixed_ver || a.c_tile_dep;
     if (refix && tid < (uint32_t)K) {
@@ -257,6 +250,17 @@ __global__ void __launch_bounds__(256, (RAB + RBB >= 4 ? 1 : 2)) k_gemm_fc(const
           asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].y, av[i].y)), "l"(f2_pack(bv[j].z, bv[j].w)));
         }
     }
+    // consumer factors of this tile (T's partner values; other warps' math covers the latency)
+    float2 xv[kFcMaxV][RA][RB];
+#pragma unroll
+    for (int v = 0; v < kFcMaxV; ++v)
+      if (v < f.nv) {
+        const float2* src = static_cast<const float2*>(f.vin[v]) + vcur[v] + vthr[v] + f.vgx[v][y];
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < RB; ++j) xv[v][i][j] = __ldg(src + va[v][i] + vb[v][j]);
+      }
     // consumer: oacc += C3_y X(o, y) T[o, y]
 #pragma unroll
     for (int i = 0; i < RA; ++i)

@@ -49,7 +49,7 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
   } else {
     if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) return false;
     const int R = g.out_rank, R3 = g3.out_rank, M3 = g3.M;
-    if (R < 11 || R > 40 || R3 < 11 || M3 < 1 || M3 > kMaxGroup || R != R3 + M3) return false;
+    if (R < 11 || R > 40 || R3 < 11 || R3 > 32 || M3 < 1 || M3 > kMaxGroup || R != R3 + M3) return false;
     // T = g.out is the consumer's input tin: full, its low R3 bits the consumer's output bits, y bit
     // k of the consumer's summed value at T bit ybit[k] >= R3
     const GIn& tIn = g3.in[tin];
