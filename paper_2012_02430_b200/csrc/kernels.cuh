@@ -1322,6 +1322,7 @@ struct ChainArgs {
   int32_t nw[kMaxChain];
   int32_t m;
   int32_t out_rank;
+  int32_t nv;       // k_chain_split: output vectors per CTA (lanes per row group), 1..32; 0 = min(32, all)
 };
 
 template <typename T>
@@ -1351,7 +1352,8 @@ __global__ void __launch_bounds__(kBucketThreads) k_chain_split(const ChainArgs 
   const T* A = static_cast<const T*>(a.A);
   T* out = static_cast<T*>(a.out);
   const uint64_t n_vec = (n_out + VEC - 1) / VEC;
-  const int nv = (int)(n_vec < 32 ? n_vec : 32);
+  const int nvmax = a.nv > 0 ? a.nv : 32;
+  const int nv = (int)(n_vec < (uint64_t)nvmax ? n_vec : (uint64_t)nvmax);
   const int ng = kBucketThreads / nv;
   const int v = threadIdx.x % nv, grp = threadIdx.x / nv;
   const int nx = 1 << a.m;
@@ -1362,7 +1364,7 @@ __global__ void __launch_bounds__(kBucketThreads) k_chain_split(const ChainArgs 
     if constexpr (VEC == 2) {
       float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
       if (o + 1 < n_out) {
-#pragma unroll 4
+#pragma unroll 8
         for (int x = x0; x < x1; ++x) {
           const float4 u = __ldcs(reinterpret_cast<const float4*>(A + o + (uint64_t)x * n_out));
           const float2 wv = reinterpret_cast<const float2&>(W[x]);

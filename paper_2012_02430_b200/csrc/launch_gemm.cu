@@ -74,9 +74,18 @@ inline int gemm_wb() {
 template <typename T>
 bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig);
 
+inline int gemm_min_m() {   // TNB_GEMM_MIN_M: groups summing fewer indices go to k_pair / k_group_t
+  static const int v = [] {
+    const char* e = std::getenv("TNB_GEMM_MIN_M");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <typename T>
 bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   static const bool contig = env_flag("TNB_GEMM_CONTIG");
+  if (g.M < gemm_min_m()) return false;
   if (std::is_same<T, float2>::value && gemm_tc_enabled() && try_launch_gemm_tc(g, st)) return true;
   return (contig && try_launch_gemm_impl<T>(g, st, true)) || try_launch_gemm_impl<T>(g, st, false);
 }

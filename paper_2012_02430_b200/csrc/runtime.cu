@@ -665,7 +665,13 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
       const uint64_t blocks = (work + kBucketThreads - 1) / kBucketThreads;
       if (blocks < (uint64_t)num_sms() * 2 && c.m >= 3) {
         // few outputs, many rows: split the rows over the threads of a CTA (k_chain_split)
-        const uint64_t nblk = std::max<uint64_t>(1, (1ull << c.out_rank) / (32ull * VEC));
+        // output vectors per CTA: enough CTAs for ~3 per SM (each thread then sums fewer rows,
+        // more loads in flight per SM); at least 8 lanes (128 contiguous bytes) per row group
+        const uint64_t n_vec = ((1ull << c.out_rank) + VEC - 1) / VEC;
+        int nv = 32;
+        while (nv > 8 && n_vec / (uint64_t)nv < 3ull * (uint64_t)num_sms()) nv >>= 1;
+        c.nv = nv;
+        const uint64_t nblk = std::max<uint64_t>(1, n_vec / (uint64_t)nv);
         const unsigned g2 = (unsigned)std::min<uint64_t>(nblk, (uint64_t)num_sms() * 8);
         k_chain_split<T><<<g2, kBucketThreads, 0, st>>>(c);
         last_kernel() = KID_CHAIN_SPLIT;
