@@ -377,7 +377,19 @@ def main():
     algo_bytes_step0 = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
     roof["path"] = {"achieved_GBps": algo_bytes_step0 / (ms_step / 1e3) / 1e9,
                     "frac": algo_bytes_step0 / (ms_step / 1e3) / 1e9 / peak,
-                    "what": "algorithmic bytes of every step of the contraction / device time per contraction"}
+                    "what": "algorithmic bytes of every launch of the contraction (fused groups: inputs + "
+                            "final output; an OP_GROUP_FEED pair: its intermediate never moves) / device "
+                            "time per contraction"}
+    # the same time against the method's own bytes: every bucket step reading its inputs and writing
+    # its output once (no fusion) -- the traffic a step-by-step contraction would need
+    bsz = 8 if dtype == T.TN_C64 else 16
+    meth = 0.0
+    for s_ in plan.steps():
+        mult = n if s_["phase"] == 1 else world
+        meth += mult * s_["bytes_c64"] * bsz / 8
+    roof["path"]["method_GB_per_step"] = meth / 1e9
+    roof["path"]["method_GBps"] = meth / (ms_step / 1e3) / 1e9
+    roof["path"]["method_frac"] = meth / (ms_step / 1e3) / 1e9 / peak
     gpu_launches = prof["all_launches"]
     algo_bytes_step = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
 

@@ -18,6 +18,9 @@
 #ifndef FC_OCC
 #define FC_OCC 2
 #endif
+#ifndef FC_XV_AT
+#define FC_XV_AT 2   // consumer loads at x = FC_XV_AT * K / 2 (0: before the GEMM, 2: after it; 0 and 1 spill at 4x4)
+#endif
 
 namespace tnb {
 
@@ -232,8 +235,22 @@ __global__ void __launch_bounds__(256, FC_OCC) k_gemm_fc(const MArgs a, const FA
     for (int i = 0; i < RA; ++i)
 #pragma unroll
       for (int j = 0; j < RB; ++j) acc[i][j] = 0ull;
+    // consumer factors of this tile (T's partner values), issued half-way through the GEMM so
+    // the second half covers their latency without holding the registers for the whole tile
+    float2 xv[kFcMaxV][RA][RB];
 #pragma unroll
     for (int x = 0; x < K; ++x) {
+      if (x == (FC_XV_AT * K) / 2) {
+#pragma unroll
+        for (int v = 0; v < kFcMaxV; ++v)
+          if (v < f.nv) {
+            const float2* src = static_cast<const float2*>(f.vin[v]) + vcur[v] + vthr[v] + f.vgx[v][y];
+#pragma unroll
+            for (int i = 0; i < RA; ++i)
+#pragma unroll
+              for (int j = 0; j < RB; ++j) xv[v][i][j] = __ldg(src + va[v][i] + vb[v][j]);
+          }
+      }
       const float2* pa = sA + ((uint32_t)a.row[0][x] << a.nch[0]);
       const float4* pb = sB + ((uint32_t)x << a.nch[1]);
       float2 av[RA];
@@ -250,17 +267,17 @@ __global__ void __launch_bounds__(256, FC_OCC) k_gemm_fc(const MArgs a, const FA
           asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].y, av[i].y)), "l"(f2_pack(bv[j].z, bv[j].w)));
         }
     }
-    // consumer factors of this tile (T's partner values; other warps' math covers the latency)
-    float2 xv[kFcMaxV][RA][RB];
+    if (FC_XV_AT == 2) {   // after the GEMM
 #pragma unroll
-    for (int v = 0; v < kFcMaxV; ++v)
-      if (v < f.nv) {
-        const float2* src = static_cast<const float2*>(f.vin[v]) + vcur[v] + vthr[v] + f.vgx[v][y];
+      for (int v = 0; v < kFcMaxV; ++v)
+        if (v < f.nv) {
+          const float2* src = static_cast<const float2*>(f.vin[v]) + vcur[v] + vthr[v] + f.vgx[v][y];
 #pragma unroll
-        for (int i = 0; i < RA; ++i)
+          for (int i = 0; i < RA; ++i)
 #pragma unroll
-          for (int j = 0; j < RB; ++j) xv[v][i][j] = __ldg(src + va[v][i] + vb[v][j]);
-      }
+            for (int j = 0; j < RB; ++j) xv[v][i][j] = __ldg(src + va[v][i] + vb[v][j]);
+        }
+    }
     // consumer: oacc += C3_y X(o, y) T[o, y]
 #pragma unroll
     for (int i = 0; i < RA; ++i)
