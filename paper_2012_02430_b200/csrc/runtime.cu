@@ -668,8 +668,10 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
         // output vectors per CTA: enough CTAs for ~3 per SM (each thread then sums fewer rows,
         // more loads in flight per SM); at least 8 lanes (128 contiguous bytes) per row group
         const uint64_t n_vec = ((1ull << c.out_rank) + VEC - 1) / VEC;
+        static const int nv_env = [] { const char* e = std::getenv("TNB_CHAIN_NV"); return e ? std::atoi(e) : 0; }();
         int nv = 32;
         while (nv > 8 && n_vec / (uint64_t)nv < 3ull * (uint64_t)num_sms()) nv >>= 1;
+        if (nv_env >= 1 && nv_env <= 32) nv = nv_env;
         c.nv = nv;
         const uint64_t nblk = std::max<uint64_t>(1, n_vec / (uint64_t)nv);
         const unsigned g2 = (unsigned)std::min<uint64_t>(nblk, (uint64_t)num_sms() * 8);

@@ -220,3 +220,43 @@ def test_open_batch_bad_arguments():
             T.build_plan(g, 1, "amplitude", "min-fill", open_qubits=bad)
     with pytest.raises(B.TnError):
         T.build_plan(g, 1, "energy", "min-fill", open_qubits=(1,))
+
+
+def _plan_env(env, g, p, k):
+    old = os.environ.get("TNB_NO_FEED")
+    try:
+        if env is None:
+            os.environ.pop("TNB_NO_FEED", None)
+        else:
+            os.environ["TNB_NO_FEED"] = env
+        return T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
+    finally:
+        if old is None:
+            os.environ.pop("TNB_NO_FEED", None)
+        else:
+            os.environ["TNB_NO_FEED"] = old
+
+
+@pytest.mark.parametrize("n,p,k", [(36, 3, 3), (70, 2, 3)])
+def test_feed_reorder_is_a_permutation_of_the_same_eliminations(n, p, k):
+    """The producer -> consumer lowering (OP_GROUP_FEED) only moves merge blocks later: the same
+    elimination steps (label, output rank, inputs) in a different execution order, the same
+    schedule and width; every moved block's consumer comes right after it; the predicted bytes
+    drop by exactly the never-written intermediates (2 x 2^R elements each)."""
+    g = random_regular_graph(n, 3, 7 * n + p)
+    a = _plan_env("1", g, p, k)      # elimination order
+    b = _plan_env(None, g, p, k)     # with the moves
+    assert a.schedule() == b.schedule()
+    assert a.width == b.width
+    sa, sb = a.steps(), b.steps()
+    key = lambda s: (s["phase"], s["label"], s["out_rank"], tuple(sorted(s["in_rank"])))
+    assert sorted(map(key, sa)) == sorted(map(key, sb))
+    assert [key(s) for s in sa if s["phase"] == 0] == [key(s) for s in sb if s["phase"] == 0]
+    moved = [i for i, (x, y) in enumerate(zip(sa, sb)) if x["label"] != y["label"]]
+    assert moved, "this instance has a producer -> consumer pair"
+    da = a.info["pred_bytes_per_slice"][0] - b.info["pred_bytes_per_slice"][0]
+    assert da > 0
+    # the saving is a sum of 2 x 8 x 2^R terms (c64): a multiple of 16 B
+    assert da % 16 == 0
+    # a plan without moves (TNB_NO_FEED=1) has no saving
+    assert a.info["pred_bytes_per_slice"][0] == _plan_env("1", g, p, k).info["pred_bytes_per_slice"][0]
