@@ -232,9 +232,16 @@ def main():
 
     import paper_2012_02430_b200 as T
 
+    # one process per GPU (torchrun); TNB_BENCH_BACKEND=gloo and local % device_count exist only for a
+    # functional check of the multi-rank path on a one-GPU box (not a measurement)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TNB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dtype = T.TN_C64 if args.dtype == "c64" else T.TN_C128
     plan, g, ga0, be0, meta = build_workload_plan(args.workload)
     info = plan.info
