@@ -54,7 +54,9 @@ def build_workload_plan(name: str = "C5a", seed: int = 0, search: bool = False):
     if not search and os.path.exists(RECIPES):
         ent = json.load(open(RECIPES)).get(name)
         if ent and ent.get("seed_graph") == seed and ent.get("best"):
-            rec = ent["best"][0]
+            # TNB_RECIPE_INDEX: another recorded candidate (plan comparisons; default the best)
+            ix = int(os.environ.get("TNB_RECIPE_INDEX", "0"))
+            rec = ent["best"][min(ix, len(ent["best"]) - 1)]
     if rec is not None:
         r = rec["recipe"]
         plan = T.build_plan(g, w.p, "amplitude", r["orderer"], n_sliced=r["n_sliced"], rg_q=r["rg_q"],

@@ -41,31 +41,37 @@ bool dispatch_fc(const MArgs& ma, const FArgs& fa, int rab, int rbb, unsigned gr
   return false;
 }
 
+#define FC_DECLINE(why)                                                                     \
+  do {                                                                                      \
+    if (env_flag("TNB_GEMM_DEBUG")) std::fprintf(stderr, "k_gemm_fc declined: %s\n", why);   \
+    return false;                                                                           \
+  } while (0)
+
 template <typename T>
 bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st) {
   if constexpr (!std::is_same<T, float2>::value) {
     (void)g; (void)g3; (void)tin; (void)st;
     return false;
   } else {
-    if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) return false;
+    if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) FC_DECLINE("producer M / inputs");
     const int R = g.out_rank, R3 = g3.out_rank, M3 = g3.M;
-    if (R < 11 || R > 40 || R3 < 11 || R3 > 32 || M3 < 1 || M3 > kMaxGroup || R != R3 + M3) return false;
+    if (R < 11 || R > 40 || R3 < 11 || R3 > 32 || M3 < 1 || M3 > kMaxGroup || R != R3 + M3) FC_DECLINE("ranks");
     // T = g.out is the consumer's input tin: full, its low R3 bits the consumer's output bits, y bit
     // k of the consumer's summed value at T bit ybit[k] >= R3
     const GIn& tIn = g3.in[tin];
-    if (tIn.out_mask != (1ull << R3) - 1 || tIn.gx[0] != 0) return false;
+    if (tIn.out_mask != (1ull << R3) - 1 || tIn.gx[0] != 0) FC_DECLINE("T not full");
     int ybit[kMaxGroup];
     for (int k = 0; k < M3; ++k) {
       const uint64_t v = tIn.gx[1u << k];
-      if (v == 0 || (v & (v - 1)) != 0) return false;
+      if (v == 0 || (v & (v - 1)) != 0) FC_DECLINE("y map");
       ybit[k] = __builtin_ctzll(v);
-      if (ybit[k] < R3 || ybit[k] >= R) return false;
+      if (ybit[k] < R3 || ybit[k] >= R) FC_DECLINE("y bits");
     }
     for (int x = 0; x < (1 << M3); ++x) {   // G_T(y) is the bit map above
       uint64_t e = 0;
       for (int k = 0; k < M3; ++k)
         if ((x >> k) & 1) e |= 1ull << ybit[k];
-      if (tIn.gx[x] != e) return false;
+      if (tIn.gx[x] != e) FC_DECLINE("y map linear");
     }
     FArgs fa;
     std::memset(&fa, 0, sizeof(fa));
@@ -75,9 +81,9 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     for (int t = 0; t < g3.n; ++t) {
       if (t == tin) continue;
       const GIn& in = g3.in[t];
-      if (in.rank > 32) return false;
+      if (in.rank > 32) FC_DECLINE("consumer rank");
       if (in.out_mask != 0) {
-        if (fa.nv >= kFcMaxV) return false;
+        if (fa.nv >= kFcMaxV) FC_DECLINE("consumer inputs");
         fa.vin[fa.nv] = in.ptr;
         fa.vmask[fa.nv] = in.out_mask;
         fa.vpv[fa.nv] = in.pv;
@@ -96,11 +102,11 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
       if (ia < 0 || r > __builtin_popcountll(g.in[ia].out_mask)) { ib = ia; ia = t; }
       else if (ib < 0 || r > __builtin_popcountll(g.in[ib].out_mask)) ib = t;
     }
-    if (g.in[ia].rank > 32 || g.in[ib].rank > 32) return false;
+    if (g.in[ia].rank > 32 || g.in[ib].rank > 32) FC_DECLINE("producer rank");
     const uint64_t full = (1ull << R) - 1;
     uint64_t ca = g.in[ia].out_mask & ~g.in[ib].out_mask, cb = g.in[ib].out_mask & ~g.in[ia].out_mask;
     const uint64_t cc = g.in[ia].out_mask & g.in[ib].out_mask, cn = full & ~(g.in[ia].out_mask | g.in[ib].out_mask);
-    if (cn & 31ull) return false;                       // lanes must be held by A or B
+    if (cn & 31ull) FC_DECLINE("lanes");   // lanes must be held by A or B
     uint64_t ymask = 0;
     for (int k = 0; k < M3; ++k) ymask |= 1ull << ybit[k];
     // B (formatted in shared memory) = the operand holding fewer y bits: the y bits flip first
@@ -114,7 +120,7 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
       if (((ca >> b) & 1) && nra < 2) ra[nra++] = b;
       if (((cb >> b) & 1) && nrb < fc_rbb()) rb[nrb++] = b;   // 4 x 4 blocks run one CTA per SM (registers)
     }
-    if (nra == 0 || nrb == 0) return false;
+    if (nra == 0 || nrb == 0) FC_DECLINE("no a / b register bits");
     uint64_t used = 31ull;
     for (int i = 0; i < nra; ++i) used |= 1ull << ra[i];
     for (int i = 0; i < nrb; ++i) used |= 1ull << rb[i];
@@ -124,11 +130,11 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
         const uint64_t cls = pass == 0 ? (ca | cb) : cc;
         if (!((used >> b) & 1) && ((cls >> b) & 1)) { wb[nw++] = b; used |= 1ull << b; }
       }
-    if (nw < 3) return false;
+    if (nw < 3) FC_DECLINE("warp bits");
     const GIn& A = g.in[ia];
     const GIn& Bq = g.in[ib];
     const int TB = 8 + nra + nrb;
-    if (R < TB + M3 || TB > kGemmMaxTB) return false;
+    if (R < TB + M3 || TB > kGemmMaxTB) FC_DECLINE("tile");
     MArgs ma;
     std::memset(&ma, 0, sizeof(ma));
     int u = 0;
@@ -140,8 +146,8 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     int nc = 0;
     for (int t = 0; t < g.n; ++t) {
       if (t == ia || t == ib) continue;
-      if (g.in[t].out_mask & tmask) return false;
-      if (g.in[t].rank > 32) return false;
+      if (g.in[t].out_mask & tmask) FC_DECLINE("constant holds a tile bit");
+      if (g.in[t].rank > 32) FC_DECLINE("constant rank");
       ma.cin[nc] = g.in[t].ptr;
       ma.cmask[nc] = g.in[t].out_mask;
       ma.cpv[nc] = g.in[t].pv;
@@ -201,7 +207,7 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     }
     ma.sm_bf_bytes = (u32 * 4 + 15) / 16 * 16;
     const size_t smem = ma.sm_bf_bytes + bf_bytes;
-    if (smem > kFcSmemBudget) return false;
+    if (smem > kFcSmemBudget) FC_DECLINE("smem");
     // traversal: the consumer's summed bits first (in the consumer's x order), then A-only bits
     // (B and B' unchanged), then B-only bits, then the rest
     // the y bits first, those held by A only before those B holds (B's chunk and B' then change
@@ -214,7 +220,7 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
         const int cls = ((cb >> b) & 1) ? 2 : ((cc >> b) & 1) ? 1 : 0;
         if (cls == pass) yo[ny++] = k;
       }
-    if (ny != M3) return false;
+    if (ny != M3) FC_DECLINE("y order");
     {
       FArgs f2 = fa;
       for (int yp = 0; yp < (1 << M3); ++yp) {
@@ -234,7 +240,7 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
         const uint64_t cls = pass == 0 ? ca : pass == 1 ? cb : (cc | cn);
         if ((cls >> b) & 1) ma.perm[np++] = (uint8_t)b;
       }
-    if (np != R - TB) return false;
+    if (np != R - TB) FC_DECLINE("perm");
     ma.out = g.out;   // not written
     ma.out_rank = R;
     if (env_flag("TNB_GEMM_DEBUG"))

@@ -1049,6 +1049,9 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   for (size_t oi = 0; oi + 1 < out.ops.size(); ++oi) {
     OpRec& a = out.ops[oi];
     const OpRec& b = out.ops[oi + 1];
+    if (std::getenv("TNB_PLAN_DEBUG") && a.phase == 1 && b.phase == 1)
+      std::fprintf(stderr, "op pair %zu: [%d,%d) type %d -> [%d,%d) type %d\n", oi, a.begin, a.end, a.type, b.begin,
+                   b.end, b.type);
     if (a.phase != 1 || b.phase != 1 || a.type != OP_GROUP || (b.type != OP_GROUP && b.type != OP_GROUP_FEED)) continue;
     const StepRec& last = out.steps[a.end - 1];
     const StepRec& head = out.steps[b.begin];
@@ -1058,6 +1061,9 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       if (head.in[t].off == last.out_off && head.in[t].out_mask == full && head.in[t].pv == (uint32_t)head.out_rank &&
           head.in[t].rank == (uint32_t)last.out_rank && (head.in[t].flags & F_REL))
         feed = true;
+    if (std::getenv("TNB_PLAN_DEBUG"))
+      std::fprintf(stderr, "feed mark: ops %zu [%d,%d) type %d -> [%d,%d) type %d: %d\n", oi, a.begin, a.end, a.type,
+                   b.begin, b.end, b.type, (int)feed);
     if (!feed) continue;
     a.type = OP_GROUP_FEED;
     const double t_elems = 2.0 * std::ldexp(1.0, last.out_rank);

@@ -294,11 +294,13 @@ def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
     assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
 
 
-@pytest.mark.parametrize("n,p,k", [(36, 3, 3), (70, 2, 3)])
-def test_feed_pairs_run_fused_and_match_oracle(n, p, k):
+@pytest.mark.parametrize("n,p,k,fused", [(36, 3, 3, True), (70, 2, 3, True), (44, 3, 3, False),
+                                          (50, 2, 2, False)])
+def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused):
     """OP_GROUP_FEED: a GEMM-shaped group whose output is a full input of the next group runs as ONE
     k_gemm_fc launch (the intermediate is never written); the contraction still matches the
-    oracle (c64 tolerance), and the fused launch is the one that ran (profile records)."""
+    oracle (c64 tolerance), and the fused launch is the one that ran (profile records).  Pairs whose
+    consumer output has fewer bits than a k_gemm_fc tile (fused=False) run as the two groups."""
     g = random_regular_graph(n, 3, 7 * n + p)
     ga, be = qaoa_angles(p, n + 1)
     plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
@@ -306,7 +308,7 @@ def test_feed_pairs_run_fused_and_match_oracle(n, p, k):
     got = plan.contract(ga, be, dtype=T.TN_C64)
     recs = plan.profile_records()
     plan.profile(False)
-    assert any(r["kernel"] == "k_gemm_fc" for r in recs), sorted({r["kernel"] for r in recs})
+    assert any(r["kernel"] == "k_gemm_fc" for r in recs) == fused, sorted({r["kernel"] for r in recs})
     pre, sl, res, _ = plan.schedule()
     ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
     assert rel(got, ref) < TOL[T.TN_C64]
