@@ -18,6 +18,9 @@
 #ifndef FC_OCC
 #define FC_OCC 2
 #endif
+#ifndef FC_PREFETCH
+#define FC_PREFETCH 0   // prefetch.global.L1 of the consumer factors: measured no gain (0.228 ms either way)
+#endif
 #ifndef FC_XV_AT
 #define FC_XV_AT 2   // consumer loads at x = FC_XV_AT * K / 2 (0: before the GEMM, 2: after it; 0 and 1 spill at 4x4)
 #endif
@@ -206,6 +209,20 @@ __global__ void __launch_bounds__(256, FC_OCC) k_gemm_fc(const MArgs a, const FA
       for (int v = 0; v < kFcMaxV; ++v) vcur[v] = v < f.nv ? (uint32_t)fmap(obo, f.vmask[v], f.vpv[v]) : 0u;
     }
     const float2 c3 = C3s[y];
+#if FC_PREFETCH
+    // the consumer factors of this tile are loaded after its GEMM: pull their lines into L1 now
+    // (no registers held; the GEMM covers the latency)
+#pragma unroll
+    for (int v = 0; v < kFcMaxV; ++v)
+      if (v < f.nv) {
+        const float2* src = static_cast<const float2*>(f.vin[v]) + vcur[v] + vthr[v] + f.vgx[v][y];
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < RB; ++j)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(src + va[v][i] + vb[v][j]));
+      }
+#endif
     const bool refix = ver[1] != fixed_ver || a.c_tile_dep;
     if (refix && tid < (uint32_t)K) {
       float2 c = make_float2(1.f, 0.f);
