@@ -460,6 +460,30 @@ def test_two_slice_lanes_match_one_lane_and_oracle(dtype):
     assert rel(plan.sum_partials(outs[1].tolist()), ref) < TOL[dtype]
 
 
+def test_slice_lanes_with_fused_pairs_match_one_lane_and_oracle():
+    """The producer -> consumer launch (k_gemm_fc) in slice lanes: 4 windows give the same partials,
+    bit for bit, as one window, and match the oracle."""
+    n, p, k = 36, 3, 3
+    g = random_regular_graph(n, 3, 7 * n + p)
+    ga, be = qaoa_angles(p, n + 1)
+    plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
+    outs = []
+    for windows in (1, 4):
+        ws = plan.workspace(T.TN_C64, batch=windows)
+        part = torch.zeros(2 * plan.n_slices, dtype=torch.float64, device="cuda")
+        plan.profile(True)
+        B.tn_contract_sliced(plan.handle, T.TN_C64, ga, be, 0, plan.n_slices, ws.data_ptr(), ws.numel(),
+                             torch.cuda.current_stream().cuda_stream, part.data_ptr())
+        torch.cuda.synchronize()
+        assert any(r["kernel"] == "k_gemm_fc" for r in plan.profile_records())
+        plan.profile(False)
+        outs.append(part.cpu())
+    assert torch.equal(outs[0], outs[1])
+    pre, sl, res, _ = plan.schedule()
+    ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
+    assert rel(plan.sum_partials(outs[1].tolist()), ref) < TOL[T.TN_C64]
+
+
 # ------------------------------------------------------------------ amplitude batches (SURVEY §8 f1)
 def _oracle_batch(n, edges, ga, be, opened, pre, sl, res):
     """Oracle batch with the plan's schedule as data: prefix once, Eq. (1) over the slices, the
