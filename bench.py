@@ -399,6 +399,9 @@ def main():
     roof["path"]["method_GB_per_step"] = meth / 1e9
     roof["path"]["method_GBps"] = meth / (ms_step / 1e3) / 1e9
     roof["path"]["method_frac"] = meth / (ms_step / 1e3) / 1e9 / peak
+    roof["path"]["method_what"] = ("bytes a step-by-step bucket elimination moves (every step reads its inputs and "
+                                   "writes its output, SURVEY 8(d) 'method bytes') / the same device time: an "
+                                   "equivalent rate, > peak because fusion avoids most of those bytes")
     gpu_launches = prof["all_launches"]
     algo_bytes_step = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
 

@@ -256,11 +256,13 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig) {
     if (smem > budget) return false;
     // traversal of the tile index: a-only bits first (B chunk and B' unchanged), then b-only, then
     // the rest
+    // (TNB_GEMM_BFIRST=1: b-only bits first -- A's chunk stays, B and B' change every tile)
+    static const bool bfirst = env_flag("TNB_GEMM_BFIRST");
     int np = 0;
     for (int pass = 0; pass < 3; ++pass)
       for (int b = 0; b < R; ++b) {
         if ((tmask >> b) & 1) continue;
-        const uint64_t cls = pass == 0 ? ca : pass == 1 ? cb : (cc | cn);
+        const uint64_t cls = pass == 0 ? (bfirst ? cb : ca) : pass == 1 ? (bfirst ? ca : cb) : (cc | cn);
         if ((cls >> b) & 1) ma.perm[np++] = (uint8_t)b;
       }
     if (np != R - TB) return false;
