@@ -227,7 +227,8 @@ tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms, d
  * them): one record per standalone launch with its plan step range, op kind (1 = single bucket
  * step, 2 = fused reduce chain, 3 = fused merge group, 4 = run of small steps in one CTA), the
  * kernel that ran it (1 = k_bucket, 2 = k_chain, 3 = k_group_t, 4 = k_pair, 5 = k_gemm,
- * 6 = k_chain_split, 7 = k_program), device milliseconds,
+ * 6 = k_chain_split, 7 = k_program, 8 = k_gemm_tc, 9 = k_gemm_fc: a producer group computed inside
+ * its consumer's launch, whose record spans both groups' steps), device milliseconds,
  * algorithmic bytes (inputs read once + output written once) and flops (8 x 2^(out_rank + M): one
  * complex multiply-add per output element and summed value).  out: host array of cap records
  * (may be NULL to query *n). */
