@@ -87,8 +87,11 @@ typedef struct {
   uint64_t launches_prefix;    /* kernel launches of the prefix */
   uint64_t launches_per_slice; /* kernel launches per slice (incl. the per-slice finalize) */
   size_t workspace_bytes[2];   /* per tn_dtype: bytes of device workspace needed by every call */
-  double pred_bytes_per_slice[2]; /* algorithmic bytes of one slice: sum over steps of
-                                     (inputs read once + output written once) x sizeof(dtype) */
+  double pred_bytes_per_slice[2]; /* algorithmic bytes of one slice: sum over launches of
+                                     (inputs read once + output written once) x sizeof(dtype); a
+                                     fused group counts its inputs and final output, a producer ->
+                                     consumer pair (OP_GROUP_FEED) not the intermediate it never
+                                     writes (tn_plan_steps gives the per-step, unfused bytes) */
   double pred_bytes_prefix[2];
   double pred_bytes_big_per_slice[2]; /* the part of pred_bytes_per_slice in standalone launches */
   uint64_t big_launches_per_slice;    /* standalone bucket-kernel launches per slice */
