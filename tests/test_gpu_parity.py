@@ -401,6 +401,28 @@ def test_c5a_full_scale_closed_forms(which):
     assert rel(got, ref) < 1e-4
 
 
+def test_c5a_full_scale_sampled_slice_vs_oracle():
+    """C5a (N=210, p=1) at the bench's plan, dtype and launch configuration (every slice, the
+    default workspace with its slice lanes, the producer -> consumer launches): slice 16 of the 32
+    against the oracle's value of that slice (complex128, the plan's schedule as data)."""
+    plan, g, ga, be, meta = _bench_plan()
+    n = plan.n_slices
+    ws = plan.workspace(T.TN_C64)
+    part = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+    plan.profile(True)
+    B.tn_contract_sliced(plan.handle, T.TN_C64, ga, be, 0, n, ws.data_ptr(), ws.numel(),
+                         torch.cuda.current_stream().cuda_stream, part.data_ptr())
+    torch.cuda.synchronize()
+    assert any(r["kernel"] == "k_gemm_fc" for r in plan.profile_records())
+    plan.profile(False)
+    j = n // 2
+    pre, sl, res, _ = plan.schedule()
+    tens = network.qaoa_amplitude_network(g.n, g.edges, ga, be)
+    _, parts = contract.contract_sliced(tens, pre, sl, res, slices=[j], return_parts=True)
+    got = complex(*part[2 * j:2 * j + 2].tolist())
+    assert rel(got, parts[0]) < TOL[T.TN_C64]
+
+
 # ------------------------------------------------------------------ batching (SURVEY §8 f1, f2)
 @pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
 def test_batched_slices_match_sequential_and_oracle(dtype):
