@@ -2,7 +2,7 @@
 O=gpurun_out/final2; mkdir -p $O
 export PATH=/usr/local/cuda/bin:$PATH
 for c in C1 C3 C4b C5a C4a C2 C5b; do
-  timeout 900 python scripts/run_configs.py --only $c --out $O/cfg_$c.json > $O/cfg_$c.log 2> $O/cfg_$c.err; echo "$c exit $?"; tail -1 $O/cfg_$c.log
+  timeout 900 python tests/run_configs.py --only $c --out $O/cfg_$c.json > $O/cfg_$c.log 2> $O/cfg_$c.err; echo "$c exit $?"; tail -1 $O/cfg_$c.log
 done
 timeout 900 python bench.py > $O/bench.log 2>&1; echo "bench exit $?"; tail -1 $O/bench.log > $O/bench_c5a.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "ncu launches exit $?"

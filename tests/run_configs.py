@@ -3,7 +3,7 @@ per config to --out (and prints a table).  Parity is always against the oracle (
 with the plan's schedule as data where the whole contraction is too big for it) and, for the
 amplitudes at full scale, against the closed forms of oracle/closed_forms.py.
 
-    python scripts/run_configs.py --out profiles/r01/configs.json [--only C1,C3]
+    python tests/run_configs.py --out profiles/r01/configs.json [--only C1,C3]
 """
 import argparse
 import json
