@@ -380,6 +380,21 @@ def test_energy_vs_oracle(dtype, n, p):
     assert 0.0 <= E <= len(g.edges)
 
 
+@pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
+@pytest.mark.parametrize("n,p,k,r", [(40, 3, 6, 2), (44, 3, 8, 4), (60, 2, 6, 3)])
+def test_multi_round_slicing_vs_oracle(dtype, n, p, k, r):
+    """Step-dependent slicing in rounds of r < n indices (reading A18: later
+    rounds' prefixes run inside every slice) -- the plans C4b / C5b use -- vs the oracle with the
+    plan's schedule as data (Eq. 1)."""
+    g = random_regular_graph(n, 3, 11 * n + p)
+    ga, be = qaoa_angles(p, n)
+    plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, r=r, rg_q=8, rg_tau=0.3)
+    assert plan.n_slices == 2 ** k
+    pre, sl, res, _ = plan.schedule()
+    ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
+    assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
+
+
 # ------------------------------------------------------------------ full-scale closed forms
 def _bench_plan():
     import bench

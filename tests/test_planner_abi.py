@@ -260,3 +260,21 @@ def test_feed_reorder_is_a_permutation_of_the_same_eliminations(n, p, k):
     assert da % 16 == 0
     # a plan without moves (TNB_NO_FEED=1) has no saving
     assert a.info["pred_bytes_per_slice"][0] == _plan_env("1", g, p, k).info["pred_bytes_per_slice"][0]
+
+
+def test_multi_round_schedule_is_exact():
+    """A plan sliced in rounds (r < n): its schedule (prefix, sliced, residual)
+    evaluated by the oracle with Eq. (1) equals the unsliced contraction, and the width does not
+    exceed the one-round plan's."""
+    n, p, k, r = 30, 3, 4, 2
+    g = random_regular_graph(n, 3, 11 * n + p)
+    ga, be = qaoa_angles(p, n)
+    plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, r=r, rg_q=8, rg_tau=0.3)
+    plan0 = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, r=0, rg_q=8, rg_tau=0.3)
+    assert plan.n_slices == 2 ** k and plan.width <= plan0.width
+    pre, sl, res, _ = plan.schedule()
+    assert len(sl) == k and len(set(pre) | set(sl) | set(res)) == len(pre) + len(sl) + len(res)
+    tens = network.qaoa_amplitude_network(n, g.edges, ga, be)
+    sliced = contract.contract_sliced(tens, pre, sl, res)
+    whole = contract.contract(tens)
+    assert abs(sliced - whole) <= 1e-12 * abs(whole)
