@@ -81,7 +81,7 @@ class Plan:
         one = B.tn_workspace_bytes(self.handle, dtype, 2) - B.tn_workspace_bytes(self.handle, dtype, 1)
         if not self.info["slices_batchable"]:
             import os
-            lanes = max(1, min(8, int(os.environ.get("TNB_LANES", "4"))))
+            lanes = max(1, min(8, int(os.environ.get("TNB_LANES", "8"))))
             lanes = 1 if os.environ.get("TNB_ONE_LANE") == "1" else lanes
             return int(max(1, min(lanes, self.n_slices, self.LANE_WINDOW_BYTES // max(1, one))))
         return int(max(1, min(self.n_slices, self.BATCH_WINDOW_BYTES // max(1, one))))
