@@ -384,6 +384,11 @@ def main():
         # timed step time) is the aggregate HBM throughput of the real run
         roof["concurrent_slice_lanes"] = lanes
     algo_bytes_step0 = (info["pred_bytes_per_slice"][dtype] * n + info["pred_bytes_prefix"][dtype] * world)
+    # the largest per-slice tensor a launch writes: a group's final output (fused groups never write
+    # the head's wider output); approximated by the largest out_rank among steps ending a launch
+    st_ = [s_ for s_ in plan.steps() if s_["phase"] == 1]
+    max_mat = max([s_["out_rank"] for i_, s_ in enumerate(st_)
+                   if i_ + 1 == len(st_) or not st_[i_ + 1]["inplace"]] or [0])
     roof["path"] = {"achieved_GBps": algo_bytes_step0 / (ms_step / 1e3) / 1e9,
                     "frac": algo_bytes_step0 / (ms_step / 1e3) / 1e9 / peak,
                     "what": "algorithmic bytes of every launch of the contraction (fused groups: inputs + "
@@ -428,8 +433,11 @@ def main():
                      "workspace_GB": info["workspace_bytes"][dtype] / 1e9},
             "plan_s": meta["plan_s"], "plan_source": meta.get("source"),
             "parallelism": f"slices x{world} (contiguous blocks, 1 NCCL all-reduce); {lanes} concurrent slice lanes per GPU",
-            "l2": "no flush needed: per-slice intermediates up to 2^%d x %d B >> 126 MB L2" % (
-                info["width"], 8 if dtype == T.TN_C64 else 16),
+            "l2": "no flush needed: every slice writes and reads intermediates of up to 2^%d x %d B "
+                  "(%.0f MB; the widest step's output is consumed in registers when fused) >> the 126 MB L2, "
+                  "and %d slices per step cycle through %.1f GB of workspace" % (
+                      max_mat, 8 if dtype == T.TN_C64 else 16, (2 ** max_mat) * (8 if dtype == T.TN_C64 else 16) / 1e6,
+                      n, info["workspace_bytes"][dtype] * lanes / 1e9),
             "algorithmic_GB_per_step": algo_bytes_step / 1e9,
             "step_GBps_algorithmic": algo_bytes_step / (ms_step / 1e3) / 1e9,
         },
