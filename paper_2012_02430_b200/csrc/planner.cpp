@@ -685,10 +685,6 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   int nA = 0;
   for (auto& ps : pend)
     if (ps.rec.phase == 0) nA++;
-  // ---- the prefix (phase A) in dependency levels: its buckets form a shallow DAG (C5a: 143
-  // steps, depth 5), so the steps of one level run side by side, one CTA each (OP_PRUN).  Phase A
-  // is stably sorted by (level, big step); the memory a level frees is released only when the
-  // level ends, so no output of a level overwrites an input another step of the level still reads.
   // ---- phase B: a merge block (a merge step and the in-place reduce steps after it) whose output
   // is a full input of a later merge step c (it holds every output bit of c and c's summed index)
   // moves down to just before c, so that the runtime can compute the block's output tile by tile
@@ -750,8 +746,16 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       syms[pend[s2].outsym].birth = s2 + 1;
     }
   }
+  // ---- the prefix (phase A) in dependency levels: its buckets form a shallow DAG (C5a: 143
+  // steps, depth 5), so the steps of one level run side by side, one CTA each (OP_PRUN).  Phase A
+  // is stably sorted by (level, big step); the memory a level frees is released only when the
+  // level ends, so no output of a level overwrites an input another step of the level still reads.
   std::vector<int> lend(nsteps + 1, 0);   // per step (new order): time at which its level ends
   std::vector<int> level(nsteps, 0);
+  // unsliced plans (k = 0, one "slice"): a phase-B run of small steps that forms a shallow DAG
+  // (C2: 62-68 steps in 3-5 levels) is level-sorted like the prefix and runs as one OP_PRUN per
+  // level; sliced plans keep their runs (slice lanes / batching already overlap them)
+  std::vector<char> parB(nsteps, 0);
   {
     std::vector<int> producer(syms.size(), -1);
     for (int si = 0; si < nsteps; ++si) producer[pend[si].outsym] = si;
@@ -772,7 +776,31 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     std::vector<PendingStep> re;
     re.reserve(nsteps);
     for (int i = 0; i < nA; ++i) { re.push_back(pend[idx[i]]); level[i] = lev[idx[i]]; }
-    for (int si = nA; si < nsteps; ++si) { re.push_back(pend[si]); level[si] = 0; }
+    {
+      int si = nA;
+      while (si < nsteps) {
+        if (k != 0 || pend[si].rec.out_rank > small_log2) {
+          level[re.size()] = 0;
+          re.push_back(pend[si]);
+          ++si;
+          continue;
+        }
+        int e = si;
+        std::map<int, int> per;
+        while (e < nsteps && pend[e].rec.out_rank <= small_log2) { per[lev[e]]++; ++e; }
+        const int len = e - si;
+        const bool go = len >= 8 && (int)per.size() * 4 <= len;
+        std::vector<int> ix;
+        for (int q = si; q < e; ++q) ix.push_back(q);
+        if (go) std::stable_sort(ix.begin(), ix.end(), [&](int a, int b) { return lev[a] < lev[b]; });
+        for (int q : ix) {
+          level[re.size()] = go ? lev[q] : 0;
+          parB[re.size()] = go ? 1 : 0;
+          re.push_back(pend[q]);
+        }
+        si = e;
+      }
+    }
     pend.swap(re);
     for (auto& sy : syms) sy.death = -1;
     for (int si = 0; si < nsteps; ++si) {
@@ -783,10 +811,25 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       int e = si;
       if (si < nA)
         while (e + 1 < nA && level[e + 1] == level[si]) ++e;
+      else if (parB[si])
+        while (e + 1 < nsteps && parB[e + 1] && level[e + 1] == level[si]) ++e;
       lend[si + 1] = e + 1;
     }
-    for (auto& sy : syms)   // phase-A inputs live until their consumer's level ends
-      if (sy.death >= 1 && sy.death <= nA) sy.death = lend[sy.death];
+    for (auto& sy : syms)   // inputs of a level-parallel step live until its level ends
+      if (sy.death >= 1 && (sy.death <= nA || parB[sy.death - 1])) sy.death = lend[sy.death];
+    if (std::getenv("TNB_PLAN_DEBUG")) {   // phase-B runs of small steps: length and depth
+      int si = nA;
+      while (si < nsteps) {
+        if (pend[si].rec.out_rank > small_log2) { ++si; continue; }
+        int e = si;
+        std::map<int, int> per;
+        while (e < nsteps && pend[e].rec.out_rank <= small_log2) { per[lev[e]]++; ++e; }
+        int wmax = 0;
+        for (auto& kv : per) wmax = std::max(wmax, kv.second);
+        std::fprintf(stderr, "phase-B run [%d,%d): %d steps, %zu levels, widest %d\n", si, e, e - si, per.size(), wmax);
+        si = e;
+      }
+    }
   }
   // lifetimes: tensors used in phase B but born before it persist across slices
   for (auto& s : syms) {
@@ -888,7 +931,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       }
       int j = i;
       while (j < nsteps && out.steps[j].phase == phase && out.steps[j].out_rank <= small_log2 &&
-             (phase == 1 || level[j] == level[i])) {
+             parB[j] == parB[i] && ((phase == 1 && !parB[i]) || level[j] == level[i])) {
         if (j > i) {
           const StepRec& s2 = out.steps[j];
           double e2 = std::ldexp(1.0, s2.out_rank);
@@ -898,7 +941,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
         ++j;
       }
       // a phase-A run lies inside one dependency level: its steps are independent (OP_PRUN)
-      out.ops.push_back(OpRec{phase == 0 ? OP_PRUN : OP_RUN, i, j, phase});
+      out.ops.push_back(OpRec{(phase == 0 || parB[i]) ? OP_PRUN : OP_RUN, i, j, phase});
       i = j;
     }
   }
