@@ -21,6 +21,12 @@ inline int fc_rbb() {   // TNB_FC_RBB = 1 (4 x 2 register blocks, 2 CTAs / SM) o
   return v;
 }
 
+inline bool fc_shrink() {   // TNB_FC_SHRINK=1: smaller blocks for small consumers (measured slower with
+                            // 8 slice lanes: C4b 52.3 vs 56.0 /s -- the lanes already fill the GPU)
+  static const bool v = env_flag("TNB_FC_SHRINK");
+  return v;
+}
+
 bool fc_enabled() {   // TNB_NO_FC=1: run producer and consumer as two launches
   static const bool off = env_flag("TNB_NO_FC");
   return !off;
@@ -37,6 +43,7 @@ template <int M>
 bool dispatch_fc(const MArgs& ma, const FArgs& fa, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
   if (rab == 2 && rbb == 2) { launch_fc<M, 2, 2>(ma, fa, grid, smem, st); return true; }
   if (rab == 2 && rbb == 1) { launch_fc<M, 2, 1>(ma, fa, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 2) { launch_fc<M, 1, 2>(ma, fa, grid, smem, st); return true; }
   if (rab == 1 && rbb == 1) { launch_fc<M, 1, 1>(ma, fa, grid, smem, st); return true; }
   return false;
 }
@@ -115,10 +122,16 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
       std::swap(ca, cb);
     }
     // register-block and warp bits: output bits of the consumer (< R3) only
+    // register blocks: 4 x 4 (TNB_FC_SHRINK=1: smaller when that leaves fewer consumer blocks than SMs)
+    int rcap_a = 2, rcap_b = fc_rbb();
+    while (rcap_a + rcap_b > 2 && R - (8 + rcap_a + rcap_b) - M3 >= 0 &&
+           (1ull << (R - (8 + rcap_a + rcap_b) - M3)) < (uint64_t)num_sms() && fc_shrink()) {
+      if (rcap_b >= rcap_a) --rcap_b; else --rcap_a;
+    }
     int ra[2], rb[2], nra = 0, nrb = 0;
     for (int b = 5; b < R3; ++b) {
-      if (((ca >> b) & 1) && nra < 2) ra[nra++] = b;
-      if (((cb >> b) & 1) && nrb < fc_rbb()) rb[nrb++] = b;   // 4 x 4 blocks run one CTA per SM (registers)
+      if (((ca >> b) & 1) && nra < rcap_a) ra[nra++] = b;
+      if (((cb >> b) & 1) && nrb < rcap_b) rb[nrb++] = b;
     }
     if (nra == 0 || nrb == 0) FC_DECLINE("no a / b register bits");
     uint64_t used = 31ull;
@@ -247,6 +260,11 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
       std::fprintf(stderr, "k_gemm_fc R=%d M=%d R3=%d M3=%d TB=%d nra=%d nrb=%d nch=(%u,%u) S=%d smem=%zu nc=%d nv=%d nw=%d\n",
                    R, g.M, R3, M3, TB, nra, nrb, ma.nch[0], ma.nch[1], ma.stages, smem, nc, fa.nv, fa.nw);
     const uint64_t groups = 1ull << (R - TB - M3);
+    static const uint64_t min_groups = [] {   // TNB_FC_MIN_GROUPS: fewer consumer blocks -> two launches
+      const char* e = std::getenv("TNB_FC_MIN_GROUPS");
+      return e ? (uint64_t)std::atoll(e) : 0ull;
+    }();
+    if (groups < min_groups) FC_DECLINE("too few consumer blocks");
     const unsigned grid = (unsigned)std::min<uint64_t>(groups, (uint64_t)num_sms() * 2);
     switch (g.M) {
       case 1: return dispatch_fc<1>(ma, fa, nra, nrb, grid, smem, st);
