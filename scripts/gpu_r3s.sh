@@ -1,0 +1,3 @@
+O=gpurun_out/r3s; mkdir -p $O
+for E in "TNB_GEMM_WS=0" "X=0" "TNB_GEMM_WS=0"; do env $E timeout 900 python bench.py --no-cpu-baseline --steps 30 > $O/b.log 2>&1; python -c "import json;d=json.loads(open('$O/b.log').read().strip().splitlines()[-1]);print('C5a $E', round(d['value'],2), d['clocks']['reasons'])"; done
+for E in "TNB_GEMM_WS=0" "X=0"; do env $E timeout 900 python bench.py --workload C4b --no-cpu-baseline --steps 20 > $O/c.log 2>&1; python -c "import json;d=json.loads(open('$O/c.log').read().strip().splitlines()[-1]);print('C4b $E', round(d['value'],2))"; done
