@@ -56,12 +56,14 @@ inline bool gemm_ra3() {
   return on;
 }
 
-// CTA size: 2^WB warps (TNB_GEMM_WB = 2 or 3); 4-warp CTAs run 4 per SM, 8-warp CTAs 2 per SM
+// preferred CTA size: 2^WB warps (TNB_GEMM_WB = 2 or 3); 4-warp CTAs run 4 per SM (half the shared
+// memory each), 8-warp CTAs 2 per SM.  Default 2 since the 8-lane / fused-pair state (C5a 88.7 vs
+// 86.7 contractions/s); a shape whose chunks do not fit the 4-warp budget takes 8-warp CTAs
 inline int gemm_wb() {
   static const int wb = [] {
     const char* v = std::getenv("TNB_GEMM_WB");
-    const int x = v ? std::atoi(v) : 3;
-    return x == 2 ? 2 : 3;
+    const int x = v ? std::atoi(v) : 2;
+    return x == 3 ? 3 : 2;
   }();
   return wb;
 }
@@ -70,7 +72,7 @@ inline int gemm_wb() {
 // register-blocked batched complex GEMM (k_gemm, c64).  Returns false when the shape does not
 // qualify (the caller then tries k_pair / k_group_t).
 template <typename T>
-bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig);
+bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB);
 
 inline int gemm_min_m() {   // TNB_GEMM_MIN_M: groups summing fewer indices go to k_pair / k_group_t
   static const int v = [] {
@@ -85,19 +87,25 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   static const bool contig = env_flag("TNB_GEMM_CONTIG");
   if (g.M < gemm_min_m()) return false;
   if (std::is_same<T, float2>::value && gemm_tc_enabled() && try_launch_gemm_tc(g, st)) return true;
-  return (contig && try_launch_gemm_impl<T>(g, st, true)) || try_launch_gemm_impl<T>(g, st, false);
+  // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
+  const int wb0 = gemm_wb(), wb1 = 5 - wb0;
+  return (contig && try_launch_gemm_impl<T>(g, st, true, wb0)) || try_launch_gemm_impl<T>(g, st, false, wb0) ||
+         try_launch_gemm_impl<T>(g, st, false, wb1);
 }
 
 template <typename T>
 bool try_launch_gemm_simt(const GDesc& g, cudaStream_t st) {
   static const bool contig = env_flag("TNB_GEMM_CONTIG");
-  return (contig && try_launch_gemm_impl<T>(g, st, true)) || try_launch_gemm_impl<T>(g, st, false);
+  // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
+  const int wb0 = gemm_wb(), wb1 = 5 - wb0;
+  return (contig && try_launch_gemm_impl<T>(g, st, true, wb0)) || try_launch_gemm_impl<T>(g, st, false, wb0) ||
+         try_launch_gemm_impl<T>(g, st, false, wb1);
 }
 
 template <typename T>
-bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig) {
+bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB) {
   if constexpr (!std::is_same<T, float2>::value) {
-    (void)g; (void)st; (void)contig;
+    (void)g; (void)st; (void)contig; (void)WB;
     return false;
   } else {
     if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) return false;
@@ -124,7 +132,6 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig) {
     uint64_t used = 31ull;
     for (int i = 0; i < nra; ++i) used |= 1ull << ra[i];
     for (int i = 0; i < nrb; ++i) used |= 1ull << rb[i];
-    const int WB = gemm_wb();
     int wb[3], nw = 0;
     // warp bits: the lowest free a/b bits (reuse), or with TNB_GEMM_CONTIG=1 the lowest free bits of
     // any class (a more contiguous tile: its 256-byte store segments closer together in HBM)
