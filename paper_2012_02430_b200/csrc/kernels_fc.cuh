@@ -43,10 +43,10 @@ struct FArgs {
   uint64_t omask;                              // (1 << R3) - 1: the o part of a T offset
 };
 
-template <int M, int RAB, int RBB>
-__global__ void __launch_bounds__(256, FC_OCC) k_gemm_fc(const MArgs a, const FArgs f) {
-  constexpr int kThreads = 256;
-  constexpr int TL = 8;                    // 5 lane bits + 3 warp bits
+template <int M, int RAB, int RBB, int WB>
+__global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_gemm_fc(const MArgs a, const FArgs f) {
+  constexpr int kThreads = 32 << WB;       // 2^WB warps: tile bits 5 .. 5 + WB - 1 on the warps
+  constexpr int TL = 5 + WB;               // 5 lane bits + WB warp bits
   constexpr int K = 1 << M, RA = 1 << RAB, RB = 1 << RBB;
   constexpr int TB = TL + RAB + RBB;
   constexpr int NB = 64 - TB;

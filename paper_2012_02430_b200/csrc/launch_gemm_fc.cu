@@ -32,20 +32,25 @@ bool fc_enabled() {   // TNB_NO_FC=1: run producer and consumer as two launches
   return !off;
 }
 
-template <int M, int RAB, int RBB>
+template <int M, int RAB, int RBB, int WB>
 void launch_fc(const MArgs& ma, const FArgs& fa, unsigned grid, size_t smem, cudaStream_t st) {
-  allow_smem(k_gemm_fc<M, RAB, RBB>, smem);
+  allow_smem(k_gemm_fc<M, RAB, RBB, WB>, smem);
   last_kernel() = KID_GEMM_FC;
-  k_gemm_fc<M, RAB, RBB><<<grid, 256, smem, st>>>(ma, fa);
+  k_gemm_fc<M, RAB, RBB, WB><<<grid, 32 << WB, smem, st>>>(ma, fa);
 }
 
-template <int M>
+template <int M, int WB>
 bool dispatch_fc(const MArgs& ma, const FArgs& fa, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
-  if (rab == 2 && rbb == 2) { launch_fc<M, 2, 2>(ma, fa, grid, smem, st); return true; }
-  if (rab == 2 && rbb == 1) { launch_fc<M, 2, 1>(ma, fa, grid, smem, st); return true; }
-  if (rab == 1 && rbb == 2) { launch_fc<M, 1, 2>(ma, fa, grid, smem, st); return true; }
-  if (rab == 1 && rbb == 1) { launch_fc<M, 1, 1>(ma, fa, grid, smem, st); return true; }
+  if (rab == 2 && rbb == 2) { launch_fc<M, 2, 2, WB>(ma, fa, grid, smem, st); return true; }
+  if (rab == 2 && rbb == 1) { launch_fc<M, 2, 1, WB>(ma, fa, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 2) { launch_fc<M, 1, 2, WB>(ma, fa, grid, smem, st); return true; }
+  if (rab == 1 && rbb == 1) { launch_fc<M, 1, 1, WB>(ma, fa, grid, smem, st); return true; }
   return false;
+}
+
+inline int fc_wb() {   // TNB_FC_WB = 2 (4-warp CTAs, 4 per SM) or 3 (8-warp CTAs, 2 per SM)
+  static const int v = [] { const char* e = std::getenv("TNB_FC_WB"); return e && e[0] == '2' ? 2 : 3; }();
+  return v;
 }
 
 #define FC_DECLINE(why)                                                                     \
@@ -55,9 +60,18 @@ bool dispatch_fc(const MArgs& ma, const FArgs& fa, int rab, int rbb, unsigned gr
   } while (0)
 
 template <typename T>
+bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, int WB);
+
+template <typename T>
 bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st) {
+  const int wb0 = fc_wb();
+  return try_launch_gemm_fc_wb<T>(g, g3, tin, st, wb0) || try_launch_gemm_fc_wb<T>(g, g3, tin, st, 5 - wb0);
+}
+
+template <typename T>
+bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, int WB) {
   if constexpr (!std::is_same<T, float2>::value) {
-    (void)g; (void)g3; (void)tin; (void)st;
+    (void)g; (void)g3; (void)tin; (void)st; (void)WB;
     return false;
   } else {
     if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) FC_DECLINE("producer M / inputs");
@@ -124,8 +138,8 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     // register-block and warp bits: output bits of the consumer (< R3) only
     // register blocks: 4 x 4 (TNB_FC_SHRINK=1: smaller when that leaves fewer consumer blocks than SMs)
     int rcap_a = 2, rcap_b = fc_rbb();
-    while (rcap_a + rcap_b > 2 && R - (8 + rcap_a + rcap_b) - M3 >= 0 &&
-           (1ull << (R - (8 + rcap_a + rcap_b) - M3)) < (uint64_t)num_sms() && fc_shrink()) {
+    while (rcap_a + rcap_b > 2 && R - (5 + WB + rcap_a + rcap_b) - M3 >= 0 &&
+           (1ull << (R - (5 + WB + rcap_a + rcap_b) - M3)) < (uint64_t)num_sms() && fc_shrink()) {
       if (rcap_b >= rcap_a) --rcap_b; else --rcap_a;
     }
     int ra[2], rb[2], nra = 0, nrb = 0;
@@ -138,21 +152,21 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     for (int i = 0; i < nra; ++i) used |= 1ull << ra[i];
     for (int i = 0; i < nrb; ++i) used |= 1ull << rb[i];
     int wb[3], nw = 0;
-    for (int pass = 0; pass < 2 && nw < 3; ++pass)
-      for (int b = 5; b < R3 && nw < 3; ++b) {
+    for (int pass = 0; pass < 2 && nw < WB; ++pass)
+      for (int b = 5; b < R3 && nw < WB; ++b) {
         const uint64_t cls = pass == 0 ? (ca | cb) : cc;
         if (!((used >> b) & 1) && ((cls >> b) & 1)) { wb[nw++] = b; used |= 1ull << b; }
       }
-    if (nw < 3) FC_DECLINE("warp bits");
+    if (nw < WB) FC_DECLINE("warp bits");
     const GIn& A = g.in[ia];
     const GIn& Bq = g.in[ib];
-    const int TB = 8 + nra + nrb;
+    const int TB = 5 + WB + nra + nrb;
     if (R < TB + M3 || TB > kGemmMaxTB) FC_DECLINE("tile");
     MArgs ma;
     std::memset(&ma, 0, sizeof(ma));
     int u = 0;
     for (int b = 0; b < 5; ++b) ma.outbit[u++] = (uint8_t)b;
-    for (int i = 0; i < 3; ++i) ma.outbit[u++] = (uint8_t)wb[i];
+    for (int i = 0; i < WB; ++i) ma.outbit[u++] = (uint8_t)wb[i];
     for (int i = 0; i < nra; ++i) ma.outbit[u++] = (uint8_t)ra[i];
     for (int i = 0; i < nrb; ++i) ma.outbit[u++] = (uint8_t)rb[i];
     const uint64_t tmask = used;
@@ -207,7 +221,8 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     const uint32_t dep_u32 = (ma.nrows[0] << (ma.nch[0] - ma.lv[0])) + (ma.nrows[1] << (ma.nch[1] - ma.lv[1]));
     const size_t bf_bytes = ((size_t)16 << g.M) << ma.nch[1];
     int S = gemm_stages();
-    while (S > 2 && ((size_t)S * (sz[0] + sz[1]) * 8 + dep_u32 * 4 + bf_bytes + 16) > kFcSmemBudget) --S;
+    const size_t budget = WB == 3 ? kFcSmemBudget : kFcSmemBudget / 2;   // 2 or 4 CTAs per SM
+    while (S > 2 && ((size_t)S * (sz[0] + sz[1]) * 8 + dep_u32 * 4 + bf_bytes + 16) > budget) --S;
     ma.stages = S;
     for (int k = 0; k < S; ++k) {
       ma.sm_in[0][k] = k * sz[0];
@@ -220,7 +235,7 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
     }
     ma.sm_bf_bytes = (u32 * 4 + 15) / 16 * 16;
     const size_t smem = ma.sm_bf_bytes + bf_bytes;
-    if (smem > kFcSmemBudget) FC_DECLINE("smem");
+    if (smem > budget) FC_DECLINE("smem");
     // traversal: the consumer's summed bits first (in the consumer's x order), then A-only bits
     // (B and B' unchanged), then B-only bits, then the rest
     // the y bits first, those held by A only before those B holds (B's chunk and B' then change
@@ -265,19 +280,21 @@ bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t s
       return e ? (uint64_t)std::atoll(e) : 0ull;
     }();
     if (groups < min_groups) FC_DECLINE("too few consumer blocks");
-    const unsigned grid = (unsigned)std::min<uint64_t>(groups, (uint64_t)num_sms() * 2);
+    const unsigned grid = (unsigned)std::min<uint64_t>(groups, (uint64_t)num_sms() * (WB == 3 ? 2 : 4));
     switch (g.M) {
-      case 1: return dispatch_fc<1>(ma, fa, nra, nrb, grid, smem, st);
-      case 2: return dispatch_fc<2>(ma, fa, nra, nrb, grid, smem, st);
-      case 3: return dispatch_fc<3>(ma, fa, nra, nrb, grid, smem, st);
-      case 4: return dispatch_fc<4>(ma, fa, nra, nrb, grid, smem, st);
-      case 5: return dispatch_fc<5>(ma, fa, nra, nrb, grid, smem, st);
+      case 1: return WB == 3 ? dispatch_fc<1, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<1, 2>(ma, fa, nra, nrb, grid, smem, st);
+      case 2: return WB == 3 ? dispatch_fc<2, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<2, 2>(ma, fa, nra, nrb, grid, smem, st);
+      case 3: return WB == 3 ? dispatch_fc<3, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<3, 2>(ma, fa, nra, nrb, grid, smem, st);
+      case 4: return WB == 3 ? dispatch_fc<4, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<4, 2>(ma, fa, nra, nrb, grid, smem, st);
+      case 5: return WB == 3 ? dispatch_fc<5, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<5, 2>(ma, fa, nra, nrb, grid, smem, st);
       default: return false;
     }
   }
 }
 
 template bool try_launch_gemm_fc<float2>(const GDesc&, const GDesc&, int, cudaStream_t);
+template bool try_launch_gemm_fc_wb<float2>(const GDesc&, const GDesc&, int, cudaStream_t, int);
+template bool try_launch_gemm_fc_wb<double2>(const GDesc&, const GDesc&, int, cudaStream_t, int);
 template bool try_launch_gemm_fc<double2>(const GDesc&, const GDesc&, int, cudaStream_t);
 
 }  // namespace tnb
