@@ -11,25 +11,30 @@
 #include <map>
 #include <mutex>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "kernels.cuh"
 
 namespace tnb {
 
-// opt in to more than 48 KB of (static + dynamic) shared memory, once per kernel instantiation
+// opt in to more than 48 KB of (static + dynamic) shared memory, once per (device, kernel
+// instantiation): cudaFuncSetAttribute applies to the current device
 template <typename K>
 inline void allow_smem(K kernel, size_t dyn) {
   static std::mutex mu;
-  static std::map<const void*, size_t> granted;   // per kernel (per device is not needed: the
-                                                   // attribute is a function property)
+  static std::map<std::pair<int, const void*>, size_t> granted;
   if (dyn + 16 * 1024 <= 48 * 1024) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  size_t& g = granted[reinterpret_cast<const void*>(kernel)];
+  size_t& g = granted[{dev, reinterpret_cast<const void*>(kernel)}];
   if (dyn > g) {
     const size_t want = std::max<size_t>(dyn, 100 * 1024);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
-    g = want;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want) == cudaSuccess)
+      g = want;
+    else
+      (void)cudaGetLastError();   // the launch then fails and reports the error
   }
 }
 

@@ -682,6 +682,11 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
   }
   const int nsteps = (int)pend.size();
   const int T_end = nsteps + 1;
+  struct FeedPair {
+    int consumer_out;         // output sym of the consumer step c
+    std::vector<int> inputs;  // syms the producer block reads (not its in-place chain)
+  };
+  std::vector<FeedPair> feed_pairs;
   int nA = 0;
   for (auto& ps : pend)
     if (ps.rec.phase == 0) nA++;
@@ -698,6 +703,7 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       for (int id : pend[si].ins) consumer[id] = si;
     std::vector<std::vector<std::pair<int, int>>> attach(nsteps);   // blocks emitted right before c
     std::vector<char> moved(nsteps, 0);
+    feed_pairs.clear();
     int si = nA;
     while (si < nsteps) {
       if (pend[si].rec.inplace) { ++si; continue; }
@@ -722,6 +728,14 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
       if (ok) {
         attach[c].push_back({si, e});
         for (int k2 = si; k2 < e; ++k2) moved[k2] = 1;
+        // the fused launch reads the block's inputs while it writes c's output: they must stay
+        // allocated until c (see the lifetime extension before the arena)
+        FeedPair fp;
+        fp.consumer_out = pend[c].outsym;
+        for (int k2 = si; k2 < e; ++k2)
+          for (size_t t2 = 0; t2 < pend[k2].ins.size(); ++t2)
+            if (!(k2 > si && t2 == 0 && pend[k2].rec.inplace)) fp.inputs.push_back(pend[k2].ins[t2]);
+        feed_pairs.push_back(fp);
       }
       si = e;
     }
@@ -829,6 +843,18 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
         std::fprintf(stderr, "phase-B run [%d,%d): %d steps, %zu levels, widest %d\n", si, e, e - si, per.size(), wmax);
         si = e;
       }
+    }
+  }
+  // producer -> consumer candidates (OP_GROUP_FEED): every input of the producer block lives until
+  // the consumer step, so the first-fit arena never places the consumer's output over memory the
+  // fused launch (k_gemm_fc) still reads in other CTAs
+  {
+    std::vector<int> at(syms.size(), -1);
+    for (int si = 0; si < nsteps; ++si) at[pend[si].outsym] = si;
+    for (const auto& fp : feed_pairs) {
+      const int c = at[fp.consumer_out];
+      if (c < 0) continue;
+      for (int id : fp.inputs) syms[id].death = std::max(syms[id].death, c + 1);
     }
   }
   // lifetimes: tensors used in phase B but born before it persist across slices
@@ -1107,6 +1133,22 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
     if (std::getenv("TNB_PLAN_DEBUG"))
       std::fprintf(stderr, "feed mark: ops %zu [%d,%d) type %d -> [%d,%d) type %d: %d\n", oi, a.begin, a.end, a.type,
                    b.begin, b.end, b.type, (int)feed);
+    // the fused launch reads every producer input while other CTAs write the consumer's output:
+    // an in-place producer head (its output aliases its own input) or any overlap of the
+    // consumer's output with a producer input rules the pair out
+    if (feed && out.steps[a.begin].inplace) feed = false;
+    if (feed) {
+      const uint64_t olo = head.out_off, ohi = head.out_off + align_up(1ull << head.out_rank);
+      for (int si2 = a.begin; si2 < a.end && feed; ++si2) {
+        const StepRec& st2 = out.steps[si2];
+        for (int t = 0; t < st2.n_in; ++t) {
+          if (si2 > a.begin && t == 0 && st2.inplace) continue;   // the producer's own chain
+          const InRec& in = st2.in[t];
+          const uint64_t ilo = in.off, ihi = in.off + align_up(1ull << (in.rank + popc(in.slice_mask)));
+          if (ilo < ohi && olo < ihi) feed = false;
+        }
+      }
+    }
     if (!feed) continue;
     a.type = OP_GROUP_FEED;
     const double t_elems = 2.0 * std::ldexp(1.0, last.out_rank);

@@ -814,6 +814,19 @@ tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int 
     CU(cudaEventRecord(dt->ev_fork, st));
     for (uint64_t l = 1; l < L; ++l) CU(cudaStreamWaitEvent(dt->side[l - 1], dt->ev_fork, 0));
   }
+  // every forked side lane joins back into the caller's stream on every exit path, so the caller
+  // never reuses ws / partials while a side lane still runs (also after an error)
+  struct JoinLanes {
+    DevTables* dt;
+    cudaStream_t st;
+    uint64_t L;
+    ~JoinLanes() {
+      for (uint64_t l = 1; l < L; ++l) {
+        cudaEventRecord(dt->ev_join[l - 1], dt->side[l - 1]);
+        cudaStreamWaitEvent(st, dt->ev_join[l - 1], 0);
+      }
+    }
+  } join{dt, st, L};
   for (uint64_t j = begin; j < end; ++j) {
     const uint64_t lane = L >= 2 ? (j - begin) % L : 0;
     cudaStream_t sj = lane ? dt->side[lane - 1] : st;
@@ -825,10 +838,6 @@ tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int 
                                                     partials_dev + 2 * (j << pl->h.n_open), rel, pl->h.n_open);
     }
     pl->all_launches++;
-  }
-  for (uint64_t l = 1; l < L; ++l) {
-    CU(cudaEventRecord(dt->ev_join[l - 1], dt->side[l - 1]));
-    CU(cudaStreamWaitEvent(st, dt->ev_join[l - 1], 0));
   }
   CU(cudaGetLastError());
   return TN_OK;

@@ -39,9 +39,17 @@ def run_sliced(plan, gammas, betas, dtype: int = 0, group=None, device=None,
     begin, end = slice_block(n, rank, world)
     if compute is None:
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        partials = torch.zeros(2 * n * getattr(plan, "batch", 1), dtype=torch.float64, device=dev)
-        if end > begin:
-            plan.contract_sliced(gammas, betas, begin, end, partials, dtype=dtype, stream=stream)
+        cur = torch.cuda.current_stream(dev)
+        s = cur if stream is None else stream
+        if s != cur:
+            s.wait_stream(cur)          # inputs / earlier work of the caller's stream come first
+        with torch.cuda.stream(s):      # zero-fill and contraction on the same stream
+            partials = torch.zeros(2 * n * getattr(plan, "batch", 1), dtype=torch.float64, device=dev)
+            if end > begin:
+                plan.contract_sliced(gammas, betas, begin, end, partials, dtype=dtype, stream=s)
+        if s != cur:
+            cur.wait_stream(s)          # the all-reduce and the host copy run on the current stream
+            partials.record_stream(cur)
     else:
         dev = torch.device("cpu") if device is None else torch.device(device)
         partials = torch.zeros(2 * n * getattr(plan, "batch", 1), dtype=torch.float64, device=dev)

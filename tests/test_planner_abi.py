@@ -278,3 +278,25 @@ def test_multi_round_schedule_is_exact():
     sliced = contract.contract_sliced(tens, pre, sl, res)
     whole = contract.contract(tens)
     assert abs(sliced - whole) <= 1e-12 * abs(whole)
+
+
+# instances where the first-fit arena / in-place chains used to put a fused pair's consumer output
+# over memory the producer still reads: N, seed, p, k, orderer
+_FEED_CASES = [(40, 2, 2, 0, "min-degree"), (60, 0, 2, 0, "min-degree"), (60, 1, 2, 3, "min-degree"),
+               (60, 3, 2, 3, "min-fill"), (80, 2, 2, 3, "min-fill"), (80, 3, 2, 6, "min-fill"),
+               (100, 1, 2, 6, "min-fill"), (150, 2, 1, 6, "min-degree"), (210, 0, 1, 5, "min-fill")]
+
+
+def test_fused_pairs_never_write_over_producer_inputs():
+    """OP_GROUP_FEED (k_gemm_fc) runs producer and consumer in ONE launch: no producer input may
+    share arena memory with the consumer's output (cross-CTA write-after-read race)."""
+    import planbuf
+
+    n_feed = 0
+    for n, seed, p, k, o in _FEED_CASES:
+        pl = T.build_plan(random_regular_graph(n, 3, seed), p, "amplitude", o, n_sliced=k)
+        P = planbuf.parse(pl.buf)
+        assert P["header"].magic == 0x32424E54 and P["header"].n_steps == len(P["steps"])
+        n_feed += sum(1 for op in P["ops"] if op.type == planbuf.OP_GROUP_FEED)
+        assert planbuf.feed_overlaps(pl.buf) == [], (n, seed, p, k, o)
+    assert n_feed > 0
