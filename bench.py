@@ -31,8 +31,8 @@ if ROOT not in sys.path:
 
 from tn_inputs import WORKLOADS, qaoa_angles, random_regular_graph  # noqa: E402
 
-MAX_WIDTH = {"C4a": 30, "C4b": 30, "C5a": 32, "C5b": 32, "C2": 62}
-K_RANGE = {"C4a": (8, 12), "C4b": (8, 12), "C5a": (5, 8), "C5b": (8, 16), "C2": (0, 0)}
+MAX_WIDTH = {"C4a": 30, "C4b": 30, "C5a": 32, "C5b": 32, "C2": 62, "C5r": 32, "C5r6": 33}
+K_RANGE = {"C4a": (8, 12), "C4b": (8, 12), "C5a": (5, 8), "C5b": (8, 16), "C2": (0, 0), "C5r": (9, 9), "C5r6": (6, 6)}
 METRIC = "sliced single-amplitude contraction throughput (QAOA MaxCut, 3-regular)"
 
 

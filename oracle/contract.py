@@ -211,3 +211,109 @@ def brute_force(tensors: Sequence[Tensor]) -> complex:
         args.append([local[l] for l in ls])
     args.append([])
     return complex(np.einsum(*args, optimize=False))
+
+
+# ------------------------------------------------------------------ sub-slicing (host RAM bound)
+def subslice_labels(tensors: Sequence[Tensor], order: Sequence[int], max_width: int) -> List[int]:
+    """Labels to fix in addition, so that bucket elimination of `tensors` along `order` (minus
+    the fixed labels) has width <= max_width -- Eq. (1) applied once more, which is exact
+    ("when host RAM is short it sub-slices further").
+    Greedy, the oracle's own rule: while too wide, fix the label that occurs in the neighbourhoods
+    of the widest steps with the largest total weight sum 2^degree (ties -> smaller label)."""
+    extra: List[int] = []
+    while True:
+        fixed = fix_indices(tensors, {l: 0 for l in extra})
+        adj = line_graph(fixed)
+        steps = []
+        for v in order:
+            if v in extra or v not in adj:
+                continue
+            steps.append((len(adj[v]), set(adj[v])))
+            eliminate_vertex(adj, v)
+        w = max((d for d, _ in steps), default=0)
+        if w <= max_width:
+            return extra
+        cnt: Dict[int, float] = {}
+        for d, nb in steps:
+            if d >= w - 1:
+                for u in nb:
+                    cnt[u] = cnt.get(u, 0.0) + 2.0 ** d
+        extra.append(max(cnt, key=lambda u: (cnt[u], -u)))
+
+
+def subslice_value(tensors: Sequence[Tensor], order: Sequence[int], extra: Sequence[int], i: int) -> complex:
+    """Sub-slice i: the labels of `extra` fixed to the bits of i (bit b = b-th label ascending),
+    then bucket elimination along `order` without them."""
+    fixed = fix_indices(tensors, slice_assignment(extra, i))
+    ex = set(extra)
+    return bucket_eliminate(fixed, [l for l in order if l not in ex])
+
+
+def contract_subsliced(tensors: Sequence[Tensor], order: Sequence[int], extra: Sequence[int],
+                       workers: int = 1, ids: Sequence[int] | None = None) -> complex:
+    """sum over the 2^m sub-slices (fixed pairwise tree over the sub-slice id), each evaluated by
+    subslice_value -- in `workers` forked processes (independent sums; the value and its rounding
+    do not depend on the worker count).  `ids`: a subset (the caller sums it)."""
+    ids = list(range(1 << len(extra))) if ids is None else list(ids)
+    return pairwise_sum(map_subslices(tensors, order, extra, ids, workers))
+
+
+_POOL_STATE = None
+
+
+def _pool_eval(i):
+    t, o, e = _POOL_STATE
+    return subslice_value(t, o, e, i)
+
+
+def map_subslices(tensors, order, extra, ids, workers: int = 1) -> List[complex]:
+    """[subslice_value(i) for i in ids], optionally over a fork-based process pool (the tensors are
+    inherited by the workers, not pickled)."""
+    global _POOL_STATE
+    ids = list(ids)
+    if workers <= 1 or len(ids) <= 1:
+        return [subslice_value(tensors, order, extra, i) for i in ids]
+    import multiprocessing as mp
+
+    _POOL_STATE = (tensors, order, list(extra))
+    try:
+        with mp.get_context("fork").Pool(min(workers, len(ids))) as pool:
+            return pool.map(_pool_eval, ids, chunksize=1)
+    finally:
+        _POOL_STATE = None
+
+
+def _pool_slice_task(task):
+    rest, sliced, residual, extra = _POOL_STATE
+    j, i = task
+    return subslice_value(fix_indices(rest, slice_assignment(sliced, j)), residual, extra, i)
+
+
+def slice_values(tensors: Sequence[Tensor], prefix: Sequence[int], sliced: Sequence[int],
+                 residual: Sequence[int], slices: Iterable[int], max_width: int | None = None,
+                 workers: int = 1):
+    """Per-slice results of Eq. (1) with a shared prefix (as contract_sliced), each slice
+    optionally sub-sliced to max_width (subslice_labels on slice 0's network; every slice has the
+    same structure) and the (slice, sub-slice) evaluations spread over `workers` forked processes.
+    Returns (values in the order of `slices`, extra labels)."""
+    global _POOL_STATE
+    rest, pscalar = partial_eliminate(tensors, prefix)
+    js = list(slices)
+    extra: List[int] = []
+    if max_width is not None and js:
+        extra = subslice_labels(fix_indices(rest, slice_assignment(sliced, js[0])), residual, max_width)
+    m = len(extra)
+    tasks = [(j, i) for j in js for i in range(1 << m)]
+    _POOL_STATE = (rest, list(sliced), list(residual), extra)
+    try:
+        if workers <= 1 or len(tasks) <= 1:
+            flat = [_pool_slice_task(t) for t in tasks]
+        else:
+            import multiprocessing as mp
+
+            with mp.get_context("fork").Pool(min(workers, len(tasks))) as pool:
+                flat = pool.map(_pool_slice_task, tasks, chunksize=1)
+    finally:
+        _POOL_STATE = None
+    vals = [pscalar * pairwise_sum(flat[a << m:(a + 1) << m]) for a in range(len(js))]
+    return vals, extra

@@ -288,3 +288,40 @@ def test_greedy_examples():
     path = [(np.ones((2, 2)), (a, a + 1)) for a in range(3)] + [(one, (0,))]
     _, d = contract.greedy_min_degree(path)
     assert max(d) == 1
+
+
+@pytest.mark.parametrize("n,p,seed,maxw", [(14, 2, 3, 4), (16, 3, 1, 6)])
+def test_subsliced_contraction_vs_statevector(n, p, seed, maxw):
+    """Sub-slicing (Eq. 1 applied once more): the chosen extra labels bring
+    the width down to max_width, and the pairwise sum over the 2^m sub-slices -- serial and over a
+    process pool -- equals the 2^N state-vector amplitude (independent of the oracle's network)."""
+    g = random_regular_graph(n, 3, seed)
+    ga, be = qaoa_angles(p, seed)
+    t = network.qaoa_amplitude_network(n, g.edges, ga, be)
+    order, degs = contract.greedy_min_degree(t)
+    extra = contract.subslice_labels(t, order, maxw)
+    assert len(extra) >= 2 and max(degs) > maxw
+    rest = [l for l in order if l not in set(extra)]
+    assert max(contract.width_of_order(network.fix_indices(t, {l: 0 for l in extra}), rest)) <= maxw
+    ref = sv.amplitude(sv.qaoa_state(n, g.edges, ga, be))
+    serial = contract.contract_subsliced(t, order, extra, workers=1)
+    pooled = contract.contract_subsliced(t, order, extra, workers=3)
+    assert abs(serial - ref) < 1e-12 * max(1.0, abs(ref)) + 1e-14
+    assert pooled == serial        # same sums in the same fixed tree: bit-identical
+
+
+def test_slice_values_pool_matches_contract_sliced():
+    """slice_values (prefix once, per-slice sub-slicing, process pool) gives the same per-slice
+    values as the plain contract_sliced, and their pairwise sum is the state-vector amplitude."""
+    n, p = 16, 2
+    g = random_regular_graph(n, 3, 5)
+    ga, be = qaoa_angles(p, 5)
+    t = network.qaoa_amplitude_network(n, g.edges, ga, be)
+    order, _ = contract.greedy_min_degree(t)
+    pre, sl, res = order[:6], sorted(order[6:9]), order[9:]
+    tot, parts = contract.contract_sliced(t, pre, sl, res, return_parts=True)
+    vals, extra = contract.slice_values(t, pre, sl, res, range(8), max_width=3, workers=4)
+    assert len(extra) >= 1
+    for a, b in zip(vals, parts):
+        assert abs(a - b) < 1e-13
+    assert abs(contract.pairwise_sum(vals) - sv.amplitude(sv.qaoa_state(n, g.edges, ga, be))) < 1e-12

@@ -153,6 +153,10 @@ WORKLOADS = {
     "C4b": Workload("C4b", 64, 3, "amplitude", note="sliced, width<=30 (p=3 companion)"),
     "C5a": Workload("C5a", 210, 1, "amplitude", note="paper's 210-qubit 1,785-gate circuit, width<=32"),
     "C5b": Workload("C5b", 70, 3, "amplitude", note="p=3 companion with 210 live indices, width<=32"),
+    # the paper's own plan for the 210-qubit circuit (greedy min-degree, r = n):
+    # k = 9 (width 30 on this instance) and k = 6 (width 33: over the 2^32 cap, reported only)
+    "C5r": Workload("C5r", 210, 1, "amplitude", note="paper-replica plan: min-degree, k=9, r=n"),
+    "C5r6": Workload("C5r6", 210, 1, "amplitude", note="paper-replica plan: min-degree, k=6, r=n"),
 }
 
 
