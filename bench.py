@@ -156,60 +156,98 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------------- oracle sample
-def oracle_sample(plan, g, ga, be, budget_s: float = 15.0, max_width: int = 22):
-    """Time the oracle (as it stands) on a bounded sample of the same contraction and scale it
-    to contractions/s.  The sample: the shared prefix, then slice 0 of the plan with the plan's
-    residual order as data, further sub-sliced (Eq. 1, exact) on the m indices that appear in the
-    most of the widest intermediates, until the width is <= max_width; as many sub-slices as fit
-    in `budget_s` are contracted; cost = prefix time + mean sub-slice time x 2^(k+m)."""
+# ---------------------------------------------------------------------------- oracle timing
+SCHEDULES = os.path.join(ROOT, "tests", "golden", "schedules.json")
+
+
+def host_info() -> dict:
+    """CPU model, logical cores and the cores this process may use."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": os.cpu_count(), "usable_cores": usable}
+
+
+def committed_schedule(name: str) -> dict:
+    """The workload's schedule as DATA (tests/golden/schedules.json, scripts/dump_schedules.py):
+    the oracle arm reads it instead of calling the product planner."""
+    with open(SCHEDULES) as f:
+        return json.load(f)[name]
+
+
+def oracle_contraction(name: str, ga, be, slices=None, workers: int = 1, max_width: int = 22,
+                       sched: dict | None = None):
+    """The oracle (as it stands: complex128 numpy.einsum per bucket, oracle/contract.py) on the
+    workload's committed schedule: prefix once, then the given slices (default: all 2^k), each
+    sub-sliced exactly (Eq. 1) to max_width, the (slice, sub-slice) evaluations spread over
+    `workers` processes.  Returns (sum of the slice values, seconds, n_slices run, sub-slices per
+    slice)."""
     from oracle import contract, network
 
-    pre, sl, res, _ = plan.schedule()
+    s = committed_schedule(name) if sched is None else sched
+    if s["k"] == 0 and "oracle_aux" in s:
+        s = s["oracle_aux"]
+    g = random_regular_graph(WORKLOADS[name].n, 3, 0)
+    n_sl = 1 << len(s["sliced"])
+    js = list(range(n_sl)) if slices is None else list(slices)
     t0 = time.perf_counter()
     tens = network.qaoa_amplitude_network(g.n, g.edges, ga, be)
-    rest, _ = contract.partial_eliminate(tens, pre)
-    t_prefix = time.perf_counter() - t0
-    rest0 = network.fix_indices(rest, contract.slice_assignment(sl, 0))
-    extra = []
-    while True:
-        fixed = network.fix_indices(rest0, {l: 0 for l in extra})
-        order = [l for l in res if l not in extra]
-        adj = contract.line_graph(fixed)
-        steps = []
-        for v in order:
-            if v in adj:
-                steps.append((len(adj[v]), set(adj[v])))
-                contract.eliminate_vertex(adj, v)
-        w = max((d for d, _ in steps), default=0)
-        if w <= max_width:
-            break
-        cnt = {}
-        for d, nb in steps:
-            if d >= w - 1:
-                for u in nb:
-                    cnt[u] = cnt.get(u, 0) + 2.0 ** d
-        extra.append(max(cnt, key=lambda u: (cnt[u], -u)))
-    m = len(extra)
-    times = []
-    t_start = time.perf_counter()
-    j = 0
-    while (time.perf_counter() - t_start) < budget_s and j < (1 << m):
-        a = {l: (j >> b) & 1 for b, l in enumerate(sorted(extra))}
-        t1 = time.perf_counter()
-        contract.bucket_eliminate(network.fix_indices(rest0, a), order)
-        times.append(time.perf_counter() - t1)
-        j += 1
-    k = len(sl)
-    est = t_prefix + statistics.mean(times) * (2 ** (k + m))
-    return {"value": 1.0 / est, "unit": "contractions/s", "cores": 1, "kind": "oracle",
-            "sample": (f"prefix ({len(pre)} steps) + {len(times)} of 2^{m} sub-slices of slice 0 of 2^{k} "
-                       f"(plan residual order as data, width {w}, complex128 numpy.einsum per bucket, "
-                       f"1 thread), scaled x 2^{k + m}; est. {est:.3g} s per contraction"),
-            "sample_s": time.perf_counter() - t0}
+    vals, extra = contract.slice_values(tens, s["prefix"], s["sliced"], s["residual"], js,
+                                        max_width=max_width, workers=workers)
+    dt = time.perf_counter() - t0
+    return contract.pairwise_sum(vals), dt, len(js), 1 << len(extra)
+
+
+def oracle_cpu_baseline(name: str, ga, be, budget_s: float = 20.0) -> dict:
+    """cpu_baseline of the ours arm: the oracle on all usable host cores on a BOUNDED sample of the
+    same contraction -- the prefix plus as many WHOLE slices (each = its 2^m exact sub-slices) as
+    fit in about budget_s, scaled to contractions/s by 2^k / (slices run).  When the whole
+    contraction fits in the budget it is timed whole (sample fraction 1)."""
+    hi = host_info()
+    P = hi["usable_cores"]
+    s = committed_schedule(name)
+    n_sl = 1 << s["k"]
+    # probe: slice 0 alone (its sub-slices over all cores); a batch of slices keeps every core busy
+    _, t1, _, sub = oracle_contraction(name, ga, be, slices=[0], workers=P)
+    per_slice = t1 * min(1.0, sub / P)
+    if s["k"] == 0 or per_slice * n_sl <= budget_s:
+        _, t, ns, sub = oracle_contraction(name, ga, be, workers=P)
+        frac, cps = 1.0, 1.0 / t
+        what = f"the whole contraction ({ns} slice(s) x {sub} exact sub-slices)"
+    else:
+        cnt = int(min(n_sl, max(1, budget_s // per_slice)))
+        _, t, ns, sub = oracle_contraction(name, ga, be, slices=range(cnt), workers=P)
+        frac = ns / n_sl
+        cps = frac / t
+        what = f"the prefix + {ns} of {n_sl} whole slices (each {sub} exact sub-slices), scaled x {n_sl}/{ns}"
+    return {"value": cps, "unit": "contractions/s", "cores": P, "kind": "oracle",
+            "sample": (f"{what}; committed schedule (tests/golden/schedules.json), complex128 numpy.einsum per "
+                       f"bucket, {P} worker processes on {hi['cpu_model']} ({hi['nproc']} logical CPUs)"),
+            "sample_fraction": frac, "sample_seconds": t, "host": hi}
 
 
 # ---------------------------------------------------------------------------- main
+def spawn_ranks(n: int):
+    """Re-exec this command under torch.distributed.run with n ranks on this node (127.0.0.1)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -219,12 +257,18 @@ def main():
     ap.add_argument("--workload", default="C5a")
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--oracle-budget", type=float, default=15.0)
+    ap.add_argument("--oracle-budget", type=float, default=20.0)
+    ap.add_argument("--reference-budget", type=float, default=240.0)
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per GPU
+        spawn_ranks(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
 
     if args.impl == "reference":
         return main_reference(args, rank, world)
@@ -255,8 +299,8 @@ def main():
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)
     partials = torch.zeros(2 * n, dtype=torch.float64, device=dev)
-    ws = plan.workspace(dtype, dev)
-    lanes = plan.batch_windows(dtype) if not info["slices_batchable"] else 1
+    ws = plan.workspace(dtype, dev, n_run=end - begin)
+    lanes = plan.batch_windows(dtype, end - begin) if not info["slices_batchable"] else 1
 
     def step(ga, be):
         partials.zero_()
@@ -315,6 +359,55 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = 1000.0 / float(te.item())
+
+    # ---- per-rank breakdown (after the timed region): prefix alone (an empty slice range runs the
+    # leaves and the shared prefix only), this rank's slices without the all-reduce, the all-reduce
+    def ev_ms(fn, reps):
+        out = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    ga_b, be_b = params[args.warmup]
+    prefix_ms = ev_ms(lambda: plan.contract_sliced(ga_b, be_b, begin, begin, partials, dtype=dtype), 5)
+    slices_ms = ev_ms(lambda: plan.contract_sliced(ga_b, be_b, begin, end, partials, dtype=dtype), 3) \
+        if end > begin else 0.0
+    ar_ms = ev_ms(lambda: dist.all_reduce(partials), 10) if world > 1 else 0.0
+    mine = torch.tensor([prefix_ms, slices_ms, ar_ms, float(end - begin)], dtype=torch.float64, device=dev)
+    if world > 1:
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [r.tolist() for r in allr]
+    else:
+        per_rank = [mine.tolist()]
+    # 1-GPU reference time for the scaling efficiency: rank 0 alone runs every slice (the others
+    # wait at a barrier); E(G) = T(1) / (G T(G)), with and without the (replicated) prefix
+    t1_ms = None
+    if world > 1:
+        dist.barrier()
+        if rank == 0:
+            t1_ms = ev_ms(lambda: plan.contract_sliced(ga_b, be_b, 0, n, partials, dtype=dtype), 3)
+            plan.release_workspaces()
+        dist.barrier()
+    else:
+        t1_ms = ms_step
+    pmax = max(r[0] for r in per_rank)
+    multi = {"per_rank": [{"rank": i, "slices": int(r[3]), "prefix_ms": r[0], "slices_ms": r[1],
+                           "allreduce_us": r[2] * 1e3} for i, r in enumerate(per_rank)],
+             "max_slices_ms": max(r[1] for r in per_rank), "max_prefix_ms": pmax,
+             "t1_ms_rank0_all_slices": t1_ms,
+             "efficiency": (t1_ms / (world * ms_step)) if t1_ms else None,
+             "efficiency_without_prefix": ((t1_ms - pmax) / (world * (ms_step - pmax)))
+             if t1_ms and ms_step > pmax else None,
+             "what": "per rank: materialise + prefix alone, its block of slices (lanes sized from the block), "
+                     "the NCCL all-reduce of the 2*2^k partials; T(1) = rank 0 running all 2^k slices alone; "
+                     "E = T(1) / (G T(G)) -- the driver computes its own scaling from the per-N values"}
 
     # ---- kernel pass: the timed region runs `lanes` slices concurrently, so a launch's duration
     # there includes sharing the GPU with other lanes.  Per-launch rates are therefore measured in
@@ -446,14 +539,14 @@ def main():
         "e2e": {"value": e2e_value, "unit": "contractions/s",
                 "h2d_bytes_per_step": 2 * w.p * 8, "d2h_bytes_per_step": 16 * n},
         "gpu_launches": gpu_launches,
+        "multi_gpu": multi,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = oracle_sample(plan, g, ga0, be0, budget_s=args.oracle_budget)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = oracle_cpu_baseline(args.workload, ga0, be0, budget_s=args.oracle_budget)
         except Exception as e:  # never let the baseline break the bench line
-            line["cpu_baseline"] = {"value": None, "unit": "contractions/s", "cores": 1, "kind": "oracle",
-                                    "sample": f"failed: {e}"}
+            line["cpu_baseline"] = {"value": None, "unit": "contractions/s", "cores": None, "kind": "oracle",
+                                    "sample": f"failed: {e!r}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -461,30 +554,53 @@ def main():
 
 
 def main_reference(args, rank, world):
-    """--impl reference: the oracle (as it stands) on the host cores, rank 0 only."""
+    """--impl reference: the oracle (as it stands: complex128 numpy.einsum per bucket) on all usable
+    host cores, rank 0 only (other ranks exit 0 without work).  It reads the workload's schedule as
+    data from tests/golden/schedules.json and loads NO product code (no libtnb200.so).  One step =
+    one WHOLE contraction for a fresh (gamma, beta) draw (the ours arm's parameter sequence):
+    the prefix and every slice, each slice sub-sliced exactly (Eq. 1) so numpy's complex128
+    tensors stay small, the (slice, sub-slice) evaluations over a process pool.  Steps run until
+    --steps are done or --reference-budget seconds are spent (at least one), so the run ends
+    within a few minutes; the line reports the steps actually timed.  Warm-up: each warm-up step
+    builds the network and contracts the prefix (the oracle has no caches or compiled state)."""
     if rank != 0:
         return
-    import paper_2012_02430_b200 as T  # planning only (host code) to fix the same schedule
-
+    hi = host_info()
+    P = hi["usable_cores"]
     w = WORKLOADS[args.workload]
-    plan, g, ga, be, meta = build_workload_plan(args.workload)
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state; warm-up steps are no-ops
-    vals, samples = [], []
-    budget = max(3.0, min(args.oracle_budget, 150.0 / max(1, args.steps)))
+    sch = committed_schedule(args.workload)
+    params = [qaoa_angles(w.p, 1000 + s) for s in range(args.warmup + args.steps)]
+    from oracle import contract, network
+
+    g = random_regular_graph(w.n, 3, 0)
+    for s in range(args.warmup):
+        ga, be = params[s]
+        sc = sch["oracle_aux"] if sch["k"] == 0 and "oracle_aux" in sch else sch
+        tens = network.qaoa_amplitude_network(w.n, g.edges, ga, be)
+        contract.partial_eliminate(tens, sc["prefix"])
+    times, sub, ns = [], 0, 0
+    t_start = time.perf_counter()
     for s in range(args.steps):
-        cb = oracle_sample(plan, g, ga, be, budget_s=budget)
-        vals.append(cb["value"])
-        samples.append(cb["sample"])
-    v = statistics.mean(vals)
+        ga, be = params[args.warmup + s]
+        _, t, ns, sub = oracle_contraction(args.workload, ga, be, workers=P, sched=sch)
+        times.append(t)
+        if time.perf_counter() - t_start + t > args.reference_budget:
+            break
+    ms = 1000.0 * statistics.mean(times)
+    v = 1000.0 / ms
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "contractions/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
+            "n_gpus": world, "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128 (fp64 complex, numpy)", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: QAOA MaxCut p={w.p}, N={w.n}", "plan_k": plan.info["k"]},
-            "cpu_baseline": {"value": v, "unit": "contractions/s", "cores": 1, "kind": "oracle",
-                             "sample": samples[0]},
-            "e2e": {"value": v, "unit": "contractions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": f"{args.workload}: QAOA MaxCut p={w.p}, N={w.n}", "k": sch["k"],
+                       "width": sch["width"], "schedule": "tests/golden/schedules.json (the ours arm's plan)"},
+            "cpu_baseline": {"value": v, "unit": "contractions/s", "cores": P, "kind": "oracle",
+                             "sample": (f"whole contractions ({ns} slices x {sub} exact sub-slices each), "
+                                        f"{len(times)} timed, {P} worker processes on {hi['cpu_model']} "
+                                        f"({hi['nproc']} logical CPUs)"),
+                             "sample_fraction": 1.0, "host": hi},
+            "e2e": {"value": v, "unit": "contractions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "step_seconds": times}
     print(json.dumps(line), flush=True)
 
 

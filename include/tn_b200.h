@@ -111,6 +111,20 @@ tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int32_t* edges,
                         const tn_build_opts* opts, void** buf, size_t* len);
 void tn_buffer_free(void* buf);
 
+/* Step-dependent slicing scan (Fig. slice_algo): for the FIRST slicing round of
+ * the amplitude network of (graph, p) with opts->n_sliced = n indices (rounds of opts->r), every
+ * candidate slice step s in [0, peak] (reading A8) with the contraction width and the predicted
+ * cost sum_i 2^{degree_i} (prefix once + 2^n x residual) of the plan that slices at s -- the data
+ * of the paper's Fig. hist_of_cost ("difference ... goes up to 9").  Host only.
+ * opts: as tn_plan_build (kind must be AMPLITUDE, 1 <= n_sliced <= 30).  Outputs: host arrays
+ * s_out / width_out (int32[cap]) and cost_out (double[cap]) receive the first min(cap, count)
+ * candidates in ascending s; *n_out = count; *peak_out (may be NULL) = the peak step of the
+ * unsliced order.  cap = 0 queries the count.  Errors: TN_E_INVAL (bad argument), TN_E_PLAN
+ * (n exceeds the live vertex count). */
+tn_status tn_slice_scan(int32_t n_qubits, int32_t n_edges, const int32_t* edges, int32_t p,
+                        const tn_build_opts* opts, int32_t* s_out, int32_t* width_out,
+                        double* cost_out, int32_t cap, int32_t* n_out, int32_t* peak_out);
+
 /* Parse + validate a plan buffer (host).  Caller owns *out; free with tn_plan_free. */
 tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out);
 void tn_plan_free(tn_plan* plan);

@@ -72,27 +72,29 @@ class Plan:
     # windows of per-slice tensors cost at most this many bytes in total
     LANE_WINDOW_BYTES = 48 << 30
 
-    def batch_windows(self, dtype: int) -> int:
-        """Windows of per-slice tensors in the default workspace: slices run per launch when every
-        per-slice step is an interpreter step (slice batching); otherwise two windows let
-        tn_contract_sliced run two slices concurrently (two slice lanes)."""
-        if self.n_slices <= 1:
+    def batch_windows(self, dtype: int, n_run: int = 0) -> int:
+        """Windows of per-slice tensors in the default workspace for a call that runs n_run slices
+        (0: all 2^k; a rank runs only its block, so its lanes are sized from the block): slices run
+        per launch when every per-slice step is an interpreter step (slice batching); otherwise
+        one window per concurrent slice lane (TNB_LANES, default 8) within LANE_WINDOW_BYTES."""
+        n_run = self.n_slices if n_run <= 0 else min(n_run, self.n_slices)
+        if n_run <= 1:
             return 1
         one = B.tn_workspace_bytes(self.handle, dtype, 2) - B.tn_workspace_bytes(self.handle, dtype, 1)
         if not self.info["slices_batchable"]:
             import os
             lanes = max(1, min(8, int(os.environ.get("TNB_LANES", "8"))))
             lanes = 1 if os.environ.get("TNB_ONE_LANE") == "1" else lanes
-            return int(max(1, min(lanes, self.n_slices, self.LANE_WINDOW_BYTES // max(1, one))))
-        return int(max(1, min(self.n_slices, self.BATCH_WINDOW_BYTES // max(1, one))))
+            return int(max(1, min(lanes, n_run, self.LANE_WINDOW_BYTES // max(1, one))))
+        return int(max(1, min(n_run, self.BATCH_WINDOW_BYTES // max(1, one))))
 
-    def workspace(self, dtype: int, device=None, batch: int = 0):
-        """Device workspace (torch.empty), cached per (dtype, device, batch).  batch = 0: the
-        plan's default (slice batching windows when batchable)."""
+    def workspace(self, dtype: int, device=None, batch: int = 0, n_run: int = 0):
+        """Device workspace (torch.empty), cached per (dtype, device, windows).  batch = 0: the
+        plan's default for a call running n_run slices (batch_windows)."""
         import torch
 
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        nb = self.batch_windows(dtype) if batch == 0 else batch
+        nb = self.batch_windows(dtype, n_run) if batch == 0 else batch
         key = (dtype, str(dev), nb)
         ws = self._ws.get(key)
         if ws is None:
@@ -116,7 +118,7 @@ class Plan:
 
     def contract_sliced(self, gammas, betas, begin: int, end: int, partials, dtype: int = TN_C64,
                         stream=None) -> None:
-        ws = self.workspace(dtype)
+        ws = self.workspace(dtype, n_run=end - begin)
         B.tn_contract_sliced(self.handle, dtype, gammas, betas, begin, end, ws.data_ptr(), ws.numel(),
                              self._stream(stream), partials.data_ptr())
 

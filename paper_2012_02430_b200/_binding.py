@@ -23,7 +23,7 @@ TN_ORDER_MIN_FILL, TN_ORDER_MIN_DEGREE, TN_ORDER_RGREEDY, TN_ORDER_RGREEDY_FILL 
 STATUS = {0: "TN_OK", -1: "TN_E_INVAL", -2: "TN_E_PLAN", -3: "TN_E_TOO_WIDE", -4: "TN_E_NOMEM",
           -5: "TN_E_CUDA", -6: "TN_E_DTYPE"}
 
-SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_plan_load", "tn_plan_free", "tn_plan_info",
+SYMBOLS = ["tn_plan_build", "tn_buffer_free", "tn_slice_scan", "tn_plan_load", "tn_plan_free", "tn_plan_info",
            "tn_plan_schedule", "tn_plan_steps", "tn_contract", "tn_contract_sliced", "tn_sum_partials", "tn_energy", "tn_energy_batch",
            "tn_workspace_bytes",
            "tn_eliminate", "tn_eliminate_group", "tn_profile_enable", "tn_profile_read", "tn_profile_records", "tn_last_error", "tn_version"]
@@ -83,6 +83,9 @@ _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _lib.tn_plan_build.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
                                C.POINTER(tn_build_opts), C.POINTER(_P), C.POINTER(C.c_size_t)]
+_lib.tn_slice_scan.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.POINTER(tn_build_opts),
+                               C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int32,
+                               C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
 _lib.tn_buffer_free.argtypes = [_P]
 _lib.tn_buffer_free.restype = None
 _lib.tn_plan_load.argtypes = [_P, C.c_size_t, C.POINTER(_P)]
@@ -151,6 +154,26 @@ def tn_plan_build(n_qubits: int, edges, p: int, kind: int = TN_KIND_AMPLITUDE,
         return C.string_at(buf, ln.value)
     finally:
         _lib.tn_buffer_free(buf)
+
+
+def tn_slice_scan(n_qubits: int, edges, p: int, n_sliced: int, orderer: int = TN_ORDER_MIN_FILL, r: int = 0,
+                  rg_q: int = 0, rg_tau: float = 0.0, rg_seed: int = 0):
+    """First-round candidates of step-dependent slicing: (list of (s, width, cost), peak)."""
+    flat = []
+    for e in edges:
+        flat.extend((int(e[0]), int(e[1])))
+    arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    oarr = (C.c_int32 * 1)()
+    opts = tn_build_opts(TN_KIND_AMPLITUDE, orderer, n_sliced, r, 0, -1, rg_q, int(round(rg_tau * 1000)),
+                         rg_seed, 0, C.cast(oarr, C.POINTER(C.c_int32)))
+    n, peak = C.c_int32(), C.c_int32()
+    _check(_lib.tn_slice_scan(n_qubits, len(flat) // 2, arr, p, C.byref(opts), None, None, None, 0, C.byref(n),
+                              C.byref(peak)), "tn_slice_scan")
+    cap = max(1, n.value)
+    so, wo, co = (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_double * cap)()
+    _check(_lib.tn_slice_scan(n_qubits, len(flat) // 2, arr, p, C.byref(opts), so, wo, co, cap, C.byref(n),
+                              C.byref(peak)), "tn_slice_scan")
+    return [(so[i], wo[i], co[i]) for i in range(n.value)], peak.value
 
 
 def tn_plan_load(buf: bytes) -> int:

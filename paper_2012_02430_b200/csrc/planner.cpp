@@ -365,7 +365,8 @@ Ordering order_graph(const BitGraph& g, const OrderSpec& spec, uint64_t salt) {
 }
 
 // ============================================================== step-dependent slicing
-Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec) {
+Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec,
+                      std::vector<SliceCandidate>* scan, int* peak_out) {
   Schedule sch;
   Ordering full0 = order_graph(g0, spec, 0);
   sch.unsliced_width = full0.width;
@@ -389,6 +390,7 @@ Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec) {
     int peak = 0;
     for (size_t i = 0; i < full.degrees.size(); ++i)
       if (full.degrees[i] > full.degrees[peak]) peak = (int)i;
+    if (first_round && peak_out) *peak_out = peak;
     // candidate steps s in [0, peak] (reading A8)
     BitGraph gs = g;
     int pmax = prefix_width;
@@ -417,6 +419,7 @@ Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec) {
       Ordering res = order_graph(gr, spec, 1 + s + 7919ull * n_done);
       const int w = std::max(pmax, res.width);
       const double cost = prefix_cost + pcost + std::ldexp(res.cost, n_done + rr);
+      if (first_round && scan) scan->push_back(SliceCandidate{s, w, cost});
       // best: smaller width, then fewer predicted operations, then smaller s (reading A10)
       if (w < best_w || (w == best_w && cost < best_cost)) {
         best_w = w;

@@ -99,8 +99,17 @@ struct Schedule {
   double cost = 0.0;
 };
 
-// step-dependent slicing (Fig. slice_algo): n indices in rounds of r
-Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec);
+// one candidate of the first slicing round: slicing after s steps of the full order
+struct SliceCandidate {
+  int s;          // candidate slice step (reading A8: s in [0, peak])
+  int width;      // max(prefix width, residual width) of the plan slicing at s
+  double cost;    // predicted sum 2^degree over the plan (prefix once + 2^n x residual)
+};
+
+// step-dependent slicing (Fig. slice_algo): n indices in rounds of r.
+// scan (optional): every candidate s of the first round (Fig. hist_of_cost)
+Schedule slice_search(const BitGraph& g0, int n, int r, const OrderSpec& spec,
+                      std::vector<SliceCandidate>* scan = nullptr, int* peak_out = nullptr);
 
 struct LoweredProgram {
   std::vector<LeafRec> leaves;

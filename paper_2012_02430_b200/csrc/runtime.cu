@@ -119,6 +119,47 @@ size_t ws_bytes_for(const PlanHeader& h, int dtype) {
 }  // namespace
 
 // ============================================================== C ABI: planning
+// step-dependent slicing scan (Fig. slice_algo; Fig. hist_of_cost)
+extern "C" tn_status tn_slice_scan(int32_t n_qubits, int32_t n_edges, const int32_t* edges, int32_t p,
+                                   const tn_build_opts* opts, int32_t* s_out, int32_t* width_out,
+                                   double* cost_out, int32_t cap, int32_t* n_out, int32_t* peak_out) {
+  if (!opts || !n_out || (n_edges > 0 && !edges) || n_qubits <= 0 || n_edges < 0 || cap < 0)
+    return fail(TN_E_INVAL, "tn_slice_scan: null or negative argument");
+  if (p < 1 || p > kMaxP) return fail(TN_E_INVAL, "tn_slice_scan: p out of range [1, 16]");
+  if (opts->kind != TN_KIND_AMPLITUDE) return fail(TN_E_INVAL, "tn_slice_scan: amplitude networks only");
+  if (opts->orderer < TN_ORDER_MIN_FILL || opts->orderer > TN_ORDER_RGREEDY_FILL)
+    return fail(TN_E_INVAL, "tn_slice_scan: unknown orderer");
+  if (opts->n_sliced < 1 || opts->n_sliced > 30 || opts->r < 0)
+    return fail(TN_E_INVAL, "tn_slice_scan: n_sliced must be in [1, 30], r >= 0");
+  if (cap > 0 && (!s_out || !width_out || !cost_out)) return fail(TN_E_INVAL, "tn_slice_scan: null output");
+  OrderSpec spec;
+  spec.orderer = opts->orderer;
+  spec.q = opts->rg_q == 0 ? 8 : opts->rg_q;
+  spec.tau = opts->rg_tau_milli == 0 ? 0.5 : opts->rg_tau_milli / 1000.0;
+  spec.seed = opts->rg_seed;
+  try {
+    std::vector<int> ev(edges, edges + 2 * (size_t)n_edges);
+    std::vector<int> opened;
+    for (int i = 0; i < opts->n_open; ++i) opened.push_back(opts->open_qubits[i]);
+    const Network net = build_amplitude_network(n_qubits, ev, p, opened);
+    std::vector<SliceCandidate> scan;
+    int peak = -1;
+    (void)slice_search(BitGraph::from_network(net), opts->n_sliced, opts->r, spec, &scan, &peak);
+    *n_out = (int32_t)scan.size();
+    if (peak_out) *peak_out = peak;
+    for (int i = 0; i < (int)scan.size() && i < cap; ++i) {
+      s_out[i] = scan[i].s;
+      width_out[i] = scan[i].width;
+      cost_out[i] = scan[i].cost;
+    }
+    return TN_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(TN_E_PLAN, std::string("tn_slice_scan: ") + e.what());
+  } catch (const std::exception& e) {
+    return fail(TN_E_NOMEM, std::string("tn_slice_scan: ") + e.what());
+  }
+}
+
 extern "C" tn_status tn_plan_build(int32_t n_qubits, int32_t n_edges, const int32_t* edges,
                                    int32_t p, const tn_build_opts* opts, void** buf, size_t* len) {
   if (!opts || !buf || !len || (n_edges > 0 && !edges) || n_qubits <= 0 || n_edges < 0)

@@ -217,6 +217,32 @@ def test_group_kernels_vs_oracle(case, kernel):
         assert np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30) < TOL[dtype] * 0.1
 
 
+def test_group_kernels_each_take_some_cases():
+    """Each explicitly named group kernel (1 k_gemm, 2 k_pair, 3 k_group_t) accepts -- and then
+    matches the oracle on -- at least one GROUP_CASES shape: the parametrised test above skips the
+    shapes a kernel declines, so this guards against a kernel that declines everything."""
+    for kernel, want in ((1, 5), (2, 1), (3, 1)):
+        took = 0
+        for case, (out_rank, M, low, xa, xb, chi) in enumerate(GROUP_CASES):
+            rng = np.random.default_rng(1000 + case)
+            cls = _cls(rng, out_rank, low)
+            masks, xms, shapes = _gemm_group(rng, out_rank, M, cls, xa, xb, chi)
+            arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+            dev = [torch.tensor(a, dtype=torch.complex64, device="cuda") for a in arrays]
+            out = torch.full((2 ** out_rank,), float("nan"), dtype=torch.complex64, device="cuda")
+            try:
+                B.tn_eliminate_group(T.TN_C64, M, [d.data_ptr() for d in dev], masks, xms, out.data_ptr(),
+                                     out_rank, kernel, torch.cuda.current_stream().cuda_stream)
+            except T.TnError:
+                continue
+            torch.cuda.synchronize()
+            got = out.cpu().numpy().astype(np.complex128)
+            ref = _oracle_group(arrays, masks, xms, M, out_rank)
+            assert np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30) < TOL[T.TN_C64] * 0.1
+            took += 1
+        assert took >= want, f"kernel {kernel} took only {took} of {len(GROUP_CASES)} shapes"
+
+
 TC_CASES = [
     # (out_rank, M, classes from bit 0 up (a: A only, b: B only, c: both), xa, xb, cmask_hi)
     (18, 3, "abccabcaabcbabaaac", None, None, 0),          # the bit pattern of C5a's top group

@@ -2,6 +2,7 @@
 include/tn_b200.h; the planner's schedules are valid, deterministic and replay to the widths
 an independent implementation (the oracle's line graph) computes; error paths."""
 import ctypes
+import json
 import math
 import os
 import re
@@ -300,3 +301,50 @@ def test_fused_pairs_never_write_over_producer_inputs():
         n_feed += sum(1 for op in P["ops"] if op.type == planbuf.OP_GROUP_FEED)
         assert planbuf.feed_overlaps(pl.buf) == [], (n, seed, p, k, o)
     assert n_feed > 0
+
+
+def _greedy_min_degree_graph(adj):
+    """Min-degree elimination of a line graph (ties -> smallest label), on a copy: degrees."""
+    adj = {v: set(nb) for v, nb in adj.items()}
+    degs = []
+    while adj:
+        v = min(adj, key=lambda x: (len(adj[x]), x))
+        degs.append(len(adj[v]))
+        contract.eliminate_vertex(adj, v)
+    return degs
+
+
+def test_planner_reports_replay():
+    """f3 reports (scripts/planner_reports.py, profiles/r02/planner): a width-vs-n row replays
+    through the oracle's line graph, and candidate rows of the width-over-s scan match an
+    independent re-run of the paper's procedure (eliminate s vertices of the
+    greedy order, remove the n highest-degree vertices of G_s, re-run greedy on the rest)."""
+    import csv
+
+    base = os.path.join(ROOT, "profiles", "r02", "planner")
+    rows = list(csv.DictReader(open(os.path.join(base, "width_vs_n.csv"))))
+    row = next(r for r in rows if r["N"] == "100" and r["seed"] == "0" and r["orderer"] == "min-degree"
+               and r["n"] == "3")
+    g = random_regular_graph(100, 3, 0)
+    ga, be = qaoa_angles(1, 0)
+    plan = T.build_plan(g, 1, "amplitude", "min-degree", n_sliced=3)
+    pre, sl, res, _ = plan.schedule()
+    tens = network.qaoa_amplitude_network(100, g.edges, ga, be)
+    assert max(_replay(tens, pre, sl, res)) == int(row["width"]) == plan.width
+    scan = json.load(open(os.path.join(base, "width_over_s.json")))["N150_n3"]
+    g = random_regular_graph(150, 3, 0)
+    tens = network.qaoa_amplitude_network(150, g.edges, *qaoa_angles(1, 0))
+    order, odeg = contract.greedy_min_degree(tens)
+    assert scan["peak"] == odeg.index(max(odeg))
+    cands = scan["candidates"]
+    for c in (cands[0], min(cands, key=lambda c: (c["width"], c["s"])), cands[len(cands) // 2]):
+        s = c["s"]
+        adj = contract.line_graph(tens)
+        for v in order[:s]:
+            contract.eliminate_vertex(adj, v)
+        S = sorted(adj, key=lambda v: (-len(adj[v]), v))[:3]
+        for v in S:
+            for a in adj.pop(v):
+                adj[a].discard(v)
+        w = max(odeg[:s] + _greedy_min_degree_graph(adj))
+        assert w == c["width"], (s, w, c["width"])
