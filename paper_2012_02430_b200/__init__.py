@@ -118,7 +118,7 @@ class Plan:
 
     def contract_sliced(self, gammas, betas, begin: int, end: int, partials, dtype: int = TN_C64,
                         stream=None) -> None:
-        ws = self.workspace(dtype, n_run=end - begin)
+        ws = self.workspace(dtype, n_run=max(1, end - begin))
         B.tn_contract_sliced(self.handle, dtype, gammas, betas, begin, end, ws.data_ptr(), ws.numel(),
                              self._stream(stream), partials.data_ptr())
 
