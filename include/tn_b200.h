@@ -125,7 +125,12 @@ tn_status tn_slice_scan(int32_t n_qubits, int32_t n_edges, const int32_t* edges,
                         const tn_build_opts* opts, int32_t* s_out, int32_t* width_out,
                         double* cost_out, int32_t cap, int32_t* n_out, int32_t* peak_out);
 
-/* Parse + validate a plan buffer (host).  Caller owns *out; free with tn_plan_free. */
+/* Parse + validate a plan buffer (host; the contract input of SPEC.md:290-298: a network plus an
+ * elimination order that covers every live label -- "order misses a live label", is
+ * raised by tn_plan_build).  Checks magic / version, record counts against the buffer length,
+ * every step's output and input ranges against the arena, and the op / scalar / program records.
+ * Caller owns *out; free with tn_plan_free.
+ * Errors: TN_E_INVAL (null argument), TN_E_PLAN (malformed or version-mismatched buffer). */
 tn_status tn_plan_load(const void* buf, size_t len, tn_plan** out);
 void tn_plan_free(tn_plan* plan);
 tn_status tn_plan_info(const tn_plan* plan, tn_plan_info_t* out);
@@ -157,13 +162,15 @@ typedef struct {
 tn_status tn_plan_steps(const tn_plan* plan, tn_step_info_t* out, int64_t cap, int64_t* n);
 
 /* ---------------------------------------------------------------- contraction (device) */
-/* Unsliced amplitude (sliced plans: all 2^k slices summed locally).  gamma, beta: host double[p].
+/* The amplitude sigma = <0^N|U(gamma, beta)|0^N> of the QAOA circuit U (§5: "the
+ * tensor expression ... with boundary indices fixed"; sliced plans: all 2^k slices of Eq. (1),
+ * PAPER.md:519-524, summed locally).  gamma, beta: host double[p].
  * ws: device buffer of >= workspace_bytes[dtype] bytes (e.g. torch.empty).  stream: cudaStream_t
  * (NULL = legacy default stream).  out: host double[2 * 2^a] = {Re, Im} of batch entry x at
  * out[2x], out[2x+1] (a = n_open; a = 0: the single amplitude sigma), 2^{-N/2} applied in FP64
  * (reading A15).  Synchronous with respect to `stream` on return. */
 tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma, const double* beta,
-                      int32_t p, void* ws, size_t ws_bytes, void* stream, double out[2]);
+                      int32_t p, void* ws, size_t ws_bytes, void* stream, double* out);
 
 /* Slices [begin, end) of a sliced plan, Eq. (1): runs the shared prefix once,
  * then every slice; writes the complex128 result of slice j, batch entry x (x < 2^a, a = n_open)
@@ -184,7 +191,9 @@ tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, const double* 
  * tn_contract_sliced (double[2 n_slices 2^a]); out: host double[2 * 2^a]. */
 tn_status tn_sum_partials(const tn_plan* plan, const double* partials_host, double* out);
 
-/* Energy plan: all E light-cone networks contracted in ONE batched launch.  zz: host double[E]
+/* QAOA MaxCut energy <psi|C|psi> as the sum of per-edge <Z_u Z_v> (§3.2: each
+ * term evaluated on its own reverse-light-cone network).  Energy plan: all E light-cone networks
+ * contracted in ONE batched launch.  zz: host double[E]
  * (Re <Z_u Z_v> per edge in the graph's edge order), zz_imag_max: host double (max |Im|, ~0),
  * energy: host double = sum_e (1 - zz[e]) / 2 (reading A3).  Synchronous on return. */
 tn_status tn_energy(const tn_plan* plan, tn_dtype dtype, const double* gamma, const double* beta,

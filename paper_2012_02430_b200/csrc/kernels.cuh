@@ -1067,15 +1067,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
   cp_async_wait<0>();
 }
 
-// ------------------------------------------------------------------ warp-specialised k_gemm
-// k_gemm_ws: the same batched complex GEMM as k_gemm (same MArgs, tiles, chunk layouts and
-// formatted B'), with the chunk traffic moved to a producer warp.  Warps 0-7 (consumers) compute;
-// warp 8 (producer) walks the CTA's tile sequence ahead of them and, whenever A's or B's chunk
-// changes, waits until the consumers released the ring slot it reuses (empty mbarrier), issues the
-// cp.async copies of the next version and makes them arrive on the slot's full mbarrier
-// (cp.async.mbarrier.arrive.noinc).  Consumers wait on full mbarriers; they synchronise among
-// themselves (named barrier 1) only when B' is rebuilt; there is no CTA-wide barrier per tile.
-// Requires a tile-independent C (no constant input holds an output bit).
+// ------------------------------------------------------------------ mbarrier helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -1096,219 +1088,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-constexpr int kGemmWsThreads = 288;   // 8 consumer warps + 1 producer warp
-constexpr int kGemmMaxSlots = 4;
-
-template <int M, int RAB, int RBB>
-__global__ void __launch_bounds__(kGemmWsThreads, 2) k_gemm_ws(const MArgs a) {
-  constexpr int NCONS = 256;
-  constexpr int TL = 8;
-  constexpr int K = 1 << M, RA = 1 << RAB, RB = 1 << RBB;
-  constexpr int TB = TL + RAB + RBB;
-  constexpr int NB = 64 - TB;
-  const uint32_t tid = threadIdx.x;
-  const bool producer = tid >= NCONS;
-  const uint64_t n_tiles = 1ull << (a.out_rank - TB);
-  extern __shared__ __align__(16) unsigned char dsm[];
-  float2* sm = reinterpret_cast<float2*>(dsm);
-  uint32_t* smu = reinterpret_cast<uint32_t*>(dsm);
-  __shared__ uint32_t fbit[2 + kMaxIn][NB];
-  __shared__ uint32_t fcum[2 + kMaxIn][NB + 1];
-  __shared__ uint64_t pbit[NB], pcum[NB + 1];
-  __shared__ float2 Cs[K];
-  __shared__ __align__(8) uint64_t full_bar[2][kGemmMaxSlots], empty_bar[2][kGemmMaxSlots];
-  const int nin = 2 + a.nc;
-  auto mask_of = [&](int t) { return t < 2 ? a.mask[t] : a.cmask[t - 2]; };
-  auto pv_of = [&](int t) { return t < 2 ? a.pv[t] : a.cpv[t - 2]; };
-  const int nperm = a.out_rank - TB;
-  const int S = a.stages;
-  for (int i = tid; i < nin * NB; i += kGemmWsThreads) {
-    const int t = i / NB, b = i % NB;
-    fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], mask_of(t), pv_of(t)) : 0u;
-  }
-  for (int b = tid; b < NB; b += kGemmWsThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const uint32_t lp = a.nch[u] - a.lv[u];
-    const uint32_t np = a.nrows[u] << lp;
-    for (uint32_t c = tid; c < np; c += kGemmWsThreads) {
-      const uint32_t ia = (c & ((1u << lp) - 1u)) << a.lv[u];
-      uint32_t off = a.rowoff[u][c >> lp];
-      for (uint32_t k = a.lv[u]; k < a.nch[u]; ++k)
-        if ((ia >> k) & 1u) off += a.posoff[u][k];
-      smu[a.sm_dep[u] + c] = off;
-    }
-  }
-  if (tid == 0) {
-    for (int u = 0; u < 2; ++u)
-      for (int k = 0; k < kGemmMaxSlots; ++k) {
-        mbar_init(&full_bar[u][k], 32);                  // one cp.async arrive per producer lane
-        mbar_init(&empty_bar[u][k], u == 0 ? 8 : 1);     // A: every consumer warp; B: after B' is built
-      }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // C[x]: tile-independent here (constants hold no output bit)
-  if (tid < (uint32_t)K) {
-    float2 c = make_float2(1.f, 0.f);
-#pragma unroll
-    for (int t = 0; t < kMaxIn - 2; ++t)
-      if (t < a.nc) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + a.cgx[t][tid]));
-    Cs[tid] = c;
-  }
-  __syncthreads();
-  const int nbu = min(NB - 1, max(0, (int)a.out_rank - TB));
-  if (tid < (uint32_t)nin) {
-    uint32_t c = 0;
-    fcum[tid][0] = 0;
-    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
-  }
-  if (tid == (uint32_t)nin) {
-    uint64_t c = 0;
-    pcum[0] = 0;
-    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
-  }
-  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
-  const uint64_t t0 = (uint64_t)blockIdx.x * per;
-  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
-  uint64_t obase = 0;
-  for (int b = 0; b < nperm && (t0 >> b); ++b)
-    if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
-  __syncthreads();
-
-  if (producer) {
-    // ---------------------------------------------------------------- producer warp
-    const uint32_t lane = tid - NCONS;
-    uint32_t cur[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
-    int ver[2] = {0, 0}, slot[2] = {0, 0};
-    auto issue = [&](int u) {
-      const float2* src = static_cast<const float2*>(a.in[u]) + cur[u];
-      float2* dst = sm + a.sm_in[u][slot[u]];
-      const uint32_t np = a.nrows[u] << (a.nch[u] - a.lv[u]);
-      const uint32_t* tab = smu + a.sm_dep[u];
-      if (a.lv[u]) {
-        for (uint32_t c = lane; c < np; c += 32) cp_async16(dst + (c << 1), src + tab[c]);
-      } else {
-        for (uint32_t c = lane; c < np; c += 32) cp_async8(dst + c, src + tab[c]);
-      }
-      mbar_cp_async_arrive(&full_bar[u][slot[u]]);
-    };
-    if (t0 < t1) { issue(0); issue(1); }
-    for (uint64_t lt = t0 + 1; lt < t1; ++lt) {
-      const int rr = __ffsll((long long)~(lt - 1)) - 1;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (fbit[u][rr] == fcum[u][rr]) continue;
-        cur[u] = cur[u] + fbit[u][rr] - fcum[u][rr];
-        ++ver[u];
-        slot[u] = slot[u] + 1 == S ? 0 : slot[u] + 1;
-        if (ver[u] >= S) mbar_wait(&empty_bar[u][slot[u]], (uint32_t)((ver[u] / S - 1) & 1));
-        issue(u);
-      }
-    }
-    cp_async_wait<0>();
-    return;
-  }
-
-  // ------------------------------------------------------------------ consumer warps
-  uint64_t othr = 0;
-  uint32_t iathr = 0, ibthr = 0;
-#pragma unroll
-  for (int k = 0; k < TL; ++k) {
-    if ((tid >> k) & 1u) {
-      othr += 1ull << a.outbit[k];
-      if (a.chbit[0][k] >= 0) iathr += 1u << a.chbit[0][k];
-      if (a.chbit[1][k] >= 0) ibthr += 1u << a.chbit[1][k];
-    }
-  }
-  uint64_t ora[RA], orb[RB];
-  uint32_t iar[RA], ibr[RB];
-#pragma unroll
-  for (int i = 0; i < RA; ++i) {
-    ora[i] = 0; iar[i] = 0;
-#pragma unroll
-    for (int k = 0; k < RAB; ++k)
-      if ((i >> k) & 1) { ora[i] += 1ull << a.outbit[TL + k]; iar[i] += 1u << a.chbit[0][TL + k]; }
-  }
-#pragma unroll
-  for (int j = 0; j < RB; ++j) {
-    orb[j] = 0; ibr[j] = 0;
-#pragma unroll
-    for (int k = 0; k < RBB; ++k)
-      if ((j >> k) & 1) { orb[j] += 1ull << a.outbit[TL + RAB + k]; ibr[j] += 1u << a.chbit[1][TL + RAB + k]; }
-  }
-  float2* out = static_cast<float2*>(a.out);
-  float4* bf = reinterpret_cast<float4*>(dsm + a.sm_bf_bytes);
-  const uint32_t nB = 1u << a.nch[1];
-  int ver[2] = {0, 0}, slot[2] = {0, 0};
-  bool needA = true, needB = true;
-  const uint32_t warp = tid >> 5, lane = tid & 31;
-  for (uint64_t tile = t0; tile < t1; ++tile) {
-    const int r = __ffsll((long long)~tile) - 1;
-    if (needA) mbar_wait(&full_bar[0][slot[0]], (uint32_t)((ver[0] / S) & 1));
-    if (needB) {
-      mbar_wait(&full_bar[1][slot[1]], (uint32_t)((ver[1] / S) & 1));
-      named_bar_sync(1, NCONS);        // every consumer is done with the previous B'
-      const float2* sBraw = sm + a.sm_in[1][slot[1]];
-      for (uint32_t e = tid; e < (uint32_t)K * nB; e += NCONS) {
-        const uint32_t x = e >> a.nch[1], idx = e & (nB - 1u);
-        const float2 b = cmul(sBraw[((uint32_t)a.row[1][x] << a.nch[1]) + idx], Cs[x]);
-        bf[e] = make_float4(b.x, b.y, -b.y, b.x);
-      }
-      named_bar_sync(1, NCONS);        // B' complete; the raw B slot is free again
-      if (tid == 0) mbar_arrive(&empty_bar[1][slot[1]]);
-    }
-    const float2* sA = sm + a.sm_in[0][slot[0]] + iathr;
-    const float4* sB = bf + ibthr;
-    uint64_t acc[RA][RB];
-#pragma unroll
-    for (int i = 0; i < RA; ++i)
-#pragma unroll
-      for (int j = 0; j < RB; ++j) acc[i][j] = 0ull;
-#pragma unroll
-    for (int x = 0; x < K; ++x) {
-      const float2* pa = sA + ((uint32_t)a.row[0][x] << a.nch[0]);
-      const float4* pb = sB + ((uint32_t)x << a.nch[1]);
-      float2 av[RA];
-      float4 bv[RB];
-#pragma unroll
-      for (int i = 0; i < RA; ++i) av[i] = pa[iar[i]];
-#pragma unroll
-      for (int j = 0; j < RB; ++j) bv[j] = pb[ibr[j]];
-#pragma unroll
-      for (int i = 0; i < RA; ++i)
-#pragma unroll
-        for (int j = 0; j < RB; ++j) {
-          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].x, av[i].x)), "l"(f2_pack(bv[j].x, bv[j].y)));
-          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].y, av[i].y)), "l"(f2_pack(bv[j].z, bv[j].w)));
-        }
-    }
-    float2* ot = out + obase + othr;
-#pragma unroll
-    for (int i = 0; i < RA; ++i)
-#pragma unroll
-      for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(acc[i][j]));
-    // advance; release A's slot when the next tile uses a new A chunk
-    const bool chA = tile + 1 < t1 && fbit[0][r] != fcum[0][r];
-    const bool chB = tile + 1 < t1 && fbit[1][r] != fcum[1][r];
-    if (chA) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[0][slot[0]]);
-      ++ver[0];
-      slot[0] = slot[0] + 1 == S ? 0 : slot[0] + 1;
-    }
-    if (chB) {
-      ++ver[1];
-      slot[1] = slot[1] + 1 == S ? 0 : slot[1] + 1;
-    }
-    needA = chA;
-    needB = chB;
-    obase = obase + pbit[r] - pcum[r];
-    (void)warp;
-  }
 }
 
 // ------------------------------------------------------------------ fused reduce chain

@@ -115,6 +115,7 @@ __device__ __forceinline__ void tf32_split(float v, float& big, float& small) {
   small = v - big;
 }
 
+#ifndef TNB_TC_HELPERS_ONLY   // launch_fc_tc.cu includes only the helpers above
 __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const TArgs a) {
   extern __shared__ __align__(128) unsigned char dsm_tc[];
   __shared__ uint64_t bar_mdone[2], bar_tempty[2], bar_ready[2], bar_rawa;
@@ -552,5 +553,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_tc(const TArgs a) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
 }
+
+#endif  // TNB_TC_HELPERS_ONLY
 
 }  // namespace tnb

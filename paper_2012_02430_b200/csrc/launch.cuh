@@ -122,7 +122,7 @@ inline bool gemm_disabled() {
 // which kernel the last launcher on this thread used (per-launch profile records)
 enum KernelId : int { KID_NONE = 0, KID_BUCKET = 1, KID_CHAIN = 2, KID_GROUP = 3, KID_PAIR = 4,
                       KID_GEMM = 5, KID_CHAIN_SPLIT = 6, KID_PROGRAM = 7,
-                      KID_GEMM_TC = 8, KID_GEMM_FC = 9 };
+                      KID_GEMM_TC = 8, KID_GEMM_FC = 9, KID_FC_TC = 10 };
 inline int& last_kernel() {
   static thread_local int k = KID_NONE;
   return k;
@@ -135,8 +135,11 @@ bool try_launch_gemm_tc(const GDesc& g, cudaStream_t st);
 bool gemm_tc_enabled();                                                          // TNB_GEMM_TC=1
 // producer group g (GEMM-shaped) computed tile by tile and consumed by group g3 (its input tin)
 template <typename T> bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
+// the same pair with the producer GEMM on tcgen05 (k_fc_tc, c64); false when the shape does not qualify
+bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
+bool fc_tc_enabled();                                                            // TNB_FC_TC=0/1
 bool fc_enabled();                                                               // TNB_NO_FC=1 off
-template <typename T> bool try_launch_gemm_simt(const GDesc& g, cudaStream_t st);   // k_gemm / k_gemm_ws only                        // tcgen05 kind::tf32, c64
+template <typename T> bool try_launch_gemm_simt(const GDesc& g, cudaStream_t st);   // k_gemm only                        // tcgen05 kind::tf32, c64
 template <typename T> bool try_launch_pair(const GDesc& g, cudaStream_t st);
 template <typename T> bool try_launch_group(const GDesc& g, cudaStream_t st);
 template <typename T> void launch_bucket_generic(const BigArgs& a, cudaStream_t st);   // k_bucket<T, n_in>

@@ -15,29 +15,6 @@ void launch_m(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
   k_gemm<M, RAB, RBB, true, WB><<<grid, 32 << WB, smem, st>>>(ma);
 }
 
-template <int M, int RAB, int RBB>
-void launch_ws(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
-  allow_smem(k_gemm_ws<M, RAB, RBB>, smem);
-  last_kernel() = KID_GEMM;
-  k_gemm_ws<M, RAB, RBB><<<grid, kGemmWsThreads, smem, st>>>(ma);
-}
-
-template <int M>
-bool dispatch_ws(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
-  if (rab == 2 && rbb == 2) { launch_ws<M, 2, 2>(ma, grid, smem, st); return true; }
-  if (rab == 2 && rbb == 1) { launch_ws<M, 2, 1>(ma, grid, smem, st); return true; }
-  if (rab == 1 && rbb == 2) { launch_ws<M, 1, 2>(ma, grid, smem, st); return true; }
-  if (rab == 1 && rbb == 1) { launch_ws<M, 1, 1>(ma, grid, smem, st); return true; }
-  return false;
-}
-
-// warp-specialised k_gemm (producer warp + mbarriers) for tile-independent C: TNB_GEMM_WS=1 on.
-// Off by default since the 8-lane / fused-pair state: C5a 86.7 vs 83.6, C4b 54.4 vs 53.3 /s.
-inline bool gemm_ws() {
-  static const bool on = env_flag("TNB_GEMM_WS");
-  return on;
-}
-
 template <int M, int WB>
 bool dispatch_m(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
   if (rab == 3 && rbb == 2) { launch_m<M, 3, 2, WB>(ma, grid, smem, st); return true; }
@@ -284,16 +261,6 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB) 
     }
     const uint64_t tiles = 1ull << (R - TB);
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * (WB == 3 ? 2 : 4));
-    if (WB == 3 && !ma.c_tile_dep && gemm_ws() && nra <= 2 && nrb <= 2 && ma.stages <= kGemmMaxSlots) {
-      switch (g.M) {
-        case 1: return dispatch_ws<1>(ma, nra, nrb, grid, smem, st);
-        case 2: return dispatch_ws<2>(ma, nra, nrb, grid, smem, st);
-        case 3: return dispatch_ws<3>(ma, nra, nrb, grid, smem, st);
-        case 4: return dispatch_ws<4>(ma, nra, nrb, grid, smem, st);
-        case 5: return dispatch_ws<5>(ma, nra, nrb, grid, smem, st);
-        default: break;
-      }
-    }
     if (WB == 2) {
       switch (g.M) {
         case 1: return dispatch_m<1, 2>(ma, nra, nrb, grid, smem, st);

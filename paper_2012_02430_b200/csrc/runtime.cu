@@ -742,7 +742,8 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
             const double tb = std::ldexp(1.0, g.out_rank);   // the never-written intermediate
             ProfScope ps(pl, st, (bytes - tb + bytes3 - tb) * sizeof(T), op.begin, nx.end, 3, g3.out_rank);
             ps.pr.flops = 8.0 * (std::ldexp(1.0, g.out_rank + g.M) + std::ldexp(1.0, g3.out_rank + g3.M));
-            const bool fused = try_launch_gemm_fc<T>(g, g3, tin, st);
+            const bool fused = (std::is_same<T, float2>::value && fc_tc_enabled() && try_launch_fc_tc(g, g3, tin, st)) ||
+                               try_launch_gemm_fc<T>(g, g3, tin, st);
             ps.cancel = !fused;
             if (fused) {
               ++oi;
@@ -909,7 +910,7 @@ extern "C" tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, con
 
 extern "C" tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma,
                                  const double* beta, int32_t p, void* ws, size_t ws_bytes,
-                                 void* stream, double out[2]) {
+                                 void* stream, double* out) {
   tn_status s = check_call(plan, dtype, gamma, beta, p, ws, ws_bytes);
   if (s != TN_OK) return s;
   if (!out) return fail(TN_E_INVAL, "null out");

@@ -320,13 +320,19 @@ def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
     assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
 
 
+FUSED_PAIR = {"k_gemm_fc", "k_fc_tc"}   # the two kernels of an OP_GROUP_FEED pair (SIMT / tcgen05)
+
+
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
 @pytest.mark.parametrize("n,p,k,fused", [(36, 3, 3, True), (70, 2, 3, True), (44, 3, 3, False),
                                           (50, 2, 2, False)])
-def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused):
+def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused, kernel, monkeypatch):
     """OP_GROUP_FEED: a GEMM-shaped group whose output is a full input of the next group runs as ONE
-    k_gemm_fc launch (the intermediate is never written); the contraction still matches the
-    oracle (c64 tolerance), and the fused launch is the one that ran (profile records).  Pairs whose
+    launch (the intermediate is never written) -- k_fc_tc (tcgen05) when its shape qualifies, else
+    k_gemm_fc (FP32 SIMT; TNB_FC_TC=0 / 1 selects); the contraction still matches the oracle
+    (c64 tolerance), and the fused launch is the one that ran (profile records).  Pairs whose
     consumer output has fewer bits than a k_gemm_fc tile (fused=False) run as the two groups."""
+    monkeypatch.setenv("TNB_FC_TC", "0" if kernel == "simt" else "1")
     g = random_regular_graph(n, 3, 7 * n + p)
     ga, be = qaoa_angles(p, n + 1)
     plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
@@ -334,10 +340,36 @@ def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused):
     got = plan.contract(ga, be, dtype=T.TN_C64)
     recs = plan.profile_records()
     plan.profile(False)
-    assert any(r["kernel"] == "k_gemm_fc" for r in recs) == fused, sorted({r["kernel"] for r in recs})
+    ran = {r["kernel"] for r in recs}
+    assert bool(ran & FUSED_PAIR) == fused, sorted(ran)
+    if kernel == "simt":
+        assert "k_fc_tc" not in ran
     pre, sl, res, _ = plan.schedule()
     ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
     assert rel(got, ref) < TOL[T.TN_C64]
+
+
+def test_fc_tc_runs_on_c5a_and_matches_simt_per_slice(monkeypatch):
+    """C5a's producer -> consumer pair (R = 26 -> 21, the bench's largest launch) runs on k_fc_tc;
+    every per-slice partial agrees with the FP32 SIMT k_gemm_fc within the c64 tolerance."""
+    plan, g, ga, be, meta = _bench_plan()
+    n = plan.n_slices
+    parts = {}
+    for kern in ("tc", "simt"):
+        monkeypatch.setenv("TNB_FC_TC", "0" if kern == "simt" else "1")
+        part = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        plan.profile(True)
+        plan.contract_sliced(ga, be, 0, n, part, dtype=T.TN_C64)
+        torch.cuda.synchronize()
+        ran = {r["kernel"] for r in plan.profile_records()}
+        plan.profile(False)
+        plan.profile_read()
+        assert ("k_fc_tc" if kern == "tc" else "k_gemm_fc") in ran, sorted(ran)
+        h = part.cpu().tolist()
+        parts[kern] = [complex(h[2 * j], h[2 * j + 1]) for j in range(n)]
+    scale = max(abs(v) for v in parts["simt"])
+    for j in range(n):
+        assert abs(parts["tc"][j] - parts["simt"][j]) / scale < 2e-5, (j, parts["tc"][j], parts["simt"][j])
 
 
 
@@ -454,7 +486,7 @@ def test_c5a_full_scale_sampled_slice_vs_oracle():
     B.tn_contract_sliced(plan.handle, T.TN_C64, ga, be, 0, n, ws.data_ptr(), ws.numel(),
                          torch.cuda.current_stream().cuda_stream, part.data_ptr())
     torch.cuda.synchronize()
-    assert any(r["kernel"] == "k_gemm_fc" for r in plan.profile_records())
+    assert {r["kernel"] for r in plan.profile_records()} & FUSED_PAIR
     plan.profile(False)
     j = n // 2
     pre, sl, res, _ = plan.schedule()
@@ -538,7 +570,7 @@ def test_slice_lanes_with_fused_pairs_match_one_lane_and_oracle():
         B.tn_contract_sliced(plan.handle, T.TN_C64, ga, be, 0, plan.n_slices, ws.data_ptr(), ws.numel(),
                              torch.cuda.current_stream().cuda_stream, part.data_ptr())
         torch.cuda.synchronize()
-        assert any(r["kernel"] == "k_gemm_fc" for r in plan.profile_records())
+        assert {r["kernel"] for r in plan.profile_records()} & FUSED_PAIR
         plan.profile(False)
         outs.append(part.cpu())
     assert torch.equal(outs[0], outs[1])
