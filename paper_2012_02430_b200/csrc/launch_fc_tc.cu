@@ -4,8 +4,13 @@
 #include "launch.cuh"
 #include "kernels_fctc.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 
 namespace tnb {
 
@@ -17,19 +22,114 @@ bool fc_tc_enabled() {
   return v ? v[0] == '1' : kFcTcDefault;
 }
 
-template <int M, int NB, int NOB>
-static void launch_ft(const FTArgs& fa, unsigned grid, size_t smem, cudaStream_t st) {
-  allow_smem(k_fc_tc<M, NB, NOB>, smem);
+// tensor maps of the launch (kernel parameters; unused in the cp.async mode)
+struct FtMaps {
+  CUtensorMap x, a;
+};
+
+template <int M, int NB, int NOB, int NL>
+static void launch_ft(const FTArgs& fa, const FtMaps& mp, unsigned grid, size_t smem, cudaStream_t st) {
+  allow_smem(k_fc_tc<M, NB, NOB, NL>, smem);
   last_kernel() = KID_FC_TC;
-  k_fc_tc<M, NB, NOB><<<grid, kFtThreads, smem, st>>>(fa);
+  k_fc_tc<M, NB, NOB, NL><<<grid, kFtThreads, smem, st>>>(fa, mp.x, mp.a);
 }
 
+// ---- TMA geometry: a tensor whose bits are "box" bits (the unit's) or traversal bits; dims = runs
+// of box bits, each followed by the traversal bits above it (coordinates); the 5th dim takes every
+// bit above its start; box bits of further runs become separate copies (at most 8)
+struct TmaGeom {
+  int ndim = 0;
+  uint32_t s[5] = {0, 0, 0, 0, 0}, nt[5] = {0, 0, 0, 0, 0}, nb[5] = {0, 0, 0, 0, 0};
+  int ncopy = 1;
+  uint32_t cdelta[8][5] = {};
+  uint32_t box_elems = 1;
+  int smem_bit[64];
+};
+
+static bool tma_geom(int Rt, const std::vector<char>& isbox, TmaGeom& G) {
+  if (Rt < 1 || Rt > 32 || !isbox[0]) return false;
+  std::vector<std::array<int, 3>> runs;   // start, box bits, total bits
+  for (int k = 0; k < Rt;) {
+    const int st = k;
+    int nb = 0;
+    while (k < Rt && isbox[k]) { ++nb; ++k; }
+    while (k < Rt && !isbox[k]) ++k;
+    runs.push_back({st, nb, k - st});
+  }
+  G.ndim = std::min<int>(5, (int)runs.size());
+  for (int& b : G.smem_bit) b = -1;
+  int sb = 0;
+  for (int d = 0; d < G.ndim; ++d) {
+    G.s[d] = (uint32_t)runs[d][0];
+    G.nb[d] = (uint32_t)runs[d][1];
+    G.nt[d] = d + 1 < G.ndim ? (uint32_t)runs[d][2] : (uint32_t)(Rt - runs[d][0]);
+    if (G.nb[d] > 8) return false;   // box dims <= 256
+    for (uint32_t i = 0; i < G.nb[d]; ++i) G.smem_bit[G.s[d] + i] = sb++;
+  }
+  std::vector<int> extra;
+  for (size_t r = G.ndim; r < runs.size(); ++r)
+    for (int i = 0; i < runs[r][1]; ++i) extra.push_back(runs[r][0] + i);
+  if (extra.size() > 3) return false;
+  G.box_elems = 1u << sb;
+  for (size_t j = 0; j < extra.size(); ++j) G.smem_bit[extra[j]] = sb + (int)j;
+  G.ncopy = 1 << extra.size();
+  const int last = G.ndim - 1;
+  for (int i = 0; i < G.ncopy; ++i)
+    for (size_t j = 0; j < extra.size(); ++j)
+      if ((i >> j) & 1) G.cdelta[i][last] += 1u << (extra[j] - G.s[last]);
+  return (G.box_elems * 8) % 128 == 0;   // every copy lands 128-byte aligned
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+static bool tma_encode(CUtensorMap* map, const void* base, int Rt, const TmaGeom& G) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dim[5], stride[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  for (int d = 0; d < 5; ++d) {
+    if (d < G.ndim) {
+      dim[d] = 1ull << G.nt[d];
+      box[d] = 1u << G.nb[d];
+    } else {
+      dim[d] = 1;
+      box[d] = 1;
+    }
+    if (d >= 1) stride[d - 1] = (d < G.ndim ? (1ull << G.s[d]) : (1ull << Rt)) * 8ull;
+  }
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dim, stride, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// instantiated shapes (column bits NB, output column bits NOB, line bits NL): 2^(NOB + NL) <= 32
+// accumulators per epilogue thread
 template <int M>
-static bool dispatch_ft(const FTArgs& fa, int nb, int nob, unsigned grid, size_t smem, cudaStream_t st) {
-#define FT_CASE(B, O) \
-  if (nb == B && nob == O) { launch_ft<M, B, O>(fa, grid, smem, st); return true; }
-  FT_CASE(5, 4) FT_CASE(5, 5) FT_CASE(5, 3) FT_CASE(4, 4) FT_CASE(4, 3) FT_CASE(3, 3)
+static bool dispatch_ft(const FTArgs& fa, const FtMaps& mp, int nb, int nob, int nl, unsigned grid, size_t smem,
+                        cudaStream_t st) {
+#define FT_CASE(B, O, L) \
+  if (nb == B && nob == O && nl == L) { launch_ft<M, B, O, L>(fa, mp, grid, smem, st); return true; }
+  FT_CASE(5, 4, 0) FT_CASE(5, 5, 0) FT_CASE(4, 4, 0) FT_CASE(4, 3, 0) FT_CASE(3, 3, 0)
+  FT_CASE(5, 4, 1) FT_CASE(4, 4, 1) FT_CASE(4, 3, 1) FT_CASE(5, 3, 2) FT_CASE(4, 3, 2) FT_CASE(3, 3, 2)
 #undef FT_CASE
+  return false;
+}
+
+static bool ft_have(int nb, int nob, int nl) {
+  static const int k[][3] = {{5, 4, 0}, {5, 5, 0}, {4, 4, 0}, {4, 3, 0}, {3, 3, 0}, {5, 4, 1}, {4, 4, 1},
+                             {4, 3, 1}, {5, 3, 2}, {4, 3, 2}, {3, 3, 2}};
+  for (const auto& e : k)
+    if (e[0] == nb && e[1] == nob && e[2] == nl) return true;
   return false;
 }
 
@@ -39,13 +139,14 @@ static bool dispatch_ft(const FTArgs& fa, int nb, int nob, unsigned grid, size_t
     return false;                                                                         \
   } while (0)
 
-// smem bytes of a configuration (must match k_fc_tc's layout)
-static size_t ft_smem(int M, int NB, int nc, int S, uint32_t* sm_b, uint32_t* sm_raw, uint32_t* sm_x,
-                      uint32_t* sm_tab) {
-  const size_t K = 1u << M, KP = 2 * K, NCOL = 1u << NB, N = 2 * NCOL;
+// smem bytes of a configuration (must match k_fc_tc's layout): operand slots, S raw per-unit
+// chunk slots, X group tiles (SX slots of NLS = 2^NL units), tables
+static size_t ft_smem(int M, int NB, int NL, int SX, int S, int xp_bits, uint32_t* sm_b, uint32_t* sm_raw,
+                      uint32_t* sm_x, uint32_t* sm_tab, uint32_t* sm_xp) {
+  const size_t K = 1u << M, KP = 2 * K, NCOL = 1u << NB, N = 2 * NCOL, NLS = 1u << NL;
   const size_t a_part = 128 * KP * 4, b_part = N * KP * 4;
-  const size_t raw_slot = 128 * K * 8 + NCOL * K * 8 + (size_t)nc * K * 8;
-  const size_t x_tile = 128 * NCOL * 8;
+  const size_t raw_slot = (128 * K * 8 + NCOL * K * 8 + (size_t)kMaxIn * K * 8 + 127) / 128 * 128;
+  const size_t x_tile = NLS * 128 * NCOL * 8;
   size_t o = 0;
   o += 2 * 2 * a_part;
   *sm_b = (uint32_t)o;
@@ -54,9 +155,11 @@ static size_t ft_smem(int M, int NB, int nc, int S, uint32_t* sm_b, uint32_t* sm
   o += (size_t)S * raw_slot;
   o = (o + 127) / 128 * 128;
   *sm_x = (uint32_t)o;
-  o += (size_t)S * x_tile;
+  o += (size_t)SX * x_tile;
   *sm_tab = (uint32_t)o;
-  o += (256 + 2 * NCOL) * 4;
+  o += (512 + 2 * NCOL) * 4;
+  *sm_xp = (uint32_t)o;
+  if (xp_bits >= 5) o += (size_t)8 << (xp_bits - 5);
   return o;
 }
 
@@ -137,24 +240,43 @@ bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
     if (r0 >= 0) rows.push_back(r0);
     for (int b : cand)
       if ((int)rows.size() < kFtRows && b != r0) rows.push_back(b);
-    // columns: output b-bits (low col bits) then y b-bits; NB <= 5, NOB >= 3, NCOL >= 8
+    // line bits: output bits outside the rows whose offset in X and in A lies inside one 128-byte
+    // line (16 c64 elements): units differing in them share DRAM lines, so they run back to back
     std::vector<int> ob, yb;
     for (int b = 0; b < R; ++b)
       if ((cb >> b) & 1) (b < R3 ? ob : yb).push_back(b);
     if ((int)ob.size() < 3) continue;
-    int best_nob = -1, best_nyb = 0;
+    std::vector<std::pair<int, int>> lc;   // (score, bit)
+    {
+      std::vector<char> isrow(R, 0);
+      for (int b : rows) isrow[b] = 1;
+      for (int b = 0; b < R3; ++b) {
+        if (isrow[b] || ((cb >> b) & 1)) continue;
+        const uint64_t xo = xoff(b);
+        const uint64_t ao = ((A.out_mask >> b) & 1) ? host_fmap(1ull << b, A.out_mask, A.pv) : 0;
+        const int sc = (xo > 0 && xo < 16 ? 1 : 0) + (ao > 0 && ao < 16 ? 1 : 0);
+        if (sc > 0) lc.push_back({-sc, b});
+      }
+      std::sort(lc.begin(), lc.end());
+    }
+    // columns: output b-bits (low col bits) then y b-bits; NB <= 5, NOB >= 3, NCOL >= 8; the
+    // cost model: units per CTA x (X tile + a fixed per-unit overhead)
+    int best_nob = -1, best_nyb = 0, best_nl = 0;
     double best_cost = 1e300;
     const int n_o_free = R3 - kFtRows;   // o bits outside the rows
-    for (int nob = 3; nob <= std::min<int>(5, (int)ob.size()); ++nob)
-      for (int nyb = 0; nyb <= (int)yb.size() && nob + nyb <= 5; ++nyb) {
-        const int nb = nob + nyb;
-        const double nblk = std::ldexp(1.0, n_o_free - nob);
-        const int nyt = M3 - nyb;
-        const double per_cta = std::ceil(nblk / num_sms()) * std::ldexp(1.0, nyt);
-        const double cost = per_cta * (std::ldexp(1.0, nb) + 16.0);
-        if (cost < best_cost) { best_cost = cost; best_nob = nob; best_nyb = nyb; }
-      }
-    if (best_nob < 0) continue;
+    for (int nl = 0; nl <= std::min<int>(2, (int)lc.size()); ++nl)
+      for (int nob = 3; nob <= std::min<int>(5, (int)ob.size()); ++nob)
+        for (int nyb = 0; nyb <= (int)yb.size() && nob + nyb <= 5; ++nyb) {
+          const int nb = nob + nyb;
+          if (!ft_have(nb, nob, nl)) continue;
+          const double nblk = std::ldexp(1.0, n_o_free - nob - nl);
+          const int nyt = M3 - nyb;
+          const double per_cta = std::ceil(nblk / num_sms()) * std::ldexp(1.0, nyt + nl);
+          // a line bit left in the block bits re-reads its lines from DRAM: x 2 per line bit
+          const double waste = std::ldexp(1.0, std::min<int>(2, (int)lc.size()) - nl);
+          const double cost = per_cta * (std::ldexp(1.0, nb) * waste + 16.0);
+          if (cost < best_cost) { best_cost = cost; best_nob = nob; best_nyb = nyb; best_nl = nl; }
+        }
     const int NOB = best_nob, NB = best_nob + best_nyb;
     std::vector<int> cols(ob.begin(), ob.begin() + NOB);
     for (int j = 0; j < best_nyb; ++j) cols.push_back(yb[j]);
@@ -171,15 +293,18 @@ bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
       ++nc;
     }
     if (!ok || nc > kMaxIn) continue;
-    // traversal: y bits first (innermost: a block = one set of consumer outputs), then the o bits
-    // X lacks (its tile is re-read from L2 right away), then those A lacks, then the rest
+    // traversal: the line bits, then the y bits (a block = one set of consumer outputs), then the
+    // o bits X lacks (its tile is re-read from L2 soon after), then those A lacks, then the rest
+    const int NL = best_nl;
     std::vector<int> trav;
+    uint64_t lmask = 0;
+    for (int i = 0; i < NL; ++i) { trav.push_back(lc[i].second); lmask |= 1ull << lc[i].second; }
     for (int b = R3; b < R; ++b)
       if (!((unit >> b) & 1)) trav.push_back(b);
-    const int nyt = (int)trav.size();
+    const int nyt = (int)trav.size() - NL;
     std::vector<int> rest;
     for (int b = 0; b < R3; ++b)
-      if (!((unit >> b) & 1)) rest.push_back(b);
+      if (!((unit >> b) & 1) && !((lmask >> b) & 1)) rest.push_back(b);
     std::stable_sort(rest.begin(), rest.end(), [&](int p, int q2) {
       auto key = [&](int b) {
         if (xoff(b) == 0) return 0;
@@ -199,7 +324,7 @@ bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
     fa.out = static_cast<float2*>(g3.out);
     fa.ntrav = (int)trav.size();
     fa.nyt = nyt;
-    fa.n_blocks = 1ull << (trav.size() - nyt);
+    fa.n_blocks = 1ull << (trav.size() - nyt - NL);
     for (int i = 0; i < kFtRows; ++i) {
       fa.arow[i] = amap(rows[i]);
       fa.xrow[i] = (uint32_t)xoff(rows[i]);
@@ -239,34 +364,163 @@ bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
     fa.M3 = M3;
     fa.apair = fa.arow[0] == 1 ? 1 : 0;
     fa.xpair = fa.xrow[0] == 1 ? 1 : 0;
+    // shared-memory layouts of the X tile and the raw A chunk: TMA boxes when the unit bits allow
+    // (TNB_FC_TMA=0 forces the cp.async path), else [c][r] / [x][r] by 8- or 16-byte cp.async
+    FtMaps mp;
+    std::memset(&mp, 0, sizeof(mp));
+    fa.tma = 0;
+    {
+      // X tile loads: coalesced 16-byte cp.async pieces in the [line][column][row] layout when row
+      // bit 0 pairs X elements (default; TNB_FC_XLOAD=tma: TMA boxes in the tensor's own order)
+      const char* e = std::getenv("TNB_FC_XLOAD");
+      const bool want = e && std::strcmp(e, "tma") == 0;
+      fa.xp_bits = 0;
+      const int RX = (int)Xin.rank, RA = (int)A.rank;
+      std::vector<char> bx(RX, 0), ba(RA, 0);
+      auto lg = [](uint64_t v) { return v ? __builtin_ctzll(v) : -1; };
+      for (int i = 0; i < kFtRows; ++i) {
+        if (fa.xrow[i]) bx[lg(fa.xrow[i])] = 1;
+        ba[lg(fa.arow[i])] = 1;
+      }
+      for (int j = 0; j < NB; ++j)
+        if (fa.xcol[j]) bx[lg(fa.xcol[j])] = 1;
+      for (int i = 0; i < NL; ++i)        // a line group's tile: the line bits are box bits too
+        if (fa.tx[i]) bx[lg(fa.tx[i])] = 1;
+      bool xok = true;
+      for (int j = 0; j < g.M; ++j) {
+        const uint64_t v = A.gx[1u << j];
+        if (v == 0 || (v & (v - 1))) xok = false;
+        else ba[lg(v)] = 1;
+      }
+      TmaGeom GX, GA;
+      // raw A chunks: TMA boxes over the unit's rows and summed values (default; TNB_FC_ATMA=0 ->
+      // cp.async), in the box layout the formatters index with as_row / as_x
+      fa.atma = 0;
+      {
+        const char* ea = std::getenv("TNB_FC_ATMA");
+        std::vector<char> ba2(RA, 0);
+        for (int i = 0; i < kFtRows; ++i) ba2[lg(fa.arow[i])] = 1;
+        bool aok = !(ea && ea[0] == '0') && xok;
+        for (int j = 0; j < g.M && aok; ++j) ba2[lg(A.gx[1u << j])] = 1;
+        if (aok && tma_geom(RA, ba2, GA) && GA.ncopy * GA.box_elems <= (128u << g.M) &&
+            tma_encode(&mp.a, A.ptr, RA, GA)) {
+          fa.atma = 1;
+          for (int d = 0; d < 5; ++d) {
+            fa.ts[1][d] = d < GA.ndim ? GA.s[d] : 0;
+            fa.tmsk[1][d] = d < GA.ndim ? (uint32_t)((1ull << GA.nt[d]) - 1) : 0u;
+            for (int i = 0; i < 8; ++i) fa.cdelta[1][i][d] = GA.cdelta[i][d];
+          }
+          fa.ncopy[1] = GA.ncopy;
+          fa.copy_elems[1] = GA.box_elems;
+          for (int i = 0; i < kFtRows; ++i) fa.as_row[i] = 1u << GA.smem_bit[lg(fa.arow[i])];
+          for (int x = 0; x < (1 << g.M); ++x) {
+            uint32_t o = 0;
+            for (int j = 0; j < g.M; ++j)
+              if ((x >> j) & 1) o += 1u << GA.smem_bit[lg(A.gx[1u << j])];
+            fa.as_x[x] = o;
+          }
+        } else {
+          for (int i = 0; i < kFtRows; ++i) fa.as_row[i] = 1u << i;
+          for (int x = 0; x < (1 << g.M); ++x) fa.as_x[x] = 128u * (uint32_t)x;
+        }
+      }
+      if (want && tma_geom(RX, bx, GX) && GX.ncopy * GX.box_elems <= (128u << NB) << NL &&
+          tma_encode(&mp.x, Xin.ptr, RX, GX)) {
+        fa.tma = 1;
+        const TmaGeom* G[1] = {&GX};
+        for (int t = 0; t < 1; ++t) {
+          for (int d = 0; d < 5; ++d) {
+            fa.ts[t][d] = d < G[t]->ndim ? G[t]->s[d] : 0;
+            fa.tmsk[t][d] = d < G[t]->ndim ? (uint32_t)((1ull << G[t]->nt[d]) - 1) : 0u;
+            for (int i = 0; i < 8; ++i) fa.cdelta[t][i][d] = G[t]->cdelta[i][d];
+          }
+          fa.ncopy[t] = G[t]->ncopy;
+          fa.copy_elems[t] = G[t]->box_elems;
+        }
+        for (int i = 0; i < kFtRows; ++i) fa.xs_row[i] = fa.xrow[i] ? 1u << GX.smem_bit[lg(fa.xrow[i])] : 0u;
+        for (int j = 0; j < NB; ++j) fa.xs_col[j] = fa.xcol[j] ? 1u << GX.smem_bit[lg(fa.xcol[j])] : 0u;
+        for (int li = 0; li < (1 << NL); ++li) {
+          uint32_t ox = 0;
+          for (int i = 0; i < NL; ++i)
+            if (((li >> i) & 1) && fa.tx[i]) ox += 1u << GX.smem_bit[lg(fa.tx[i])];
+          fa.xs_line[li] = ox;
+        }
+      } else {
+        if (fa.xpair) {
+          std::vector<std::pair<uint32_t, uint32_t>> pb;   // (global, smem) per piece bit
+          for (int i = 1; i < kFtRows; ++i) pb.push_back({fa.xrow[i], 1u << i});
+          for (int j = 0; j < NB; ++j) pb.push_back({fa.xcol[j], 128u << j});
+          for (int i = 0; i < NL; ++i) pb.push_back({fa.tx[i], (128u << NB) << i});
+          std::stable_sort(pb.begin(), pb.end(), [](const auto& p1, const auto& p2) { return p1.first < p2.first; });
+          if (pb.size() <= 24 && pb.size() >= 5) {
+            fa.xp_bits = (int)pb.size();
+            for (size_t k = 0; k < pb.size(); ++k) { fa.xp_g[k] = pb[k].first; fa.xp_s[k] = pb[k].second; }
+          }
+        }
+        for (int i = 0; i < kFtRows; ++i) fa.xs_row[i] = 1u << i;
+        for (int j = 0; j < NB; ++j) fa.xs_col[j] = 128u << j;
+        for (int li = 0; li < (1 << NL); ++li) fa.xs_line[li] = (uint32_t)li * (128u << NB);
+      }
+    }
     const int N = 2 << NB;
     fa.tmem_cols = 32;
     while (fa.tmem_cols < (uint32_t)(2 * N)) fa.tmem_cols <<= 1;
     size_t smem = 0;
-    int S = 3;
-    for (; S >= 2; --S) {
-      smem = ft_smem(g.M, NB, nc, S, &fa.sm_b, &fa.sm_raw, &fa.sm_x, &fa.sm_tab);
-      if (smem <= 220 * 1024) break;
+    int SX = 0, SU = 0;
+    for (const auto& c : {std::make_pair(2, 4), std::make_pair(2, 3), std::make_pair(2, 2), std::make_pair(1, 3),
+                          std::make_pair(1, 2)}) {
+      smem = ft_smem(g.M, NB, NL, c.first, c.second, fa.xp_bits, &fa.sm_b, &fa.sm_raw, &fa.sm_x, &fa.sm_tab,
+                     &fa.sm_xp);
+      if (smem <= 218 * 1024) { SX = c.first; SU = c.second; break; }
     }
-    if (S < 2) continue;
-    fa.S = S;
+    if (SX == 0) continue;
+    fa.S = SU;
+    fa.SX = SX;
+    const int S = SX * 10 + SU;   // (trace print)
     const unsigned grid = (unsigned)std::min<uint64_t>(fa.n_blocks, (uint64_t)num_sms());
+    static unsigned long long* trace = nullptr;
+    const bool want_trace = env_flag("TNB_FT_TRACE");
+    if (want_trace && !trace && cudaMalloc(&trace, 256 * 8 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
+    fa.trace = want_trace ? trace : nullptr;
+    if (fa.trace) cudaMemsetAsync(fa.trace, 0, 256 * 8 * sizeof(unsigned long long), st);
     if (env_flag("TNB_GEMM_DEBUG")) {
-      std::fprintf(stderr, "k_fc_tc R=%d M=%d R3=%d M3=%d swap=%d NB=%d NOB=%d nyt=%d blocks=%llu S=%d smem=%zu "
-                   "apair=%d xpair=%d rows=", R, g.M, R3, M3, swap, NB, NOB, nyt, (unsigned long long)fa.n_blocks,
-                   S, smem, fa.apair, fa.xpair);
+      std::fprintf(stderr, "k_fc_tc R=%d M=%d R3=%d M3=%d swap=%d NB=%d NOB=%d NL=%d nyt=%d blocks=%llu S=%d smem=%zu "
+                   "apair=%d xpair=%d tma=%d atma=%d xp_bits=%d (copies %d,%d) rows=", R, g.M, R3, M3, swap, NB, NOB, NL,
+                   nyt, (unsigned long long)fa.n_blocks, S, smem, fa.apair, fa.xpair, fa.tma, fa.atma, fa.xp_bits,
+                   fa.ncopy[0], fa.ncopy[1]);
       for (int b : rows) std::fprintf(stderr, "%d,", b);
       std::fprintf(stderr, " cols=");
       for (int b : cols) std::fprintf(stderr, "%d,", b);
+      std::fprintf(stderr, " trav=");
+      for (int b : trav) std::fprintf(stderr, "%d,", b);
       std::fprintf(stderr, "\n");
     }
+    bool ok2 = false;
     switch (g.M) {
-      case 2: return dispatch_ft<2>(fa, NB, NOB, grid, smem, st);
-      case 3: return dispatch_ft<3>(fa, NB, NOB, grid, smem, st);
-      case 4: return dispatch_ft<4>(fa, NB, NOB, grid, smem, st);
-      case 5: return dispatch_ft<5>(fa, NB, NOB, grid, smem, st);
+      case 2: ok2 = dispatch_ft<2>(fa, mp, NB, NOB, NL, grid, smem, st); break;
+      case 3: ok2 = dispatch_ft<3>(fa, mp, NB, NOB, NL, grid, smem, st); break;
+      case 4: ok2 = dispatch_ft<4>(fa, mp, NB, NOB, NL, grid, smem, st); break;
+      case 5: ok2 = dispatch_ft<5>(fa, mp, NB, NOB, NL, grid, smem, st); break;
       default: return false;
     }
+    if (ok2 && fa.trace) {   // debugging aid: CTA 0's pipeline timeline (clock64), averaged gaps
+      unsigned long long h[256 * 8];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, fa.trace, sizeof(h), cudaMemcpyDeviceToHost);
+      const int n = (int)std::min<uint64_t>(256, (fa.n_blocks / grid) << (NL + nyt));
+      const char* nm[8] = {"prod_start", "fmt_done", "mma_issue", "epi_start", "epi_end", "prod_done", "fmt_start", "epi_wait0"};
+      std::fprintf(stderr, "k_fc_tc trace (CTA 0, %d units): per-unit mean of (event - ld_ready):", n);
+      for (int e = 1; e < 8; ++e) {
+        double sum = 0;
+        int c = 0;
+        for (int u = 8; u < n; ++u)
+          if (h[u * 8 + e] && h[u * 8]) { sum += (double)(long long)(h[u * 8 + e] - h[u * 8]); ++c; }
+        std::fprintf(stderr, " %s %.0f", nm[e], c ? sum / c : 0.0);
+      }
+      double per = n > 16 ? (double)(h[(n - 1) * 8 + 4] - h[8 * 8 + 4]) / (n - 9) : 0;
+      std::fprintf(stderr, " | cycles per unit %.0f\n", per);
+    }
+    return ok2;
   }
   FT_DECLINE("no row / column assignment");
 }

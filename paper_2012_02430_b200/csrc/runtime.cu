@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -38,13 +39,36 @@ static tn_status fail(tn_status s, const std::string& msg) {
   } while (0)
 
 // ============================================================== plan object
+// a captured tn_contract_sliced body (prefix + slices, all lanes) for one argument set: replayed by
+// one cudaGraphLaunch (TNB_GRAPH=0 disables)
+struct GraphKey {
+  int dtype;
+  uintptr_t ws, partials, stream;
+  size_t ws_bytes;
+  uint64_t begin, end;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(dtype, ws, partials, stream, ws_bytes, begin, end) <
+           std::tie(o.dtype, o.ws, o.partials, o.stream, o.ws_bytes, o.begin, o.end);
+  }
+};
+struct GraphRec {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches = 0;   // kernels in the graph
+  bool direct = false;     // capture failed once: always run directly
+};
+
 struct DevTables {
+  std::map<GraphKey, GraphRec> graphs;
   StepRec* steps = nullptr;
   LeafRec* leaves = nullptr;
   ScalarRec* scalars = nullptr;
   ProgramRec* progs = nullptr;
   cudaStream_t side[kMaxLanes - 1] = {};   // slice lanes 1.. (tn_contract_sliced, one window each)
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes - 1] = {};
+  // graphs are captured and replayed on a library stream ordered after / before the caller's (the
+  // legacy default stream cannot be captured)
+  cudaStream_t cap = nullptr;
+  cudaEvent_t ev_cin = nullptr, ev_cout = nullptr;
 };
 
 struct ProfRec {
@@ -68,6 +92,7 @@ struct tn_plan {
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
   uint64_t all_launches = 0;
+  uint64_t graph_launches = 0;   // cudaGraphLaunch calls (each replays a captured slice range)
   bool batchable = false;   // every per-slice op is an interpreter run -> slices can run batched
   ~tn_plan() {
     for (auto& kv : dev) {
@@ -81,6 +106,11 @@ struct tn_plan {
         if (kv.second.ev_join[l]) cudaEventDestroy(kv.second.ev_join[l]);
       }
       if (kv.second.ev_fork) cudaEventDestroy(kv.second.ev_fork);
+      if (kv.second.cap) cudaStreamDestroy(kv.second.cap);
+      if (kv.second.ev_cin) cudaEventDestroy(kv.second.ev_cin);
+      if (kv.second.ev_cout) cudaEventDestroy(kv.second.ev_cout);
+      for (auto& g : kv.second.graphs)
+        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     }
     for (auto& p : prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -516,6 +546,9 @@ tn_status ensure_dev(tn_plan* pl, DevTables** out) {
       CU(cudaEventCreateWithFlags(&t.ev_join[l], cudaEventDisableTiming));
     }
     CU(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
+    CU(cudaStreamCreateWithFlags(&t.cap, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&t.ev_cin, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&t.ev_cout, cudaEventDisableTiming));
     it = pl->dev.emplace(dev, t).first;
   }
   *out = &it->second;
@@ -819,6 +852,18 @@ tn_status check_call(const tn_plan* plan, int dtype, const double* gamma, const 
 }
 
 template <typename T>
+tn_status sliced_body(tn_plan* pl, DevTables* dt, uint64_t begin, uint64_t end, void* wsv, size_t ws_bytes,
+                      cudaStream_t st, double* partials_dev);
+
+inline bool graphs_enabled() {
+  const char* v = std::getenv("TNB_GRAPH");
+  return !(v && v[0] == '0') && !env_flag("TNB_FT_TRACE") && !debug_checks();
+}
+
+// leaves from (gamma, beta) (a direct launch: the angles change every call), then the prefix and
+// the slices -- captured once per argument set into a CUDA graph and replayed (host enqueue of one
+// contraction: one graph launch instead of ~15 launches per slice)
+template <typename T>
 tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int p, uint64_t begin,
                       uint64_t end, void* wsv, size_t ws_bytes, cudaStream_t st, double* partials_dev) {
   DevTables* dt = nullptr;
@@ -826,6 +871,73 @@ tn_status sliced_impl(tn_plan* pl, const double* gamma, const double* beta, int 
   if (s != TN_OK) return s;
   T* ws = static_cast<T*>(wsv);
   if ((s = materialize<T>(pl, *dt, gamma, beta, p, ws, st)) != TN_OK) return s;
+  if (pl->profiling || !graphs_enabled())
+    return sliced_body<T>(pl, dt, begin, end, wsv, ws_bytes, st, partials_dev);
+  const GraphKey key{sizeof(T) == 8 ? 0 : 1, reinterpret_cast<uintptr_t>(wsv), reinterpret_cast<uintptr_t>(partials_dev),
+                     reinterpret_cast<uintptr_t>(st), ws_bytes, begin, end};
+  GraphRec rec;
+  {
+    // the first call with an argument set runs directly (single-shot calls never pay for a
+    // capture); the second captures, later ones replay
+    std::lock_guard<std::mutex> lk(pl->mu);
+    auto it = dt->graphs.find(key);
+    if (it == dt->graphs.end()) {
+      if (dt->graphs.size() >= 256) {   // bounded cache
+        for (auto& g : dt->graphs)
+          if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+        dt->graphs.clear();
+      }
+      dt->graphs[key] = GraphRec{};
+      rec.launches = ~0ull;
+    } else {
+      rec = it->second;
+    }
+  }
+  if (rec.launches == ~0ull || rec.direct) return sliced_body<T>(pl, dt, begin, end, wsv, ws_bytes, st, partials_dev);
+  const cudaStream_t cs = dt->cap;
+  CU(cudaEventRecord(dt->ev_cin, st));
+  CU(cudaStreamWaitEvent(cs, dt->ev_cin, 0));
+  if (!rec.exec) {
+    const uint64_t l0 = pl->all_launches;
+    bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    cudaGraph_t graph = nullptr;
+    if (ok) {
+      s = sliced_body<T>(pl, dt, begin, end, wsv, ws_bytes, cs, partials_dev);
+      ok = cudaStreamEndCapture(cs, &graph) == cudaSuccess && s == TN_OK;
+      if (ok) ok = cudaGraphInstantiate(&rec.exec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    const uint64_t captured = pl->all_launches - l0;
+    pl->all_launches = l0;   // counted when the graph runs
+    if (!ok) {   // run this argument set directly from now on
+      (void)cudaGetLastError();
+      rec.exec = nullptr;
+      rec.direct = true;
+      {
+        std::lock_guard<std::mutex> lk(pl->mu);
+        dt->graphs[key] = rec;
+      }
+      CU(cudaEventRecord(dt->ev_cout, cs));
+      CU(cudaStreamWaitEvent(st, dt->ev_cout, 0));
+      return sliced_body<T>(pl, dt, begin, end, wsv, ws_bytes, st, partials_dev);
+    }
+    rec.launches = captured;
+    std::lock_guard<std::mutex> lk(pl->mu);
+    dt->graphs[key] = rec;
+  }
+  CU(cudaGraphLaunch(rec.exec, cs));
+  CU(cudaEventRecord(dt->ev_cout, cs));
+  CU(cudaStreamWaitEvent(st, dt->ev_cout, 0));
+  pl->all_launches += rec.launches;
+  pl->graph_launches++;
+  return TN_OK;
+}
+
+template <typename T>
+tn_status sliced_body(tn_plan* pl, DevTables* dt, uint64_t begin, uint64_t end, void* wsv, size_t ws_bytes,
+                      cudaStream_t st, double* partials_dev) {
+  tn_status s;
+  T* ws = static_cast<T*>(wsv);
   const ProgramRec& pr = pl->progs[0];
   if ((s = run_ops<T>(pl, *dt, pr.opA_begin, pr.opA_end, ws, 0, 0, st)) != TN_OK) return s;
   // batched slices: every per-slice step runs in the interpreter -> one launch

@@ -1,0 +1,12 @@
+python -c "import __graft_entry__ as g; g.build()"
+mkdir -p gpurun_out/r2n
+TNB_FC_TC=1 TNB_FT_TRACE=1 TNB_GEMM_DEBUG=1 timeout 300 python scripts/c5a_one_pass.py C5a 2 2>&1 | grep -a "k_fc_tc" | head -2
+TNB_FC_ATMA=0 TNB_FC_TC=1 TNB_FT_TRACE=1 timeout 300 python scripts/c5a_one_pass.py C5a 2 2>&1 | grep -a "k_fc_tc trace" | head -1
+TNB_FC_XLOAD=tma TNB_FC_TC=1 TNB_FT_TRACE=1 timeout 300 python scripts/c5a_one_pass.py C5a 2 2>&1 | grep -a "k_fc_tc trace" | head -1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "feed or fc_tc or graph" > gpurun_out/r2n/pytest_fc.log 2>&1
+tail -2 gpurun_out/r2n/pytest_fc.log
+TNB_FC_ATMA=0 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "fc_tc" > gpurun_out/r2n/pytest_fc2.log 2>&1
+tail -1 gpurun_out/r2n/pytest_fc2.log
+TNB_FC_TC=1 timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2n/bench_tc1.json 2> gpurun_out/r2n/bench_tc1.err
+python -c "
+import json; d=json.load(open('gpurun_out/r2n/bench_tc1.json')); r=d['roofline']; print('TC=1 VALUE', d['value'], 'e2e', d['e2e']['value'], r['kernel'], r['avg_launch_ms']); print(json.dumps(r['families']))"
