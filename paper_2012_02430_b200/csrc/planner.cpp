@@ -1094,9 +1094,15 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
           ops2.push_back(op);
           continue;
         }
+        // only chains on inputs of >= 2^run_chain_min elements pay for their own launch; shorter
+        // ones stay in the interpreter run (TNB_RUN_CHAIN_MIN, default 15)
+        static const int run_chain_min = [] {
+          const char* e = std::getenv("TNB_RUN_CHAIN_MIN");
+          return e ? std::atoi(e) : 15;
+        }();
         int i = op.begin, run_start = op.begin;
         while (i < op.end) {
-          if (is_reduce(out.steps[i])) {
+          if (is_reduce(out.steps[i]) && (int)out.steps[i].in[0].rank >= run_chain_min) {
             int j = i + 1;
             while (j < op.end && j - i < kMaxChain && out.steps[j].inplace && is_reduce(out.steps[j]) &&
                    out.steps[j].in[0].off == out.steps[j - 1].out_off)
