@@ -262,9 +262,19 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
     }
     int np = 0;
     for (int k = 0; k < M3; ++k) ma.perm[np++] = (uint8_t)ybit[yo[k]];
+    // TNB_FC_XFIRST=1: output bits the consumer factor X lacks right after the y bits, so the
+    // consumer blocks reading the same X values run back to back -- measured worse on C5a (DRAM
+    // 668 vs ~430 MB per launch: A's and B's chunks then change every block; 89.0 vs 90.4 /s), off
+    static const bool xfirst = env_flag("TNB_FC_XFIRST");
+    uint64_t xlack = 0;
+    if (xfirst && fa.nv == 1)
+      for (int b = 0; b < R3; ++b)
+        if (!((fa.vmask[0] >> b) & 1) && !(((tmask | ymask) >> b) & 1)) xlack |= 1ull << b;
+    for (int b = 0; b < R; ++b)
+      if ((xlack >> b) & 1) ma.perm[np++] = (uint8_t)b;
     for (int pass = 0; pass < 3; ++pass)
       for (int b = 0; b < R; ++b) {
-        if (((tmask | ymask) >> b) & 1) continue;
+        if (((tmask | ymask | xlack) >> b) & 1) continue;
         const uint64_t cls = pass == 0 ? ca : pass == 1 ? cb : (cc | cn);
         if ((cls >> b) & 1) ma.perm[np++] = (uint8_t)b;
       }

@@ -1095,10 +1095,11 @@ LoweredProgram lower(const Network& net, const Schedule& sch, int small_log2, st
           continue;
         }
         // only chains on inputs of >= 2^run_chain_min elements pay for their own launch; shorter
-        // ones stay in the interpreter run (TNB_RUN_CHAIN_MIN, default 15)
+        // ones stay in the interpreter run (TNB_RUN_CHAIN_MIN, default 10: C5a's 2^13 -> 2^5 chain
+        // keeps its launch (9 us; 41 us in the one-CTA interpreter), the 2^5 -> 1 tail joins the run)
         static const int run_chain_min = [] {
           const char* e = std::getenv("TNB_RUN_CHAIN_MIN");
-          return e ? std::atoi(e) : 15;
+          return e ? std::atoi(e) : 10;
         }();
         int i = op.begin, run_start = op.begin;
         while (i < op.end) {
