@@ -10,7 +10,7 @@ namespace tnb {
 
 constexpr size_t kTcSmemLimit = 220 * 1024;   // + ~6 KB static <= 227 KB per block
 
-// In a plan the tensor-core path is opt-in (TNB_GEMM_TC=1): measured slower than k_gemm_ws on the
+// In a plan the tensor-core path is opt-in (TNB_GEMM_TC=1): measured slower than the FP32 k_gemm kernels on the
 // C5a groups ("k_gemm_tc"); tn_eliminate_group(kernel = 4) always takes it.
 bool gemm_tc_enabled() {
   static const bool on = env_flag("TNB_GEMM_TC");
