@@ -17,7 +17,6 @@ void launch_m(const MArgs& ma, unsigned grid, size_t smem, cudaStream_t st) {
 
 template <int M, int WB>
 bool dispatch_m(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, cudaStream_t st) {
-  if (rab == 3 && rbb == 2) { launch_m<M, 3, 2, WB>(ma, grid, smem, st); return true; }
   if (rab == 2 && rbb == 2) { launch_m<M, 2, 2, WB>(ma, grid, smem, st); return true; }
   if (rab == 2 && rbb == 1) { launch_m<M, 2, 1, WB>(ma, grid, smem, st); return true; }
   if (rab == 1 && rbb == 2) { launch_m<M, 1, 2, WB>(ma, grid, smem, st); return true; }
@@ -25,13 +24,6 @@ bool dispatch_m(const MArgs& ma, int rab, int rbb, unsigned grid, size_t smem, c
   return false;
 }
 
-inline bool gemm_ra3() {
-  static const bool on = [] {
-    const char* v = std::getenv("TNB_GEMM_RA3");   // measured slower on C5a (61 vs 66 /s): off
-    return v && v[0] == '1';
-  }();
-  return on;
-}
 
 // preferred CTA size: 2^WB warps (TNB_GEMM_WB = 2 or 3); 4-warp CTAs run 4 per SM (half the shared
 // memory each), 8-warp CTAs 2 per SM.  Default 2 since the 8-lane / fused-pair state (C5a 88.7 vs
@@ -49,7 +41,7 @@ inline int gemm_wb() {
 // register-blocked batched complex GEMM (k_gemm, c64).  Returns false when the shape does not
 // qualify (the caller then tries k_pair / k_group_t).
 template <typename T>
-bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB);
+bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, int WB);
 
 inline int gemm_min_m() {   // TNB_GEMM_MIN_M: groups summing fewer indices go to k_pair / k_group_t
   static const int v = [] {
@@ -61,28 +53,23 @@ inline int gemm_min_m() {   // TNB_GEMM_MIN_M: groups summing fewer indices go t
 
 template <typename T>
 bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
-  static const bool contig = env_flag("TNB_GEMM_CONTIG");
   if (g.M < gemm_min_m()) return false;
   if (std::is_same<T, float2>::value && gemm_tc_enabled() && try_launch_gemm_tc(g, st)) return true;
   // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
   const int wb0 = gemm_wb(), wb1 = 5 - wb0;
-  return (contig && try_launch_gemm_impl<T>(g, st, true, wb0)) || try_launch_gemm_impl<T>(g, st, false, wb0) ||
-         try_launch_gemm_impl<T>(g, st, false, wb1);
+  return try_launch_gemm_impl<T>(g, st, wb0) || try_launch_gemm_impl<T>(g, st, wb1);
 }
 
 template <typename T>
 bool try_launch_gemm_simt(const GDesc& g, cudaStream_t st) {
-  static const bool contig = env_flag("TNB_GEMM_CONTIG");
-  // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
   const int wb0 = gemm_wb(), wb1 = 5 - wb0;
-  return (contig && try_launch_gemm_impl<T>(g, st, true, wb0)) || try_launch_gemm_impl<T>(g, st, false, wb0) ||
-         try_launch_gemm_impl<T>(g, st, false, wb1);
+  return try_launch_gemm_impl<T>(g, st, wb0) || try_launch_gemm_impl<T>(g, st, wb1);
 }
 
 template <typename T>
-bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB) {
+bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, int WB) {
   if constexpr (!std::is_same<T, float2>::value) {
-    (void)g; (void)st; (void)contig; (void)WB;
+    (void)g; (void)st; (void)WB;
     return false;
   } else {
     if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) return false;
@@ -110,11 +97,11 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB) 
     for (int i = 0; i < nra; ++i) used |= 1ull << ra[i];
     for (int i = 0; i < nrb; ++i) used |= 1ull << rb[i];
     int wb[3], nw = 0;
-    // warp bits: the lowest free a/b bits (reuse), or with TNB_GEMM_CONTIG=1 the lowest free bits of
-    // any class (a more contiguous tile: its 256-byte store segments closer together in HBM)
-    for (int pass = contig ? 1 : 0; pass < 2 && nw < WB; ++pass)
+    // warp bits: the lowest free a/b bits (reuse), then c bits (round 1's TNB_GEMM_CONTIG -- the
+    // lowest free bits of any class for a more contiguous tile -- measured slower and was removed)
+    for (int pass = 0; pass < 2 && nw < WB; ++pass)
       for (int b = 5; b < R && nw < WB; ++b) {
-        const uint64_t cls = pass == 0 ? (ca | cb) : (contig ? (ca | cb | cc) : cc);
+        const uint64_t cls = pass == 0 ? (ca | cb) : cc;
         if (!((used >> b) & 1) && ((cls >> b) & 1)) { wb[nw++] = b; used |= 1ull << b; }
       }
     if (nw < WB) return false;
@@ -131,27 +118,6 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB) 
         std::swap(ra, rb);
         std::swap(nra, nrb);
       }
-    }
-    // an 8 x 4 register block when A has a third exclusive bit to spare (TNB_GEMM_RA3=1; off by
-    // default -- 128 registers, measured slower):
-    // half the shared loads per FFMA2 and the per-tile overhead spread over twice the outputs
-    if (nra == 2 && nrb == 2 && gemm_ra3()) {
-      for (int b = 5; b < R; ++b)
-        if (((ca >> b) & 1) && !((used >> b) & 1)) { ra[nra++] = b; used |= 1ull << b; break; }
-      bool ok3 = nra == 3 && R >= 5 + WB + nra + nrb;
-      if (ok3) {   // shared memory of the larger tile at two ring slots must fit the budget
-        auto rows = [&](const GIn& in) {
-          std::vector<uint64_t> parts;
-          for (int x = 0; x < (1 << g.M); ++x)
-            if (std::find(parts.begin(), parts.end(), in.gx[x]) == parts.end()) parts.push_back(in.gx[x]);
-          return (uint64_t)parts.size();
-        };
-        const uint64_t na = rows(g.in[ia]) << __builtin_popcountll(used & g.in[ia].out_mask);
-        const uint64_t nb = rows(g.in[ib]) << __builtin_popcountll(used & g.in[ib].out_mask);
-        const uint64_t need = 2 * (na + nb) * 8 + (na + nb) * 4 + ((16ull << g.M) << __builtin_popcountll(used & g.in[ib].out_mask)) + 16;
-        ok3 = need <= (WB == 3 ? kGemmSmemBudget : kGemmSmemBudget / 2);
-      }
-      if (nra == 3 && !ok3) { used &= ~(1ull << ra[2]); --nra; }
     }
     const GIn& A = g.in[ia];
     const GIn& Bq = g.in[ib];
@@ -238,13 +204,12 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, bool contig, int WB) 
     if (smem > budget) return false;
     // traversal of the tile index: a-only bits first (B chunk and B' unchanged), then b-only, then
     // the rest
-    // (TNB_GEMM_BFIRST=1: b-only bits first -- A's chunk stays, B and B' change every tile)
-    static const bool bfirst = env_flag("TNB_GEMM_BFIRST");
+    // (b-only bits first -- round 1's TNB_GEMM_BFIRST -- measured slower: B and B' change every tile)
     int np = 0;
     for (int pass = 0; pass < 3; ++pass)
       for (int b = 0; b < R; ++b) {
         if ((tmask >> b) & 1) continue;
-        const uint64_t cls = pass == 0 ? (bfirst ? cb : ca) : pass == 1 ? (bfirst ? ca : cb) : (cc | cn);
+        const uint64_t cls = pass == 0 ? ca : pass == 1 ? cb : (cc | cn);
         if ((cls >> b) & 1) ma.perm[np++] = (uint8_t)b;
       }
     if (np != R - TB) return false;
