@@ -49,6 +49,9 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
   constexpr int TL = 5 + WB;               // 5 lane bits + WB warp bits
   constexpr int K = 1 << M, RA = 1 << RAB, RB = 1 << RBB;
   constexpr int TB = TL + RAB + RBB;
+  // consumer loads X at x = XV * K / 2: after the GEMM (2) with 4 x 4 blocks (earlier spills), at
+  // the start of the tile (0) with 4 x 2 blocks (the loads then overlap the tile's GEMM)
+  constexpr int XV = RBB <= 1 ? 0 : FC_XV_AT;
   constexpr int NB = 64 - TB;
   const uint32_t tid = threadIdx.x;
   const uint64_t n_tiles = 1ull << (a.out_rank - TB);
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
     float2 xv[kFcMaxV][RA][RB];
 #pragma unroll
     for (int x = 0; x < K; ++x) {
-      if (x == (FC_XV_AT * K) / 2) {
+      if (x == (XV * K) / 2) {
 #pragma unroll
         for (int v = 0; v < kFcMaxV; ++v)
           if (v < f.nv) {
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
           asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][j]) : "l"(f2_pack(av[i].y, av[i].y)), "l"(f2_pack(bv[j].z, bv[j].w)));
         }
     }
-    if (FC_XV_AT == 2) {   // after the GEMM
+    if (XV == 2) {   // after the GEMM
 #pragma unroll
       for (int v = 0; v < kFcMaxV; ++v)
         if (v < f.nv) {
