@@ -47,7 +47,8 @@ namespace tnb {
 constexpr int kFtRows = 7;                       // MMA M = 128
 constexpr int kFtMaxTrav = 40;                   // traversal bits
 constexpr int kFtEpi = 4, kFtLd = 4;
-constexpr int kFtThreads = (kFtEpi + kFtLd + 2) * 32;   // + the MMA warp and the producer warp
+constexpr int kFtXw = 2;                         // X-tile loader warps
+constexpr int kFtThreads = (kFtEpi + kFtLd + 2 + kFtXw) * 32;   // + the MMA warp, the producer warp, X loaders
 
 struct FTArgs {
   const float2* A;
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kFtThreads, 1) k_fc_tc(const FTArgs a, const _
     }
     for (int s = 0; s < 4; ++s) {
       // X tile: the producer's TMA expect_tx (1 arrival) or its 32 lanes' cp.async arrivals
-      tc_mbar_init(&x_full[s], a.tma ? 1 : 32);
+      tc_mbar_init(&x_full[s], a.tma ? 1 : 32 * kFtXw);
       tc_mbar_init(&x_empty[s], kFtEpi);
       // raw A / B / C chunk: 32 cp.async arrivals of the producer lanes (+ 1 expect_tx for TMA A)
       tc_mbar_init(&raw_full[s], a.atma ? 33 : 32);
@@ -259,6 +260,61 @@ __global__ void __launch_bounds__(kFtThreads, 1) k_fc_tc(const FTArgs a, const _
       }
       __syncwarp();
     }
+  } else if (warp >= kFtEpi + kFtLd + 2) {
+    // ================================ X loader warps: the X tile of each line group (the 2^NL
+    // units sharing X's and A's DRAM lines) into X slot g % SX once the epilogue released it --
+    // coalesced 16-byte cp.async pieces in the [line][column][row] layout (the epilogue's reads are
+    // then conflict-free) split over the loader warps, or TMA boxes issued by the first one
+    const int xw = warp - (kFtEpi + kFtLd + 2);
+    uint32_t ts0[5], tm0[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) { ts0[d] = a.ts[0][d]; tm0[d] = a.tmsk[0][d]; }
+    const int ncx = a.ncopy[0];
+    const uint32_t cex = a.copy_elems[0];
+    uint32_t lX[NLS];
+#pragma unroll
+    for (int li = 0; li < NLS; ++li) lX[li] = trav_at(FT_X, (uint64_t)li);
+    uint32_t xp_g = 0, xp_s = 0;       // this lane's X piece: global / smem offsets of the low 5 piece bits
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+      if ((lane >> b) & 1) { xp_g += a.xp_g[b]; xp_s += a.xp_s[b]; }
+    const uint32_t nG = nU >> NL;
+    for (uint32_t g = 0; g < nG; ++g) {
+      const uint64_t u = u0 + ((uint64_t)g << NL);
+      const uint32_t iX = trav_at(FT_X, u);
+      const int xsl = (int)(g % (uint32_t)SX);
+      float2* xs = reinterpret_cast<float2*>(dsm_ft + a.sm_x + (uint32_t)xsl * X_TILE * NLS);
+      if (g >= (uint32_t)SX) tc_mbar_wait(&x_empty[xsl], ((g / SX) - 1) & 1u);
+      if (a.tma) {
+        if (xw == 0 && lane == 0) {
+          uint32_t c[5];
+          ft_expect_tx(&x_full[xsl], (uint32_t)ncx * cex * 8u);
+          for (int i = 0; i < ncx; ++i) {
+#pragma unroll
+            for (int d = 0; d < 5; ++d) c[d] = ((iX >> ts0[d]) & tm0[d]) + a.cdelta[0][i][d];
+            ft_tma5(xs + (size_t)i * cex, &tmX, c, &x_full[xsl]);
+          }
+        }
+      } else {
+        if (a.xp_bits >= 5) {
+          const uint32_t* hi = reinterpret_cast<const uint32_t*>(dsm_ft + a.sm_xp);
+          for (int k = xw; k < (1 << (a.xp_bits - 5)); k += kFtXw)
+            cp_async16(xs + xp_s + hi[2 * k + 1], a.X + iX + xp_g + hi[2 * k]);
+        } else {
+#pragma unroll
+          for (int li = 0; li < NLS; ++li) {
+            float2* xl = xs + li * (X_TILE / 8);
+            for (int p = lane + 32 * xw; p < 128 * NCOL; p += 32 * kFtXw) {
+              const int r = p & 127, c = p >> 7;
+              cp_async8(xl + c * 128 + r, a.X + iX + lX[li] + t_xrow[r] + t_xcol[c]);
+            }
+          }
+        }
+        mbar_cp_async_arrive(&x_full[xsl]);
+      }
+      if (lane == 0 && xw == 0) FT_TR(g, 5);
+    }
+    cp_async_wait<0>();
   } else if (warp == kFtEpi + kFtLd + 1) {
     // ================================ producer warp.  Per line group (the 2^NL units sharing X's
     // and A's DRAM lines): the X tile into X slot g % SX (coalesced 16-byte cp.async pieces in the
@@ -297,38 +353,6 @@ __global__ void __launch_bounds__(kFtThreads, 1) k_fc_tc(const FTArgs a, const _
     }
     for (uint32_t v = 0; v < nU; ++v) {
       const uint64_t u = u0 + v;
-      if ((v & (NLS - 1)) == 0) {      // a new line group: its X tile
-        const uint32_t g = v >> NL;
-        const int xsl = (int)(g % (uint32_t)SX);
-        float2* xs = reinterpret_cast<float2*>(dsm_ft + a.sm_x + (uint32_t)xsl * X_TILE * NLS);
-        if (g >= (uint32_t)SX) tc_mbar_wait(&x_empty[xsl], ((g / SX) - 1) & 1u);
-        if (a.tma) {
-          if (lane == 0) {
-            uint32_t c[5];
-            ft_expect_tx(&x_full[xsl], (uint32_t)ncx * cex * 8u);
-            for (int i = 0; i < ncx; ++i) {
-#pragma unroll
-              for (int d = 0; d < 5; ++d) c[d] = ((iX >> ts0[d]) & tm0[d]) + a.cdelta[0][i][d];
-              ft_tma5(xs + (size_t)i * cex, &tmX, c, &x_full[xsl]);
-            }
-          }
-        } else if (a.xp_bits >= 5) {
-          const uint32_t* hi = reinterpret_cast<const uint32_t*>(dsm_ft + a.sm_xp);
-          for (int k = 0; k < (1 << (a.xp_bits - 5)); ++k)
-            cp_async16(xs + xp_s + hi[2 * k + 1], a.X + iX + xp_g + hi[2 * k]);
-          mbar_cp_async_arrive(&x_full[xsl]);
-        } else {
-#pragma unroll
-          for (int li = 0; li < NLS; ++li) {
-            float2* xl = xs + li * (X_TILE / 8);
-            for (int p = lane; p < 128 * NCOL; p += 32) {
-              const int r = p & 127, c = p >> 7;
-              cp_async8(xl + c * 128 + r, a.X + iX + lX[li] + t_xrow[r] + t_xcol[c]);
-            }
-          }
-          mbar_cp_async_arrive(&x_full[xsl]);
-        }
-      }
       const int sl = (int)(v % (uint32_t)S);
       float2* ra = reinterpret_cast<float2*>(raw + sl * raw_slot);
       float2* rb = reinterpret_cast<float2*>(raw + sl * raw_slot + A_RAW);
@@ -369,7 +393,6 @@ __global__ void __launch_bounds__(kFtThreads, 1) k_fc_tc(const FTArgs a, const _
         trav_step(FT_X, iX, u);
         if (has_c) trav_step(FT_C + cq, iC, u);
       }
-      if (lane == 0) FT_TR(v, 5);
     }
     cp_async_wait<0>();
   } else if (warp >= kFtEpi) {

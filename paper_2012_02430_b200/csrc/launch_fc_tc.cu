@@ -370,11 +370,11 @@ bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
     std::memset(&mp, 0, sizeof(mp));
     fa.tma = 0;
     {
-      // X tile loads: TMA boxes in the tensor's own bit order (default), or (TNB_FC_XLOAD=cp)
-      // coalesced 16-byte cp.async pieces in the [line][column][row] layout when row bit 0 pairs X
-      // elements (conflict-free epilogue reads; measured slower: 3,290 vs 2,309 cycles per unit)
+      // X tile loads: coalesced 16-byte cp.async pieces in the [line][column][row] layout when row
+      // bit 0 pairs X elements (default: conflict-free epilogue reads; 2,016 cycles per unit with
+      // two loader warps), or (TNB_FC_XLOAD=tma) TMA boxes in the tensor's own bit order (2,257)
       const char* e = std::getenv("TNB_FC_XLOAD");
-      const bool want = !(e && std::strcmp(e, "cp") == 0);
+      const bool want = e && std::strcmp(e, "tma") == 0;
       fa.xp_bits = 0;
       const int RX = (int)Xin.rank, RA = (int)A.rank;
       std::vector<char> bx(RX, 0), ba(RA, 0);
