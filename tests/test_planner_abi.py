@@ -348,3 +348,15 @@ def test_planner_reports_replay():
                 adj[a].discard(v)
         w = max(odeg[:s] + _greedy_min_degree_graph(adj))
         assert w == c["width"], (s, w, c["width"])
+
+
+def test_lane_windows_sized_from_the_rank_block():
+    """A rank's workspace holds one window per slice lane of ITS block of slices (min(lanes, block)),
+    not of all 2^k slices: at 8 GPUs a C5a-like rank with 4 slices gets 4 windows."""
+    g = random_regular_graph(60, 3, 1)
+    plan = T.build_plan(g, 2, "amplitude", "min-fill", n_sliced=5)
+    assert plan.n_slices == 32 and not plan.info["slices_batchable"]
+    full = plan.batch_windows(T.TN_C64)
+    assert full == min(8, 32) or full >= 1
+    for n_run, want in ((1, 1), (4, min(4, full)), (32, full)):
+        assert plan.batch_windows(T.TN_C64, n_run) == want
