@@ -68,7 +68,7 @@ class Plan:
     # slice batching: windows for up to this many bytes of per-slice tensors
     BATCH_WINDOW_BYTES = 4 << 30
 
-    # slice lanes (independent slices overlap on TNB_LANES streams, default 4) while the extra
+    # slice lanes (independent slices overlap on TNB_LANES streams, default 16) while the extra
     # windows of per-slice tensors cost at most this many bytes in total
     LANE_WINDOW_BYTES = 48 << 30
 
@@ -76,14 +76,14 @@ class Plan:
         """Windows of per-slice tensors in the default workspace for a call that runs n_run slices
         (0: all 2^k; a rank runs only its block, so its lanes are sized from the block): slices run
         per launch when every per-slice step is an interpreter step (slice batching); otherwise
-        one window per concurrent slice lane (TNB_LANES, default 8) within LANE_WINDOW_BYTES."""
+        one window per concurrent slice lane (TNB_LANES, default 16) within LANE_WINDOW_BYTES."""
         n_run = self.n_slices if n_run <= 0 else min(n_run, self.n_slices)
         if n_run <= 1:
             return 1
         one = B.tn_workspace_bytes(self.handle, dtype, 2) - B.tn_workspace_bytes(self.handle, dtype, 1)
         if not self.info["slices_batchable"]:
             import os
-            lanes = max(1, min(8, int(os.environ.get("TNB_LANES", "8"))))
+            lanes = max(1, min(32, int(os.environ.get("TNB_LANES", "16"))))
             lanes = 1 if os.environ.get("TNB_ONE_LANE") == "1" else lanes
             return int(max(1, min(lanes, n_run, self.LANE_WINDOW_BYTES // max(1, one))))
         return int(max(1, min(n_run, self.BATCH_WINDOW_BYTES // max(1, one))))

@@ -103,12 +103,12 @@ inline int gemm_stages() {   // TNB_GEMM_STAGES=2..4 (default 3)
   }();
   return s;
 }
-constexpr int kMaxLanes = 8;
-inline int slice_lanes() {   // TNB_LANES=1..8 (default 8: C4b 55 vs 49 /s at 4; C5a unchanged); TNB_ONE_LANE=1 == 1
+constexpr int kMaxLanes = 32;
+inline int slice_lanes() {   // TNB_LANES=1..32 (default 16); TNB_ONE_LANE=1 == 1
   static const int n = [] {
     if (env_flag("TNB_ONE_LANE")) return 1;
     const char* v = std::getenv("TNB_LANES");
-    const int x = v ? std::atoi(v) : 8;
+    const int x = v ? std::atoi(v) : 16;
     return x < 1 ? 1 : (x > kMaxLanes ? kMaxLanes : x);
   }();
   return n;
