@@ -1309,6 +1309,32 @@ __global__ void __launch_bounds__(kProgramThreads) k_program(const StepRec* __re
   }
 }
 
+// energy (§8 a12): one CTA per light cone (x) and angle set (y), as k_program mode 1, with the cone's
+// whole arena -- leaves included -- copied into shared memory first, so the ~150-200 small steps of
+// a cone read and write shared memory instead of L2 (the host launches it when the largest
+// cone arena fits)
+template <typename T>
+__global__ void __launch_bounds__(kProgramThreads) k_cone_smem(const StepRec* __restrict__ steps,
+                                                               const ProgramRec* __restrict__ progs,
+                                                               const ScalarRec* __restrict__ scal, const T* ws,
+                                                               double2* results, uint64_t win0, uint64_t win_elems) {
+  extern __shared__ __align__(16) unsigned char dsm_cone[];
+  T* sm = reinterpret_cast<T*>(dsm_cone);
+  const ProgramRec& pr = progs[blockIdx.x];
+  const uint64_t rel = window_rel(blockIdx.y, win0, win_elems);
+  const uint64_t a0 = pr.arena_begin, n = pr.arena_end - pr.arena_begin;
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) sm[i] = ws[rel + a0 + i];
+  __syncthreads();
+  T* base = sm - a0;   // every tensor of the cone at its arena offset
+  for (int s = pr.stepB_begin; s < pr.stepB_end; ++s) {
+    run_step<T>(steps[s], base, 0, 0ull, true);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    results[(uint64_t)blockIdx.y * gridDim.x + blockIdx.x] =
+        final_product<T>(scal, pr.scal_begin, pr.scal_end, base, 0, pr.log2_scale, 0ull, true);
+}
+
 // per slice: the product of the final factors in FP64 x 2^{log2_scale}; with open indices (§6)
 // thread o computes batch entry o (element pext(o, open_mask) of every factor)
 template <typename T>

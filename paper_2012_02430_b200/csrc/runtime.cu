@@ -1076,8 +1076,25 @@ tn_status energy_impl(tn_plan* pl, const double* gammas, const double* betas, in
                                            pl->h.arena_elems);
   }
   dim3 grid((unsigned)E, (unsigned)B);
-  k_program<T><<<grid, kProgramThreads, 0, st>>>(dt->steps, 0, 0, ws, 0, dt->progs, dt->scalars, results, 1,
-                                                 win0, pl->h.arena_elems);
+  // shared-memory-resident cones for a single angle set when the largest cone arena fits (C3 c64:
+  // 237 vs 296 us per call); batches keep the L2 path, whose CTAs share an SM (C3 c64 batch of 256:
+  // 55 vs 111 us per energy with 187 KB cones); TNB_CONE_SMEM=0: always the L2 path
+  uint64_t max_arena = 0;
+  for (const auto& pr : pl->progs) max_arena = std::max<uint64_t>(max_arena, pr.arena_end - pr.arena_begin);
+  const size_t cone_bytes = (size_t)max_arena * es;
+  static const bool cone_smem = !(std::getenv("TNB_CONE_SMEM") && std::getenv("TNB_CONE_SMEM")[0] == '0');
+  if (cone_smem && B == 1 && cone_bytes <= 200 * 1024) {
+    if (cone_bytes > 48 * 1024) {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      CU(cudaFuncSetAttribute(k_cone_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    }
+    k_cone_smem<T><<<grid, kProgramThreads, cone_bytes, st>>>(dt->steps, dt->progs, dt->scalars, ws, results, win0,
+                                                              pl->h.arena_elems);
+  } else {
+    k_program<T><<<grid, kProgramThreads, 0, st>>>(dt->steps, 0, 0, ws, 0, dt->progs, dt->scalars, results, 1,
+                                                   win0, pl->h.arena_elems);
+  }
   pl->all_launches += 2;
   CU(cudaGetLastError());
   std::vector<double> h(2 * (size_t)E * B);
