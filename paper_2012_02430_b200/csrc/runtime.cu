@@ -94,6 +94,7 @@ struct tn_plan {
   uint64_t all_launches = 0;
   uint64_t graph_launches = 0;   // cudaGraphLaunch calls (each replays a captured slice range)
   bool batchable = false;   // every per-slice op is an interpreter run -> slices can run batched
+  std::vector<int32_t> waveA;   // per op: wave of independent prefix ops (-1: phase B), see prefix_waves
   ~tn_plan() {
     for (auto& kv : dev) {
       cudaSetDevice(kv.first);
@@ -851,9 +852,76 @@ tn_status check_call(const tn_plan* plan, int dtype, const double* gamma, const 
   return TN_OK;
 }
 
+// Prefix (phase A) ops in waves: consecutive ops that neither read nor write memory another op of
+// the wave writes (the planner level-sorts phase A and releases a level's memory only when the level
+// ends, so the ops of one dependency level form a wave).  A wave of >= 2 ops runs on forked streams:
+// the prefix's critical path becomes its dependency depth instead of its op count.
+inline void prefix_waves(tn_plan* pl) {
+  std::lock_guard<std::mutex> lk(pl->mu);
+  if (!pl->waveA.empty()) return;
+  pl->waveA.assign(pl->ops.size(), -1);
+  std::vector<std::pair<uint64_t, uint64_t>> rd, wr;
+  int wave = 0;
+  auto hit = [](const std::vector<std::pair<uint64_t, uint64_t>>& v, uint64_t lo, uint64_t hi) {
+    for (const auto& x : v)
+      if (lo < x.second && x.first < hi) return true;
+    return false;
+  };
+  for (size_t oi = 0; oi < pl->ops.size(); ++oi) {
+    const OpRec& op = pl->ops[oi];
+    if (op.phase != 0) continue;
+    std::vector<std::pair<uint64_t, uint64_t>> r2, w2;
+    for (int si = op.begin; si < op.end; ++si) {
+      const StepRec& st = pl->steps[si];
+      w2.push_back({st.out_off, st.out_off + (1ull << st.out_rank)});
+      for (int t = 0; t < st.n_in; ++t)
+        r2.push_back({st.in[t].off, st.in[t].off + (1ull << (st.in[t].rank + __builtin_popcount(st.in[t].slice_mask)))});
+    }
+    bool conflict = false;
+    for (const auto& x : w2) conflict = conflict || hit(rd, x.first, x.second) || hit(wr, x.first, x.second);
+    for (const auto& x : r2) conflict = conflict || hit(wr, x.first, x.second);
+    if (conflict) { ++wave; rd.clear(); wr.clear(); }
+    rd.insert(rd.end(), r2.begin(), r2.end());
+    wr.insert(wr.end(), w2.begin(), w2.end());
+    pl->waveA[oi] = wave;
+  }
+}
+
 template <typename T>
 tn_status sliced_body(tn_plan* pl, DevTables* dt, uint64_t begin, uint64_t end, void* wsv, size_t ws_bytes,
                       cudaStream_t st, double* partials_dev);
+
+// phase A: waves of independent ops on forked streams (TNB_PREFIX_WAVES=0: one stream)
+template <typename T>
+tn_status run_prefix(tn_plan* pl, DevTables* dt, int op_b, int op_e, T* ws, cudaStream_t st) {
+  static const bool waves = !(std::getenv("TNB_PREFIX_WAVES") && std::getenv("TNB_PREFIX_WAVES")[0] == '0');
+  if (!waves || pl->profiling) return run_ops<T>(pl, *dt, op_b, op_e, ws, 0, 0, st);
+  prefix_waves(pl);
+  tn_status s;
+  int oi = op_b;
+  while (oi < op_e) {
+    int oe = oi + 1;
+    while (oe < op_e && pl->waveA[oe] == pl->waveA[oi]) ++oe;
+    const int n = std::min(oe - oi, kMaxLanes);
+    if (n < 2) {
+      if ((s = run_ops<T>(pl, *dt, oi, oe, ws, 0, 0, st)) != TN_OK) return s;
+      oi = oe;
+      continue;
+    }
+    CU(cudaEventRecord(dt->ev_fork, st));
+    for (int k = 1; k < n; ++k) CU(cudaStreamWaitEvent(dt->side[k - 1], dt->ev_fork, 0));
+    for (int k = 0; k < oe - oi; ++k) {
+      cudaStream_t sk = (k % n) == 0 ? st : dt->side[(k % n) - 1];
+      if ((s = run_ops<T>(pl, *dt, oi + k, oi + k + 1, ws, 0, 0, sk)) != TN_OK) return s;
+    }
+    for (int k = 1; k < n; ++k) {
+      CU(cudaEventRecord(dt->ev_join[k - 1], dt->side[k - 1]));
+      CU(cudaStreamWaitEvent(st, dt->ev_join[k - 1], 0));
+    }
+    oi = oe;
+  }
+  return TN_OK;
+}
 
 inline bool graphs_enabled() {
   const char* v = std::getenv("TNB_GRAPH");
@@ -939,7 +1007,7 @@ tn_status sliced_body(tn_plan* pl, DevTables* dt, uint64_t begin, uint64_t end, 
   tn_status s;
   T* ws = static_cast<T*>(wsv);
   const ProgramRec& pr = pl->progs[0];
-  if ((s = run_ops<T>(pl, *dt, pr.opA_begin, pr.opA_end, ws, 0, 0, st)) != TN_OK) return s;
+  if ((s = run_prefix<T>(pl, dt, pr.opA_begin, pr.opA_end, ws, st)) != TN_OK) return s;
   // batched slices: every per-slice step runs in the interpreter -> one launch
   // runs up to nb slices, each CTA in its own window for the per-slice tensors
   const size_t es = sizeof(T);
