@@ -236,8 +236,11 @@ tn_status tn_eliminate(tn_dtype dtype, int32_t n_in, const void* const* in_dev,
  * (register-blocked batched complex GEMM on the FP32 pipes, c64 only), 2 = k_pair, 3 = k_group_t,
  * 4 = k_gemm_tc (the same GEMM on the tensor cores: tcgen05.mma kind::tf32 with a 3xTF32 split,
  * accumulators in TMEM; c64 only; needs >= 7 output bits held by one operand only, >= 3 by the
- * other only, 2 <= ... <= 32 summed values per tile row fitting shared memory); TN_E_INVAL when the
- * requested kernel does not take this shape.  Asynchronous on `stream`. */
+ * other only, 2 <= ... <= 32 summed values per tile row fitting shared memory), 5 = k_gemm_hm (the
+ * same GEMM on the warp-level tensor cores: mma.sync m16n8k8 tf32 with a 3xTF32 split; c64 only;
+ * needs M >= 2, out_rank >= 14, >= 4 output bits held by one operand only and >= 2 by the other
+ * only, output bits 0 and 1 held by an operand, inputs other than the two holding no output bit);
+ * TN_E_INVAL when the requested kernel does not take this shape.  Asynchronous on `stream`. */
 tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in, const void* const* in_dev,
                              const uint64_t* out_mask, const uint32_t* x_mask, void* out_dev,
                              int32_t out_rank, int32_t kernel, void* stream);
@@ -254,7 +257,8 @@ tn_status tn_profile_read(tn_plan* plan, uint64_t* launches, double* total_ms, d
  * step, 2 = fused reduce chain, 3 = fused merge group, 4 = run of small steps in one CTA), the
  * kernel that ran it (1 = k_bucket, 2 = k_chain, 3 = k_group_t, 4 = k_pair, 5 = k_gemm,
  * 6 = k_chain_split, 7 = k_program, 8 = k_gemm_tc, 9 = k_gemm_fc: a producer group computed inside
- * its consumer's launch, whose record spans both groups' steps), device milliseconds,
+ * its consumer's launch, whose record spans both groups' steps, 10 = k_fc_tc, 11 = k_gemm_hm),
+ * device milliseconds,
  * algorithmic bytes (inputs read once + output written once) and flops (8 x 2^(out_rank + M): one
  * complex multiply-add per output element and summed value).  out: host array of cap records
  * (may be NULL to query *n). */

@@ -1,0 +1,388 @@
+// kernels_hm.cuh -- k_gemm_hm: the two-operand merge group of k_gemm (a batched complex GEMM with
+// K = 2^M summed values; the re-associated bucket elimination of PAPER.md:361-368)
+// on the warp-level tensor cores: mma.sync.m16n8k8 kind tf32 with a 3xTF32 split.
+//
+//   out[o] = sum_{x < K} C[x] R[F_R(o) + G_R(x)] Q[F_Q(o) + G_Q(x)]
+//
+// R (the "row" operand) holds >= 4 output bits Q does not hold; Q (the "column" operand) >= 2 bits
+// R does not hold.  As a real GEMM per batch (bits held by both):
+//   [Re T, Im T][m][2j+f] = sum_{x,e} R'[m][2x+e] Q'[2x+e][2j+f],
+//   R'[m][2x+e] = (Re, Im)_e of R[m][x],
+//   Q'[2x][2j] = Re q, Q'[2x][2j+1] = Im q, Q'[2x+1][2j] = -Im q, Q'[2x+1][2j+1] = Re q  (q = C[x] Q[x][j]),
+// so the MMA's (c0, c1) are (Re, Im) of one complex output.  Every operand value v is split as
+// big = cvt.rna.tf32(v), small = v - big; D += Rs Qb + Rb Qs + Rb Qb (the dropped Rs Qs term is
+// ~2^-22 relative; measured 7e-7 against 7e-4 for one TF32 product, profiles/r01/tc/NOTES.md).
+//
+// Why mma.sync and not tcgen05 here: an MMA row of R is a set of R-only output bits whose elements
+// are scattered over R's bit order (SURVEY F5 layouts), so each thread gathers its fragment values
+// from the shared-memory chunk itself -- the register-fed warp MMA takes any row -> address map,
+// while tcgen05 needs canonical shared-memory tiles (the formatting pass that made k_fc_tc / k_gemm_tc
+// latency-bound).  What it buys over k_gemm's FFMA2: one HMMA does the work of
+// 16 FFMA2 at 3.8x the FP32 FMA rate (scripts/probe/mma_rate.cu), and k_gemm was bound by its
+// instruction stream (711 warp instructions per tile, issue 50 %, profiles/r02/hm/).
+//
+// Tile-local bits (HArgs.outbit order, chosen by launch_gemm_hm.cu):
+//   0, 1      tig bits (lane & 3): two Q-only bits = the MMA's complex column within an n8 block
+//   2, 3, 4   g bits (lane >> 2): three R-only bits = MMA rows 0..7
+//   5         r8: an R-only bit = MMA rows 8..15 (register slot 0)
+//   6 ..      WB warp bits
+//   then the fragment bits (register slots 1 ..): NFA R-only bits (row blocks), NFB Q-only bits
+//   (column blocks), NFC shared bits (batches): 2^(NFA+NFB+NFC) accumulator fragments of 16 x 8.
+// Output bits 0 and 1 are register slots (P0, P1), so each thread writes whole 32-byte sectors with
+// one 256-bit store: the MMA's lane -> output map alone would write half sectors (the low output
+// bits are often of the shared class), which HBM3e turns into read-modify-writes.
+// Warp roles: one producer warp (lane 0 arms a slot, the 32 lanes issue its copies) streams the R chunk of every tile and, when it changes,
+// the Q chunk -- every x-row, every tile bit the operand holds -- as cp.async.bulk copies of whole
+// contiguous runs into an S-slot ring per operand (full / empty mbarriers, no block-wide barrier);
+// 2^WB consumer warps each own a part of the tile.  A consumer keeps its Q fragments (split, in
+// fragment order, one float4 per lane per (column block, batch, k-step)) in shared memory, rebuilt
+// only when Q's chunk changes; R fragments are gathered from the raw chunk and split in registers.
+#pragma once
+#include "kernels.cuh"
+
+namespace tnb {
+
+struct HArgs {
+  void* out;
+  const void* in[2];                   // R (MMA rows), Q (MMA columns)
+  uint64_t mask[2];                    // F_t(o) = ins0(pext(o, mask_t), pv_t)
+  uint32_t pv[2];
+  uint8_t row[2][1 << kMaxGroup];      // x -> chunk row
+  uint32_t rowoff[2][1 << kMaxGroup];  // element offset G_t(x) of chunk row r (distinct x-part)
+  uint32_t posoff[2][kGemmMaxTB];      // element offset (within the operand) of chunk bit k
+  uint32_t nrows[2];                   // chunk rows (distinct x parts)
+  uint32_t nch[2];                     // tile bits held by the operand (chunk row = 2^nch elements)
+  uint32_t runl[2];                    // log2 elements of one contiguous run (one bulk copy), >= 1
+  int8_t chbit[2][kGemmMaxTB];         // tile-local bit u -> chunk bit (-1: absent)
+  uint8_t outbit[kGemmMaxTB];          // tile-local bit u -> output bit (all < 32)
+  uint8_t sbit[kGemmMaxTB];            // tile-local bit u -> staging bit (rank among the tile's output bits)
+  uint32_t sm_in[2][4];                // dynamic smem byte offset of ring slot (operand, slot)
+  uint32_t sm_run[2];                  // dynamic smem byte offset of the run table (element offset of run q)
+  uint32_t sm_q;                       // dynamic smem byte offset of the Q fragments
+  int32_t p0, p1;                      // register slots holding output bits 0 and 1
+  int32_t stages;                      // ring slots (2..4); lookahead = stages - 1 tiles
+  const void* cin[kMaxIn];             // constant inputs: no output bit (C[x] = prod_t cin[t][cgx[t][x]])
+  uint32_t cgx[kMaxIn][1 << kMaxGroup];
+  int32_t nc;
+  int32_t out_rank;
+  uint8_t perm[64];                    // logical tile-index bit b -> output bit (traversal order)
+};
+
+__device__ __forceinline__ void tf32_split(float v, uint32_t& big, uint32_t& small) {
+  uint32_t b;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v));
+  big = b;
+  small = __float_as_uint(v - __uint_as_float(b));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void hm_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void hm_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void hm_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n HM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra HM_WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void hm_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_v8_cs(float* p, const float (&v)[8]) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
+// The thread's 2^NR complex outputs (register slot 0 = r8: acc[f][0..1] / acc[f][2..3]; slots 1.. =
+// fragment index f) as 256-bit stores of the 4 values whose output bits 0 / 1 are slots P0 / P1.
+template <int P0, int P1, int NR, int NF>
+__device__ __forceinline__ void hm_store(float* ob, const float (&acc)[NF][4], const uint32_t (&so)[NR]) {
+#pragma unroll
+  for (int q = 0; q < (1 << NR); ++q) {
+    if (q & ((1 << P0) | (1 << P1))) continue;
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k)
+      if ((q >> k) & 1) o += so[k];
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int reg = q | ((e & 1) << P0) | ((e >> 1) << P1);
+      v[2 * e] = acc[reg >> 1][2 * (reg & 1)];
+      v[2 * e + 1] = acc[reg >> 1][2 * (reg & 1) + 1];
+    }
+    st_v8_cs(ob + 2 * (size_t)o, v);
+  }
+}
+
+template <int M, int NFA, int NFB, int NFC, int WB>
+__global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
+  constexpr int NW = 1 << WB;              // consumer warps; warp NW is the producer
+  constexpr int kThreads = 32 * NW + 32;
+  constexpr int K = 1 << M;
+  constexpr int KS = K / 4;                // k-steps of 8 real values (4 complex x)
+  constexpr int RA = 1 << NFA, RB = 1 << NFB, RC = 1 << NFC;
+  constexpr int NFR = NFA + NFB + NFC;     // fragment bits
+  constexpr int NF = 1 << NFR;
+  constexpr int NR = 1 + NFR;              // register slots (r8 + fragment bits)
+  constexpr int TB = 6 + WB + NFR;
+  constexpr int NB = 64 - TB;
+  static_assert(M >= 2 && M <= kMaxGroup, "k_gemm_hm: 2 <= M <= 5");
+  static_assert(NFR >= 1 && NFR <= 3, "k_gemm_hm: 1..3 fragment bits");
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+  const uint32_t g = lane >> 2, tig = lane & 3u;
+  const uint64_t n_tiles = 1ull << (a.out_rank - TB);
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ uint32_t fbit[2][NB];
+  __shared__ uint32_t fcum[2][NB + 1];
+  __shared__ uint64_t pbit[NB], pcum[NB + 1];
+  __shared__ float2 Cs[K];
+  __shared__ uint32_t rowf[K];             // R chunk row of x, in floats (row << nch, x 2)
+  __shared__ __align__(8) uint64_t bars[2][2][4];   // [full / empty][operand][slot]
+  const int nperm = a.out_rank - TB;
+  for (int i = tid; i < 2 * NB; i += kThreads) {
+    const int t = i / NB, b = i % NB;
+    fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], a.mask[t], a.pv[t]) : 0u;
+  }
+  for (int b = tid; b < NB; b += kThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
+  if (tid < (uint32_t)K) {
+    rowf[tid] = ((uint32_t)a.row[0][tid] << a.nch[0]) * 2u;
+    float2 c = make_float2(1.f, 0.f);
+    for (int t = 0; t < a.nc; ++t) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + a.cgx[t][tid]));
+    Cs[tid] = c;
+  }
+  // run tables: run q of operand u's chunk (2^runl contiguous elements) -> element offset from the base
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t lp = a.nch[u] - a.runl[u];
+    const uint32_t nr = a.nrows[u] << lp;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm + a.sm_run[u]);
+    for (uint32_t q = tid; q < nr; q += kThreads) {
+      const uint32_t w = (q & ((1u << lp) - 1u)) << a.runl[u];
+      uint32_t off = a.rowoff[u][q >> lp];
+      for (uint32_t k = a.runl[u]; k < a.nch[u]; ++k)
+        if ((w >> k) & 1u) off += a.posoff[u][k];
+      tab[q] = off;
+    }
+  }
+  if (tid == 0) {
+    for (int u = 0; u < 2; ++u)
+      for (int s = 0; s < a.stages; ++s) {
+        mbar_init(&bars[0][u][s], 1);
+        mbar_init(&bars[1][u][s], NW);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nbu = min(NB - 1, max(0, nperm));
+  if (tid < 2u) {
+    uint32_t c = 0;
+    fcum[tid][0] = 0;
+    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+  }
+  if (tid == 2u) {
+    uint64_t c = 0;
+    pcum[0] = 0;
+    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+  }
+  __syncthreads();
+  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t obase = 0;
+  for (int b = 0; b < nperm && (t0 >> b); ++b)
+    if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
+  const uint32_t bar_full = smem_u32(&bars[0][0][0]);   // + (u * 4 + slot) * 8
+  const uint32_t bar_empty = smem_u32(&bars[1][0][0]);
+  const int S = a.stages;
+
+  if (wid == (uint32_t)NW) {
+    // ---------------------------------------------------------------- producer warp: lane 0 arms
+    // the slot's full barrier, the 32 lanes issue the chunk's bulk copies
+    if (t0 < t1) {
+      uint32_t cur[2];
+      int ver[2] = {0, 0};
+      for (int u = 0; u < 2; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
+      const uint32_t* tab[2] = {reinterpret_cast<const uint32_t*>(dsm + a.sm_run[0]),
+                                reinterpret_cast<const uint32_t*>(dsm + a.sm_run[1])};
+      auto issue = [&](int u) {
+        const int v = ver[u], slot = v % S;
+        if (v >= S) hm_wait(bar_empty + (uint32_t)(u * 4 + slot) * 8u, (uint32_t)((v / S) - 1) & 1u);
+        const uint32_t nr = a.nrows[u] << (a.nch[u] - a.runl[u]);
+        const uint32_t bytes = 8u << a.runl[u];
+        const uint32_t bar = bar_full + (uint32_t)(u * 4 + slot) * 8u;
+        if (lane == 0) hm_expect_tx(bar, nr * bytes);
+        __syncwarp();
+        const float2* src = static_cast<const float2*>(a.in[u]) + cur[u];
+        const uint32_t dst = smem_u32(dsm + a.sm_in[u][slot]);
+        for (uint32_t q = lane; q < nr; q += 32) hm_bulk(dst + q * bytes, src + tab[u][q], bytes, bar);
+      };
+      issue(0);
+      issue(1);
+      for (uint64_t tile = t0; tile + 1 < t1; ++tile) {
+        const int r = __ffsll((long long)~tile) - 1;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (fbit[u][r] != fcum[u][r]) {
+            cur[u] = cur[u] + fbit[u][r] - fcum[u][r];
+            ++ver[u];
+            issue(u);
+          }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  auto chunk_off = [&](int u, int k) -> uint32_t { return a.chbit[u][k] >= 0 ? 1u << a.chbit[u][k] : 0u; };
+  auto obit = [&](int k) -> uint32_t { return 1u << a.outbit[k]; };
+  constexpr int FB0 = 6 + WB;              // tile-local index of the first fragment bit
+  uint32_t othr = 0, ia_thr = 0, ib_w = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if ((tig >> k) & 1u) othr += obit(k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if ((g >> k) & 1u) { othr += obit(2 + k); ia_thr += chunk_off(0, 2 + k); }
+#pragma unroll
+  for (int k = 0; k < WB; ++k)
+    if ((wid >> k) & 1u) { othr += obit(6 + k); ia_thr += chunk_off(0, 6 + k); ib_w += chunk_off(1, 6 + k); }
+  const uint32_t ia_r8 = chunk_off(0, 5) * 2u;
+  // output offset of each register slot (0 = r8, 1 + k = fragment bit k)
+  uint32_t so[NR];
+  so[0] = obit(5);
+#pragma unroll
+  for (int k = 0; k < NFR; ++k) so[1 + k] = obit(FB0 + k);
+  // Q fragment entry of this lane: column j = g >> 1 (tile bits 0, 1), f = g & 1, e = tig & 1
+  const uint32_t ib_lane = ib_w + (((g >> 1) & 1u) ? chunk_off(1, 0) : 0u) + (((g >> 2) & 1u) ? chunk_off(1, 1) : 0u);
+  const uint32_t qf = g & 1u, qe = tig & 1u;
+  // this warp's Q fragments: [batch][column block][k-step][lane] float4 (b0 big, b1 big, b0 small, b1 small)
+  float4* qfrag = reinterpret_cast<float4*>(dsm + a.sm_q) + (size_t)wid * RB * RC * KS * 32 + lane;
+  float* out = static_cast<float*>(a.out);
+
+  int ver[2] = {0, 0}, cslot[2] = {0, 0};
+  uint32_t cpar[2] = {0u, 0u};
+  bool qready = false;
+  for (uint64_t tile = t0; tile < t1; ++tile) {
+    const int r = __ffsll((long long)~tile) - 1;
+    if (!qready) {                       // Q's chunk changed: rebuild this warp's Q fragments
+      hm_wait(bar_full + (uint32_t)(4 + cslot[1]) * 8u, cpar[1]);
+      const float2* Qraw = reinterpret_cast<const float2*>(dsm + a.sm_in[1][cslot[1]]);
+#pragma unroll
+      for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+        for (int fb = 0; fb < RB; ++fb) {
+          uint32_t ib = ib_lane;
+#pragma unroll
+          for (int k = 0; k < NFB; ++k)
+            if ((fb >> k) & 1) ib += chunk_off(1, FB0 + NFA + k);
+#pragma unroll
+          for (int k = 0; k < NFC; ++k)
+            if ((fc >> k) & 1) ib += chunk_off(1, FB0 + NFA + NFB + k);
+#pragma unroll
+          for (int s = 0; s < KS; ++s) {
+            float v[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int x = 4 * s + 2 * h + (int)(tig >> 1);
+              const float2 q = cmul(Qraw[((uint32_t)a.row[1][x] << a.nch[1]) + ib], Cs[x]);
+              // Q'[2x+e][2j+f]: (e, f) = (0, 0) Re, (0, 1) Im, (1, 0) -Im, (1, 1) Re
+              v[h] = qe == qf ? q.x : (qe ? -q.y : q.y);
+            }
+            uint32_t b0, b1, s0, s1;
+            tf32_split(v[0], b0, s0);
+            tf32_split(v[1], b1, s1);
+            qfrag[((fc * RB + fb) * KS + s) * 32] =
+                make_float4(__uint_as_float(b0), __uint_as_float(b1), __uint_as_float(s0), __uint_as_float(s1));
+          }
+        }
+      __syncwarp();
+      if (lane == 0) hm_arrive(bar_empty + (uint32_t)(4 + cslot[1]) * 8u);   // raw Q no longer read
+      qready = true;
+    }
+    hm_wait(bar_full + (uint32_t)cslot[0] * 8u, cpar[0]);
+    const float* Rraw = reinterpret_cast<const float*>(dsm + a.sm_in[0][cslot[0]]) + qe;
+    float acc[NF][4];
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[f][k] = 0.f;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const uint32_t rf0 = rowf[4 * s + (tig >> 1)], rf1 = rowf[4 * s + 2 + (tig >> 1)];
+      uint32_t ab[RC][RA][4], as[RC][RA][4];
+#pragma unroll
+      for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+        for (int fa = 0; fa < RA; ++fa) {
+          uint32_t ia = ia_thr;
+#pragma unroll
+          for (int k = 0; k < NFA; ++k)
+            if ((fa >> k) & 1) ia += chunk_off(0, FB0 + k);
+#pragma unroll
+          for (int k = 0; k < NFC; ++k)
+            if ((fc >> k) & 1) ia += chunk_off(0, FB0 + NFA + NFB + k);
+          ia *= 2u;
+          tf32_split(Rraw[rf0 + ia], ab[fc][fa][0], as[fc][fa][0]);
+          tf32_split(Rraw[rf0 + ia + ia_r8], ab[fc][fa][1], as[fc][fa][1]);
+          tf32_split(Rraw[rf1 + ia], ab[fc][fa][2], as[fc][fa][2]);
+          tf32_split(Rraw[rf1 + ia + ia_r8], ab[fc][fa][3], as[fc][fa][3]);
+        }
+      float4 qv[RC][RB];
+#pragma unroll
+      for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+        for (int fb = 0; fb < RB; ++fb) qv[fc][fb] = qfrag[((fc * RB + fb) * KS + s) * 32];
+#pragma unroll
+      for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+        for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+          for (int fb = 0; fb < RB; ++fb)
+#pragma unroll
+            for (int fa = 0; fa < RA; ++fa) {
+              const int f = fa + RA * (fb + RB * fc);
+              const float4 q = qv[fc][fb];
+              if (pass == 0) mma_tf32(acc[f], as[fc][fa], __float_as_uint(q.x), __float_as_uint(q.y));
+              else if (pass == 1) mma_tf32(acc[f], ab[fc][fa], __float_as_uint(q.z), __float_as_uint(q.w));
+              else mma_tf32(acc[f], ab[fc][fa], __float_as_uint(q.x), __float_as_uint(q.y));
+            }
+    }
+    // chunk versions for the next tile; release the slots this warp is done with
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (fbit[u][r] != fcum[u][r]) {
+        if (u == 0) {
+          __syncwarp();
+          if (lane == 0) hm_arrive(bar_empty + (uint32_t)cslot[0] * 8u);
+        } else {
+          qready = false;
+        }
+        ++ver[u];
+        if (++cslot[u] == S) { cslot[u] = 0; cpar[u] ^= 1u; }
+      }
+    float* ob = out + 2 * (obase + othr);
+    switch (a.p0 * 4 + a.p1) {
+#define HM_ST(P0, P1) \
+      case P0 * 4 + P1: if constexpr (P0 < NR && P1 < NR) hm_store<P0, P1, NR, NF>(ob, acc, so); break;
+      HM_ST(0, 1) HM_ST(0, 2) HM_ST(0, 3) HM_ST(1, 0) HM_ST(1, 2) HM_ST(1, 3)
+      HM_ST(2, 0) HM_ST(2, 1) HM_ST(2, 3) HM_ST(3, 0) HM_ST(3, 1) HM_ST(3, 2)
+#undef HM_ST
+      default: break;
+    }
+    obase = obase + pbit[r] - pcum[r];
+  }
+}
+
+}  // namespace tnb

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -118,11 +119,30 @@ inline bool gemm_disabled() {
   return off;
 }
 
+// TNB_GEMM_DEBUG: one line per input of a group: rank, output bits held (bit 0 first), and which
+// summed values x it varies over (distinct gx rows)
+inline void debug_group(const char* tag, const GDesc& g) {
+  std::fprintf(stderr, "  %s R=%d M=%d n=%d\n", tag, g.out_rank, g.M, g.n);
+  for (int t = 0; t < g.n; ++t) {
+    char bits[65];
+    for (int b = 0; b < g.out_rank && b < 64; ++b) bits[b] = ((g.in[t].out_mask >> b) & 1) ? '1' : '.';
+    bits[g.out_rank < 64 ? g.out_rank : 64] = 0;
+    int nrow = 0;
+    uint64_t seen[1 << kMaxGroup];
+    for (int x = 0; x < (1 << g.M); ++x) {
+      bool f = false;
+      for (int r = 0; r < nrow; ++r) f = f || seen[r] == g.in[t].gx[x];
+      if (!f) seen[nrow++] = g.in[t].gx[x];
+    }
+    std::fprintf(stderr, "    in%d rank=%u rows=%d pv=%u %s\n", t, g.in[t].rank, nrow, g.in[t].pv, bits);
+  }
+}
+
 
 // which kernel the last launcher on this thread used (per-launch profile records)
 enum KernelId : int { KID_NONE = 0, KID_BUCKET = 1, KID_CHAIN = 2, KID_GROUP = 3, KID_PAIR = 4,
                       KID_GEMM = 5, KID_CHAIN_SPLIT = 6, KID_PROGRAM = 7,
-                      KID_GEMM_TC = 8, KID_GEMM_FC = 9, KID_FC_TC = 10 };
+                      KID_GEMM_TC = 8, KID_GEMM_FC = 9, KID_FC_TC = 10, KID_GEMM_HM = 11 };
 inline int& last_kernel() {
   static thread_local int k = KID_NONE;
   return k;
@@ -132,6 +152,9 @@ inline int& last_kernel() {
 // each returns false when the shape has no instantiation / does not qualify
 template <typename T> bool try_launch_gemm(const GDesc& g, cudaStream_t st);   // k_gemm_tc first (c64), else k_gemm
 bool try_launch_gemm_tc(const GDesc& g, cudaStream_t st);
+// the same GEMM groups on mma.sync tf32 (k_gemm_hm, c64, 3xTF32); false when the shape does not qualify
+bool try_launch_gemm_hm(const GDesc& g, cudaStream_t st);
+bool gemm_hm_enabled();                                                          // TNB_GEMM_HM=0 off
 bool gemm_tc_enabled();                                                          // TNB_GEMM_TC=1
 // producer group g (GEMM-shaped) computed tile by tile and consumed by group g3 (its input tin)
 template <typename T> bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);

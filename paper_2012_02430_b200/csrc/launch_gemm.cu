@@ -55,6 +55,10 @@ template <typename T>
 bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   if (g.M < gemm_min_m()) return false;
   if (std::is_same<T, float2>::value && gemm_tc_enabled() && try_launch_gemm_tc(g, st)) return true;
+  // k_gemm_hm where it measured faster on C5a's groups (M >= 3 and >= 2^22 outputs: 78 vs 95 us on
+  // the top group; smaller or M = 2 groups are bound by its per-tile pipeline, profiles/r02/hm/)
+  if (std::is_same<T, float2>::value && gemm_hm_enabled() && g.M >= 3 && g.out_rank >= 22 && try_launch_gemm_hm(g, st))
+    return true;
   // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
   const int wb0 = gemm_wb(), wb1 = 5 - wb0;
   return try_launch_gemm_impl<T>(g, st, wb0) || try_launch_gemm_impl<T>(g, st, wb1);
@@ -223,6 +227,7 @@ bool try_launch_gemm_impl(const GDesc& g, cudaStream_t st, int WB) {
       std::fprintf(stderr, " perm=");
       for (int b = 0; b < np && b < 8; ++b) std::fprintf(stderr, "%d,", ma.perm[b]);
       std::fprintf(stderr, "\n");
+      debug_group("k_gemm", g);
     }
     const uint64_t tiles = 1ull << (R - TB);
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * (WB == 3 ? 2 : 4));

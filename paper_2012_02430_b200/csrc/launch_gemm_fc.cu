@@ -284,6 +284,7 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
     if (env_flag("TNB_GEMM_DEBUG"))
       std::fprintf(stderr, "k_gemm_fc R=%d M=%d R3=%d M3=%d TB=%d nra=%d nrb=%d nch=(%u,%u) S=%d smem=%zu nc=%d nv=%d nw=%d\n",
                    R, g.M, R3, M3, TB, nra, nrb, ma.nch[0], ma.nch[1], ma.stages, smem, nc, fa.nv, fa.nw);
+    if (env_flag("TNB_GEMM_DEBUG")) { debug_group("producer", g); debug_group("consumer", g3); }
     const uint64_t groups = 1ull << (R - TB - M3);
     static const uint64_t min_groups = [] {   // TNB_FC_MIN_GROUPS: fewer consumer blocks -> two launches
       const char* e = std::getenv("TNB_FC_MIN_GROUPS");

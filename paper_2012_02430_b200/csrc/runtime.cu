@@ -1265,7 +1265,7 @@ extern "C" tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in,
     return fail(TN_E_INVAL, "tn_eliminate_group: bad argument");
   if (out_rank < 11 || out_rank > 40) return fail(TN_E_INVAL, "tn_eliminate_group: out_rank out of range");
   if (dtype != TN_C64 && dtype != TN_C128) return fail(TN_E_DTYPE, "unsupported dtype");
-  if (kernel < 0 || kernel > 4) return fail(TN_E_INVAL, "tn_eliminate_group: unknown kernel");
+  if (kernel < 0 || kernel > 5) return fail(TN_E_INVAL, "tn_eliminate_group: unknown kernel");
   GDesc g;
   std::memset(&g, 0, sizeof(g));
   g.out = out_dev;
@@ -1301,6 +1301,7 @@ extern "C" tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in,
   if (dtype == TN_C64) {
     ok = kernel == 1 ? try_launch_gemm_simt<float2>(g, st)
        : kernel == 4 ? try_launch_gemm_tc(g, st)
+       : kernel == 5 ? try_launch_gemm_hm(g, st)
        : kernel == 2 ? try_launch_pair<float2>(g, st)
        : kernel == 3 ? try_launch_group<float2>(g, st)
        : (try_launch_gemm<float2>(g, st) || try_launch_pair<float2>(g, st) || try_launch_group<float2>(g, st));

@@ -1,5 +1,5 @@
 """Time one fused merge group of a given bit-class pattern through tn_eliminate_group with each
-GEMM kernel (1 = k_gemm FP32 pipes, 4 = k_gemm_tc tensor cores); CUDA events, inputs resident.
+GEMM kernel (1 = k_gemm FP32 pipes, 4 = k_gemm_tc tcgen05, 5 = k_gemm_hm mma.sync); CUDA events, inputs resident.
 Default shape = C5a's top group (steps 173-175 of the bench plan: out 2^26, A 2^23, B 2^15, M=3).
     python scripts/gemm_shape_bench.py [--cls abcc...] [--M 3] [--kernels 1,4] [--iters 20]"""
 import argparse
@@ -17,7 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cls", default=TOP)
     ap.add_argument("--M", type=int, default=3)
-    ap.add_argument("--kernels", default="1,4")
+    ap.add_argument("--kernels", default="1,5")
     ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     import torch

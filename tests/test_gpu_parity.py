@@ -277,6 +277,56 @@ def test_gemm_tc_vs_oracle(case):
     assert err < TOL[T.TN_C64] * 0.1, err
 
 
+HM_CASES = [
+    # (out_rank, M, classes from bit 0 up (a: A only, b: B only, c: both), xa, xb, expected (FA, FB))
+    (21, 3, "bcbaacaacacababcaabca", None, None),   # the low bits of C5a's top standalone group
+    (20, 3, "abccabcaabcbabaaacaa", None, None),    # the low bits of C5a's producer group (FB = 3)
+    (17, 3, "bacbbcabbabbbcbbb", None, None),       # B holds the most exclusive bits (roles swap)
+    (19, 2, "ccaaaaaaabbbbbcbbac", 0b01, None),     # A lacks x_1: chunk rows shared; K = 4 (one k-step)
+    (18, 5, "aabbcaaaaabbbcccab", None, 0b10110),   # K = 32, B lacks x_0 and x_3
+    (20, 4, "acbcacbcaaaaabbbbccc", None, None),
+    (18, 3, "aaaaaaaaabbccccaca", None, None),      # two B-only bits: FB = 0, FA = 3
+    (22, 3, "cbcbaacaaacabcaabbacac", None, None),  # several tiles per CTA
+]
+
+
+@pytest.mark.parametrize("case", range(len(HM_CASES)))
+def test_gemm_hm_vs_oracle(case):
+    """k_gemm_hm (mma.sync m16n8k8 tf32, 3xTF32 split) on GEMM-shaped merge groups vs the oracle at
+    the complex64 tolerance (the tile covers the lanes' a/b bits, rows shared across x, K = 4 .. 32,
+    swapped operand roles, every fragment-block split)."""
+    out_rank, M, cls_s, xa, xb = HM_CASES[case]
+    rng = np.random.default_rng(7000 + case)
+    cls = list(cls_s)
+    assert len(cls) == out_rank
+    masks, xms, shapes = _gemm_group(rng, out_rank, M, cls, xa, xb)
+    arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+    dev = [torch.tensor(a, dtype=torch.complex64, device="cuda") for a in arrays]
+    out = torch.full((2 ** out_rank,), float("nan"), dtype=torch.complex64, device="cuda")
+    B.tn_eliminate_group(T.TN_C64, M, [d.data_ptr() for d in dev], masks, xms, out.data_ptr(), out_rank,
+                         5, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.complex128)
+    ref = _oracle_group(arrays, masks, xms, M, out_rank)
+    assert np.all(np.isfinite(got)), "output element not written"
+    err = np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30)
+    assert err < TOL[T.TN_C64] * 0.1, err
+
+
+def test_gemm_hm_declines_tile_dependent_constants():
+    """A constant factor holding an output bit would force the Q fragments to be rebuilt every
+    tile: k_gemm_hm declines (the library's choice then takes k_gemm)."""
+    rng = np.random.default_rng(7100)
+    out_rank, M = 19, 3
+    cls = list("abcabcaaaabbbcccaab")
+    masks, xms, shapes = _gemm_group(rng, out_rank, M, cls, None, None, 1 << 18)
+    dev = [torch.zeros(2 ** r, dtype=torch.complex64, device="cuda") for r in shapes]
+    out = torch.empty(2 ** out_rank, dtype=torch.complex64, device="cuda")
+    with pytest.raises(T.TnError):
+        B.tn_eliminate_group(T.TN_C64, M, [d.data_ptr() for d in dev], masks, xms, out.data_ptr(), out_rank,
+                             5, torch.cuda.current_stream().cuda_stream)
+
+
 # ------------------------------------------------------------------ amplitudes, small/medium
 @pytest.mark.parametrize("dtype", [T.TN_C64, T.TN_C128])
 @pytest.mark.parametrize("n,p,k,orderer", [(12, 1, 0, "min-fill"), (14, 2, 0, "min-degree"),
