@@ -76,7 +76,7 @@ class tn_prof_record_t(C.Structure):
 
 
 KERNEL_NAMES = {0: "?", 1: "k_bucket", 2: "k_chain", 3: "k_group_t", 4: "k_pair", 5: "k_gemm",
-                6: "k_chain_split", 7: "k_program", 8: "k_gemm_tc", 9: "k_gemm_fc", 10: "k_fc_tc", 11: "k_gemm_hm"}
+                6: "k_chain_split", 7: "k_program", 8: "k_gemm_tc", 9: "k_gemm_fc", 10: "k_fc_tc", 11: "k_gemm_hm", 12: "k_fc_hm"}
 
 
 _P = C.c_void_p

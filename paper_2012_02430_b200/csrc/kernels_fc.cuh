@@ -41,6 +41,8 @@ struct FArgs {
   const void* win[kMaxIn];
   uint32_t wgx[kMaxIn][1 << kMaxGroup];
   uint64_t omask;                              // (1 << R3) - 1: the o part of a T offset
+  int32_t xpf;                                 // 1: prefetch the next tile's X lines into L2 (X holds
+                                               // output bits 0..4 at its positions 0..4)
 };
 
 template <int M, int RAB, int RBB, int WB>
@@ -147,6 +149,21 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
   for (int u = 0; u < 2; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
 #pragma unroll
   for (int t = 0; t < kMaxIn - 2; ++t) curc[t] = t < a.nc ? (uint32_t)fmap(obase, a.cmask[t], a.cpv[t]) : 0u;
+  // X prefetch: a warp's RA x RB consumer loads cover 2 RA RB 128-byte lines of X (lanes = output
+  // bits 0..4 = X positions 0..4); lane l < 2 RA RB fetches line l & 1 of load l >> 1 for the next tile
+  uint32_t pfo = 0;
+  const bool pf_lane = f.xpf && f.nv > 0 && (tid & 31u) < 2u * RA * RB;
+  if (pf_lane) {
+    const uint32_t q = (tid & 31u) >> 1, i = q / RB, j = q % RB;
+    uint32_t o = (othr & ~31u) + ((tid & 1u) << 4);
+#pragma unroll
+    for (int k = 0; k < RAB; ++k)
+      if ((i >> k) & 1) o += 1u << a.outbit[TL + k];
+#pragma unroll
+    for (int k = 0; k < RBB; ++k)
+      if ((j >> k) & 1) o += 1u << a.outbit[TL + RAB + k];
+    pfo = (uint32_t)fmap(o, f.vmask[0], f.vpv[0]);
+  }
   float2* out3 = static_cast<float2*>(f.out3);
   if (tid < (1u << f.M3)) {
     float2 c3 = make_float2(1.f, 0.f);
@@ -212,6 +229,8 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
       for (int v = 0; v < kFcMaxV; ++v) vcur[v] = v < f.nv ? (uint32_t)fmap(obo, f.vmask[v], f.vpv[v]) : 0u;
     }
     const float2 c3 = C3s[y];
+    if (pf_lane && y < ymask)              // the next tile (same block, y + 1): its X lines into L2
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const float2*>(f.vin[0]) + vcur[0] + pfo + f.vgx[0][y + 1]));
 #if FC_PREFETCH
     // the consumer factors of this tile are loaded after its GEMM: pull their lines into L1 now
     // (no registers held; the GEMM covers the latency)

@@ -44,23 +44,24 @@ namespace tnb {
 
 struct HArgs {
   void* out;
-  const void* in[2];                   // R (MMA rows), Q (MMA columns)
-  uint64_t mask[2];                    // F_t(o) = ins0(pext(o, mask_t), pv_t)
-  uint32_t pv[2];
-  uint8_t row[2][1 << kMaxGroup];      // x -> chunk row
-  uint32_t rowoff[2][1 << kMaxGroup];  // element offset G_t(x) of chunk row r (distinct x-part)
-  uint32_t posoff[2][kGemmMaxTB];      // element offset (within the operand) of chunk bit k
-  uint32_t nrows[2];                   // chunk rows (distinct x parts)
-  uint32_t nch[2];                     // tile bits held by the operand (chunk row = 2^nch elements)
-  uint32_t runl[2];                    // log2 elements of one contiguous run (one bulk copy), >= 1
-  int8_t chbit[2][kGemmMaxTB];         // tile-local bit u -> chunk bit (-1: absent)
+  // streams: 0 = R (MMA rows), 1 = Q (MMA columns), 2 = X (FC mode: the consumer factor, one row)
+  const void* in[3];
+  uint64_t mask[3];                    // F_t(o) = ins0(pext(o, mask_t), pv_t)
+  uint32_t pv[3];
+  uint8_t row[3][1 << kMaxGroup];      // x -> chunk row
+  uint32_t rowoff[3][1 << kMaxGroup];  // element offset G_t(x) of chunk row r (distinct x-part)
+  uint32_t posoff[3][kGemmMaxTB];      // element offset (within the operand) of chunk bit k
+  uint32_t nrows[3];                   // chunk rows (distinct x parts)
+  uint32_t nch[3];                     // tile bits held by the operand (chunk row = 2^nch elements)
+  uint32_t runl[3];                    // log2 elements of one contiguous run (one bulk copy), >= 1
+  int8_t chbit[3][kGemmMaxTB];         // tile-local bit u -> chunk bit (-1: absent)
   uint8_t outbit[kGemmMaxTB];          // tile-local bit u -> output bit (all < 32)
   uint8_t sbit[kGemmMaxTB];            // tile-local bit u -> staging bit (rank among the tile's output bits)
-  uint32_t sm_in[2][4];                // dynamic smem byte offset of ring slot (operand, slot)
-  uint32_t sm_run[2];                  // dynamic smem byte offset of the run table (element offset of run q)
+  uint32_t sm_in[3][4];                // dynamic smem byte offset of ring slot (stream, slot)
+  uint32_t sm_run[3];                  // dynamic smem byte offset of the run table (element offset of run q)
   uint32_t sm_q;                       // dynamic smem byte offset of the Q fragments
   int32_t p0, p1;                      // register slots holding output bits 0 and 1
-  int32_t stages;                      // ring slots (2..4); lookahead = stages - 1 tiles
+  int32_t stages[3];                   // ring slots per stream (2..4)
   const void* cin[kMaxIn];             // constant inputs: no output bit (C[x] = prod_t cin[t][cgx[t][x]])
   uint32_t cgx[kMaxIn][1 << kMaxGroup];
   int32_t nc;
@@ -126,8 +127,56 @@ __device__ __forceinline__ void hm_store(float* ob, const float (&acc)[NF][4], c
   }
 }
 
-template <int M, int NFA, int NFB, int NFC, int WB>
-__global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
+// k_fc_hm mode (FC = true): the group's output T is never written -- it is the full input of the
+// next group (OP_GROUP_FEED, kernels_fc.cuh), out3[o] = sum_y C3_y X(o, y) T[o, y].  Tile bits are
+// consumer output bits o; the traversal runs over the consumer's summed bits y first (HArgs.perm),
+// so 2^M3 consecutive tiles of a CTA share o and every thread accumulates its outputs in registers.
+// X (the consumer's other input holding output bits) arrives by 256-bit loads issued at the start of
+// the tile (the tile's MMAs cover their latency).
+struct FHArgs {
+  void* out3;                                  // consumer output (2^R3 elements)
+  int32_t M3;                                  // consumer summed indices (y bits of T)
+  const void* xin;                             // X, or nullptr (the consumer has only weights)
+  uint64_t xmask;                              // F_X(o) = ins0(pext(o, xmask), xpv)
+  uint32_t xpv;
+  uint32_t xgx[1 << kMaxGroup];                // G_X(y), y in traversal order
+  int32_t nw;                                  // consumer inputs holding no output bit (weights)
+  const void* win[kMaxIn];
+  uint32_t wgx[kMaxIn][1 << kMaxGroup];        // y in traversal order
+  uint64_t omask;                              // (1 << R3) - 1
+};
+
+__device__ __forceinline__ void ld_v8_stream(float (&v)[8], const float* p) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
+// FC: the thread's 2^NR consumer factors X (register-slot order, as hm_store's values) from the X
+// chunk in shared memory: the quads whose output bits 0 / 1 are slots P0 / P1 (X chunk positions 0, 1)
+// as two 16-byte loads each
+template <int P0, int P1, int NR>
+__device__ __forceinline__ void hm_load_x(float (&xr)[1 << NR][2], const float2* xb, const uint32_t (&xs)[NR]) {
+#pragma unroll
+  for (int q = 0; q < (1 << NR); ++q) {
+    if (q & ((1 << P0) | (1 << P1))) continue;
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k)
+      if ((q >> k) & 1) o += xs[k];
+    const float4 v0 = *reinterpret_cast<const float4*>(xb + o), v1 = *reinterpret_cast<const float4*>(xb + o + 2);
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int reg = q | ((e & 1) << P0) | ((e >> 1) << P1);
+      xr[reg][0] = v[2 * e];
+      xr[reg][1] = v[2 * e + 1];
+    }
+  }
+}
+
+template <int M, int NFA, int NFB, int NFC, int WB, bool FC = false>
+__global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const HArgs a, const FHArgs f) {
   constexpr int NW = 1 << WB;              // consumer warps; warp NW is the producer
   constexpr int kThreads = 32 * NW + 32;
   constexpr int K = 1 << M;
@@ -144,14 +193,16 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
   const uint32_t g = lane >> 2, tig = lane & 3u;
   const uint64_t n_tiles = 1ull << (a.out_rank - TB);
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ uint32_t fbit[2][NB];
-  __shared__ uint32_t fcum[2][NB + 1];
+  constexpr int NOPS = FC ? 3 : 2;         // streams
+  __shared__ uint32_t fbit[NOPS][NB];
+  __shared__ uint32_t fcum[NOPS][NB + 1];
   __shared__ uint64_t pbit[NB], pcum[NB + 1];
   __shared__ float2 Cs[K];
   __shared__ uint32_t rowf[K];             // R chunk row of x, in floats (row << nch, x 2)
-  __shared__ __align__(8) uint64_t bars[2][2][4];   // [full / empty][operand][slot]
+  __shared__ __align__(8) uint64_t bars[2][3][4];   // [full / empty][stream][slot]
+  __shared__ float2 C3s[FC ? (1 << kMaxGroup) : 1];   // product of the consumer's weights per y
   const int nperm = a.out_rank - TB;
-  for (int i = tid; i < 2 * NB; i += kThreads) {
+  for (int i = tid; i < NOPS * NB; i += kThreads) {
     const int t = i / NB, b = i % NB;
     fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], a.mask[t], a.pv[t]) : 0u;
   }
@@ -162,9 +213,9 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
     for (int t = 0; t < a.nc; ++t) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + a.cgx[t][tid]));
     Cs[tid] = c;
   }
-  // run tables: run q of operand u's chunk (2^runl contiguous elements) -> element offset from the base
+  // run tables: run q of stream u's chunk (2^runl contiguous elements) -> element offset from the base
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < NOPS; ++u) {
     const uint32_t lp = a.nch[u] - a.runl[u];
     const uint32_t nr = a.nrows[u] << lp;
     uint32_t* tab = reinterpret_cast<uint32_t*>(dsm + a.sm_run[u]);
@@ -176,9 +227,14 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
       tab[q] = off;
     }
   }
+  if (FC && tid < (1u << f.M3)) {
+    float2 c3 = make_float2(1.f, 0.f);
+    for (int w = 0; w < f.nw; ++w) c3 = cmul(c3, __ldg(static_cast<const float2*>(f.win[w]) + f.wgx[w][tid]));
+    C3s[tid] = c3;
+  }
   if (tid == 0) {
-    for (int u = 0; u < 2; ++u)
-      for (int s = 0; s < a.stages; ++s) {
+    for (int u = 0; u < NOPS; ++u)
+      for (int s = 0; s < a.stages[u]; ++s) {
         mbar_init(&bars[0][u][s], 1);
         mbar_init(&bars[1][u][s], NW);
       }
@@ -186,37 +242,44 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
   }
   __syncthreads();
   const int nbu = min(NB - 1, max(0, nperm));
-  if (tid < 2u) {
+  if (tid < (uint32_t)NOPS) {
     uint32_t c = 0;
     fcum[tid][0] = 0;
     for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
   }
-  if (tid == 2u) {
+  if (tid == 3u) {
     uint64_t c = 0;
     pcum[0] = 0;
     for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
   }
   __syncthreads();
-  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
-  const uint64_t t0 = (uint64_t)blockIdx.x * per;
-  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t t0, t1;
+  if (FC) {   // whole groups of 2^M3 tiles per CTA (a consumer output block is finished inside one CTA)
+    const uint64_t n_groups = n_tiles >> f.M3;
+    const uint64_t gper = (n_groups + gridDim.x - 1) / gridDim.x;
+    t0 = ((uint64_t)blockIdx.x * gper) << f.M3;
+    const uint64_t t1e = (((uint64_t)blockIdx.x + 1) * gper) << f.M3;
+    t1 = t1e < n_tiles ? t1e : n_tiles;
+  } else {
+    const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+    t0 = (uint64_t)blockIdx.x * per;
+    t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  }
   uint64_t obase = 0;
   for (int b = 0; b < nperm && (t0 >> b); ++b)
     if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
   const uint32_t bar_full = smem_u32(&bars[0][0][0]);   // + (u * 4 + slot) * 8
   const uint32_t bar_empty = smem_u32(&bars[1][0][0]);
-  const int S = a.stages;
 
   if (wid == (uint32_t)NW) {
     // ---------------------------------------------------------------- producer warp: lane 0 arms
     // the slot's full barrier, the 32 lanes issue the chunk's bulk copies
     if (t0 < t1) {
-      uint32_t cur[2];
-      int ver[2] = {0, 0};
-      for (int u = 0; u < 2; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
-      const uint32_t* tab[2] = {reinterpret_cast<const uint32_t*>(dsm + a.sm_run[0]),
-                                reinterpret_cast<const uint32_t*>(dsm + a.sm_run[1])};
-      auto issue = [&](int u) {
+      uint32_t cur[3];
+      int ver[3] = {0, 0, 0};
+      for (int u = 0; u < NOPS; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
+      auto issue = [&](int u, uint32_t base) {
+        const int S = a.stages[u];
         const int v = ver[u], slot = v % S;
         if (v >= S) hm_wait(bar_empty + (uint32_t)(u * 4 + slot) * 8u, (uint32_t)((v / S) - 1) & 1u);
         const uint32_t nr = a.nrows[u] << (a.nch[u] - a.runl[u]);
@@ -224,21 +287,28 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
         const uint32_t bar = bar_full + (uint32_t)(u * 4 + slot) * 8u;
         if (lane == 0) hm_expect_tx(bar, nr * bytes);
         __syncwarp();
-        const float2* src = static_cast<const float2*>(a.in[u]) + cur[u];
+        const float2* src = static_cast<const float2*>(a.in[u]) + base;
         const uint32_t dst = smem_u32(dsm + a.sm_in[u][slot]);
-        for (uint32_t q = lane; q < nr; q += 32) hm_bulk(dst + q * bytes, src + tab[u][q], bytes, bar);
+        const uint32_t* tab = reinterpret_cast<const uint32_t*>(dsm + a.sm_run[u]);
+        for (uint32_t q = lane; q < nr; q += 32) hm_bulk(dst + q * bytes, src + tab[q], bytes, bar);
       };
-      issue(0);
-      issue(1);
+      issue(0, cur[0]);
+      issue(1, cur[1]);
+      if (FC) issue(2, cur[2] + f.xgx[0]);
       for (uint64_t tile = t0; tile + 1 < t1; ++tile) {
         const int r = __ffsll((long long)~tile) - 1;
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (fbit[u][r] != fcum[u][r]) {
-            cur[u] = cur[u] + fbit[u][r] - fcum[u][r];
+        for (int u = 0; u < NOPS; ++u) {
+          const bool changed = fbit[u][r] != fcum[u][r];
+          if (changed) cur[u] = cur[u] + fbit[u][r] - fcum[u][r];
+          if (u == 2) {                  // X: a new chunk every tile (the tile's y)
+            ++ver[2];
+            issue(2, cur[2] + f.xgx[(uint32_t)(tile + 1) & ((1u << f.M3) - 1u)]);
+          } else if (changed) {
             ++ver[u];
-            issue(u);
+            issue(u, cur[u]);
           }
+        }
       }
     }
     return;
@@ -270,12 +340,39 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
   // this warp's Q fragments: [batch][column block][k-step][lane] float4 (b0 big, b1 big, b0 small, b1 small)
   float4* qfrag = reinterpret_cast<float4*>(dsm + a.sm_q) + (size_t)wid * RB * RC * KS * 32 + lane;
   float* out = static_cast<float*>(a.out);
+  // FC: X chunk index of this thread's outputs: lanes / warps, register slots
+  uint32_t xthr = 0, xs[NR];
+  float oacc[FC ? NF : 1][4];
+  const uint32_t ymask = FC ? (1u << f.M3) - 1u : 0u;
+  if (FC) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if ((tig >> k) & 1u) xthr += chunk_off(2, k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if ((g >> k) & 1u) xthr += chunk_off(2, 2 + k);
+#pragma unroll
+    for (int k = 0; k < WB; ++k)
+      if ((wid >> k) & 1u) xthr += chunk_off(2, 6 + k);
+    xs[0] = chunk_off(2, 5);
+#pragma unroll
+    for (int k = 0; k < NFR; ++k) xs[1 + k] = chunk_off(2, FB0 + k);
+  }
 
-  int ver[2] = {0, 0}, cslot[2] = {0, 0};
-  uint32_t cpar[2] = {0u, 0u};
+  int cslot[3] = {0, 0, 0};
+  uint32_t cpar[3] = {0u, 0u, 0u};
   bool qready = false;
   for (uint64_t tile = t0; tile < t1; ++tile) {
     const int r = __ffsll((long long)~tile) - 1;
+    const uint32_t y = (uint32_t)tile & ymask;
+    if constexpr (FC) {
+      if (y == 0u) {                     // a new consumer output block
+#pragma unroll
+        for (int i = 0; i < NF; ++i)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) oacc[i][k] = 0.f;
+      }
+    }
     if (!qready) {                       // Q's chunk changed: rebuild this warp's Q fragments
       hm_wait(bar_full + (uint32_t)(4 + cslot[1]) * 8u, cpar[1]);
       const float2* Qraw = reinterpret_cast<const float2*>(dsm + a.sm_in[1][cslot[1]]);
@@ -369,17 +466,55 @@ __global__ void __launch_bounds__((32 << WB) + 32, 3) k_gemm_hm(const HArgs a) {
         } else {
           qready = false;
         }
-        ++ver[u];
-        if (++cslot[u] == S) { cslot[u] = 0; cpar[u] ^= 1u; }
+        if (++cslot[u] == a.stages[u]) { cslot[u] = 0; cpar[u] ^= 1u; }
       }
-    float* ob = out + 2 * (obase + othr);
-    switch (a.p0 * 4 + a.p1) {
+    if constexpr (FC) {
+      // consumer: oacc += C3_y X(o, y) T[o, y], X from this tile's X chunk (4 complex per quad)
+      hm_wait(bar_full + (uint32_t)(8 + cslot[2]) * 8u, cpar[2]);
+      float xr[2 * NF][2];
+      {
+        const float2* xb = reinterpret_cast<const float2*>(dsm + a.sm_in[2][cslot[2]]) + xthr;
+        switch (a.p0 * 4 + a.p1) {
+#define HM_LD(P0, P1) \
+          case P0 * 4 + P1: if constexpr (P0 < NR && P1 < NR) hm_load_x<P0, P1, NR>(xr, xb, xs); break;
+          HM_LD(0, 1) HM_LD(0, 2) HM_LD(0, 3) HM_LD(1, 0) HM_LD(1, 2) HM_LD(1, 3)
+          HM_LD(2, 0) HM_LD(2, 1) HM_LD(2, 3) HM_LD(3, 0) HM_LD(3, 1) HM_LD(3, 2)
+#undef HM_LD
+          default: break;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) hm_arrive(bar_empty + (uint32_t)(8 + cslot[2]) * 8u);
+      if (++cslot[2] == a.stages[2]) { cslot[2] = 0; cpar[2] ^= 1u; }
+      const float2 c3 = C3s[y];
+#pragma unroll
+      for (int reg = 0; reg < 2 * NF; ++reg) {
+        const float xx0 = c3.x * xr[reg][0] - c3.y * xr[reg][1], xx1 = c3.x * xr[reg][1] + c3.y * xr[reg][0];
+        const float t0r = acc[reg >> 1][2 * (reg & 1)], t0i = acc[reg >> 1][2 * (reg & 1) + 1];
+        oacc[reg >> 1][2 * (reg & 1)] += xx0 * t0r - xx1 * t0i;
+        oacc[reg >> 1][2 * (reg & 1) + 1] += xx0 * t0i + xx1 * t0r;
+      }
+      if (y == ymask) {                  // last y of the block: the consumer output is final
+        float* ob = static_cast<float*>(f.out3) + 2 * ((obase & f.omask) + othr);
+        switch (a.p0 * 4 + a.p1) {
 #define HM_ST(P0, P1) \
-      case P0 * 4 + P1: if constexpr (P0 < NR && P1 < NR) hm_store<P0, P1, NR, NF>(ob, acc, so); break;
-      HM_ST(0, 1) HM_ST(0, 2) HM_ST(0, 3) HM_ST(1, 0) HM_ST(1, 2) HM_ST(1, 3)
-      HM_ST(2, 0) HM_ST(2, 1) HM_ST(2, 3) HM_ST(3, 0) HM_ST(3, 1) HM_ST(3, 2)
+          case P0 * 4 + P1: if constexpr (P0 < NR && P1 < NR) hm_store<P0, P1, NR, NF>(ob, oacc, so); break;
+          HM_ST(0, 1) HM_ST(0, 2) HM_ST(0, 3) HM_ST(1, 0) HM_ST(1, 2) HM_ST(1, 3)
+          HM_ST(2, 0) HM_ST(2, 1) HM_ST(2, 3) HM_ST(3, 0) HM_ST(3, 1) HM_ST(3, 2)
 #undef HM_ST
-      default: break;
+          default: break;
+        }
+      }
+    } else {
+      float* ob = out + 2 * (obase + othr);
+      switch (a.p0 * 4 + a.p1) {
+#define HM_ST(P0, P1) \
+        case P0 * 4 + P1: if constexpr (P0 < NR && P1 < NR) hm_store<P0, P1, NR, NF>(ob, acc, so); break;
+        HM_ST(0, 1) HM_ST(0, 2) HM_ST(0, 3) HM_ST(1, 0) HM_ST(1, 2) HM_ST(1, 3)
+        HM_ST(2, 0) HM_ST(2, 1) HM_ST(2, 3) HM_ST(3, 0) HM_ST(3, 1) HM_ST(3, 2)
+#undef HM_ST
+        default: break;
+      }
     }
     obase = obase + pbit[r] - pcum[r];
   }

@@ -142,7 +142,7 @@ inline void debug_group(const char* tag, const GDesc& g) {
 // which kernel the last launcher on this thread used (per-launch profile records)
 enum KernelId : int { KID_NONE = 0, KID_BUCKET = 1, KID_CHAIN = 2, KID_GROUP = 3, KID_PAIR = 4,
                       KID_GEMM = 5, KID_CHAIN_SPLIT = 6, KID_PROGRAM = 7,
-                      KID_GEMM_TC = 8, KID_GEMM_FC = 9, KID_FC_TC = 10, KID_GEMM_HM = 11 };
+                      KID_GEMM_TC = 8, KID_GEMM_FC = 9, KID_FC_TC = 10, KID_GEMM_HM = 11, KID_FC_HM = 12 };
 inline int& last_kernel() {
   static thread_local int k = KID_NONE;
   return k;
@@ -155,6 +155,9 @@ bool try_launch_gemm_tc(const GDesc& g, cudaStream_t st);
 // the same GEMM groups on mma.sync tf32 (k_gemm_hm, c64, 3xTF32); false when the shape does not qualify
 bool try_launch_gemm_hm(const GDesc& g, cudaStream_t st);
 bool gemm_hm_enabled();                                                          // TNB_GEMM_HM=0 off
+// producer group g on mma.sync tf32 consumed by g3 in registers (k_fc_hm); false when it does not qualify
+bool try_launch_fc_hm(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
+bool fc_hm_enabled();                                                            // TNB_FC_HM=0 off
 bool gemm_tc_enabled();                                                          // TNB_GEMM_TC=1
 // producer group g (GEMM-shaped) computed tile by tile and consumed by group g3 (its input tin)
 template <typename T> bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);

@@ -116,6 +116,12 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
         ++fa.nw;
       }
     }
+    {   // X prefetch (TNB_FC_XPF=0 off): X holds output bits 0..4 at its positions 0..4
+      const char* e = std::getenv("TNB_FC_XPF");
+      bool ok = fa.nv == 1 && !(e && e[0] == '0');
+      for (int k = 0; k < 5 && ok; ++k) ok = host_fmap(1ull << k, fa.vmask[0], fa.vpv[0]) == (1ull << k);
+      fa.xpf = ok ? 1 : 0;
+    }
     // producer: A, B = the two inputs with the most output bits
     int ia = -1, ib = -1;
     for (int t = 0; t < g.n; ++t) {

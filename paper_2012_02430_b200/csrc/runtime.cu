@@ -777,6 +777,7 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
             ProfScope ps(pl, st, (bytes - tb + bytes3 - tb) * sizeof(T), op.begin, nx.end, 3, g3.out_rank);
             ps.pr.flops = 8.0 * (std::ldexp(1.0, g.out_rank + g.M) + std::ldexp(1.0, g3.out_rank + g3.M));
             const bool fused = (std::is_same<T, float2>::value && fc_tc_enabled() && try_launch_fc_tc(g, g3, tin, st)) ||
+                               (std::is_same<T, float2>::value && fc_hm_enabled() && try_launch_fc_hm(g, g3, tin, st)) ||
                                try_launch_gemm_fc<T>(g, g3, tin, st);
             ps.cancel = !fused;
             if (fused) {

@@ -370,19 +370,21 @@ def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
     assert rel(plan.contract(ga, be, dtype=dtype), ref) < TOL[dtype]
 
 
-FUSED_PAIR = {"k_gemm_fc", "k_fc_tc"}   # the two kernels of an OP_GROUP_FEED pair (SIMT / tcgen05)
+FUSED_PAIR = {"k_gemm_fc", "k_fc_tc", "k_fc_hm"}   # the kernels of an OP_GROUP_FEED pair (SIMT / tcgen05 / mma.sync)
+FC_ENV = {"tc": {"TNB_FC_TC": "1"}, "simt": {"TNB_FC_TC": "0", "TNB_FC_HM": "0"}, "hm": {"TNB_FC_TC": "0", "TNB_FC_HM": "1"}}
 
 
-@pytest.mark.parametrize("kernel", ["tc", "simt"])
+@pytest.mark.parametrize("kernel", ["tc", "simt", "hm"])
 @pytest.mark.parametrize("n,p,k,fused", [(36, 3, 3, True), (70, 2, 3, True), (44, 3, 3, False),
                                           (50, 2, 2, False)])
 def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused, kernel, monkeypatch):
     """OP_GROUP_FEED: a GEMM-shaped group whose output is a full input of the next group runs as ONE
-    launch (the intermediate is never written) -- k_fc_tc (tcgen05) when its shape qualifies, else
-    k_gemm_fc (FP32 SIMT; TNB_FC_TC=0 / 1 selects); the contraction still matches the oracle
+    launch (the intermediate is never written) -- k_fc_tc (tcgen05, TNB_FC_TC=1), k_fc_hm (mma.sync,
+    the default) or k_gemm_fc (FP32 SIMT) when the shape qualifies; the contraction still matches the oracle
     (c64 tolerance), and the fused launch is the one that ran (profile records).  Pairs whose
     consumer output has fewer bits than a k_gemm_fc tile (fused=False) run as the two groups."""
-    monkeypatch.setenv("TNB_FC_TC", "0" if kernel == "simt" else "1")
+    for key, val in FC_ENV[kernel].items():
+        monkeypatch.setenv(key, val)
     g = random_regular_graph(n, 3, 7 * n + p)
     ga, be = qaoa_angles(p, n + 1)
     plan = T.build_plan(g, p, "amplitude", "rgreedy-fill", n_sliced=k, small_log2=0, rg_q=4, rg_tau=0.4)
@@ -392,21 +394,26 @@ def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused, kernel, monkeypat
     plan.profile(False)
     ran = {r["kernel"] for r in recs}
     assert bool(ran & FUSED_PAIR) == fused, sorted(ran)
-    if kernel == "simt":
+    if kernel != "tc":
         assert "k_fc_tc" not in ran
+    if kernel == "simt":
+        assert "k_fc_hm" not in ran
     pre, sl, res, _ = plan.schedule()
     ref = contract.contract_sliced(network.qaoa_amplitude_network(n, g.edges, ga, be), pre, sl, res)
     assert rel(got, ref) < TOL[T.TN_C64]
 
 
-def test_fc_tc_runs_on_c5a_and_matches_simt_per_slice(monkeypatch):
-    """C5a's producer -> consumer pair (R = 26 -> 21, the bench's largest launch) runs on k_fc_tc;
-    every per-slice partial agrees with the FP32 SIMT k_gemm_fc within the c64 tolerance."""
+@pytest.mark.parametrize("fast", ["tc", "hm"])
+def test_fc_fast_kernels_run_on_c5a_and_match_simt_per_slice(fast, monkeypatch):
+    """C5a's producer -> consumer pair (R = 26 -> 21, the bench's largest launch) runs on k_fc_tc
+    (tcgen05) / k_fc_hm (mma.sync, the default); every per-slice partial agrees with the FP32 SIMT
+    k_gemm_fc within the c64 tolerance."""
     plan, g, ga, be, meta = _bench_plan()
     n = plan.n_slices
     parts = {}
-    for kern in ("tc", "simt"):
-        monkeypatch.setenv("TNB_FC_TC", "0" if kern == "simt" else "1")
+    for kern in (fast, "simt"):
+        for key, val in FC_ENV[kern].items():
+            monkeypatch.setenv(key, val)
         part = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
         plan.profile(True)
         plan.contract_sliced(ga, be, 0, n, part, dtype=T.TN_C64)
@@ -414,12 +421,12 @@ def test_fc_tc_runs_on_c5a_and_matches_simt_per_slice(monkeypatch):
         ran = {r["kernel"] for r in plan.profile_records()}
         plan.profile(False)
         plan.profile_read()
-        assert ("k_fc_tc" if kern == "tc" else "k_gemm_fc") in ran, sorted(ran)
+        assert {"tc": "k_fc_tc", "hm": "k_fc_hm", "simt": "k_gemm_fc"}[kern] in ran, sorted(ran)
         h = part.cpu().tolist()
         parts[kern] = [complex(h[2 * j], h[2 * j + 1]) for j in range(n)]
     scale = max(abs(v) for v in parts["simt"])
     for j in range(n):
-        assert abs(parts["tc"][j] - parts["simt"][j]) / scale < 2e-5, (j, parts["tc"][j], parts["simt"][j])
+        assert abs(parts[fast][j] - parts["simt"][j]) / scale < 2e-5, (j, parts[fast][j], parts["simt"][j])
 
 
 
