@@ -93,6 +93,22 @@ def fp32_peak_tflops() -> float:
     return 148 * 128 * 2 * mhz * 1e6 / 1e12
 
 
+# mma.sync m16n8k8 tf32 throughput measured on this pool's B200 (scripts/probe/mma_rate.cu,
+# profiles/r02/hm/mma_rate.txt: 138.4 TMAC/s = 276.8 TFLOP/s dense tf32 on the warp-level path)
+MMA_SYNC_TF32_TFLOPS = 276.8
+TENSOR_FAMILIES = {"k_gemm_hm", "k_fc_hm"}
+
+
+def alu_peak_tflops(kernel: str):
+    """(peak, source) of a kernel family's arithmetic: FP32 FFMA for the SIMT kernels; for the
+    mma.sync 3xTF32 kernels the measured tf32 rate / 3 (three products per complex-as-real MAC set),
+    i.e. the FP32-equivalent rate of the flops bench counts (8 per complex multiply-add)."""
+    if kernel in TENSOR_FAMILIES:
+        return MMA_SYNC_TF32_TFLOPS / 3.0, ("measured mma.sync tf32 276.8 TFLOP/s / 3 (3xTF32), "
+                                           "profiles/r02/hm/mma_rate.txt")
+    return fp32_peak_tflops(), "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md section 5)"
+
+
 def load_traffic(kernel: str) -> dict:
     """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
     (profiles/traffic.json, written by scripts/ncu_traffic.py)."""
@@ -443,16 +459,26 @@ def main():
         f["launches"] += 1
     kb_ms = sum(f["ms"] for f in fam.values())
     dom = max(fam, key=lambda k: fam[k]["ms"]) if fam else None
-    fp32_peak = fp32_peak_tflops()
     roof = {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None, "traffic": None}
     if dom is not None:
         d = fam[dom]
+        # arithmetic peak of the family: FP32 FFMA for the SIMT kernels, the measured mma.sync tf32
+        # rate / 3 (3xTF32 products) for the warp-level tensor-core kernels
+        fp32_peak, alu_src = alu_peak_tflops(dom)
         achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
         t_hbm = d["bytes"] / (peak * 1e9)
         t_alu = d["flops"] / (fp32_peak * 1e12)
         tr = load_traffic(dom)
-        roof = {"bound": "hbm" if t_hbm >= t_alu else "alu", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": tr.get("dram_bytes_per_launch"),
+        bound = "hbm" if t_hbm >= t_alu else "alu"
+        # an ALU-bound family is reported against its arithmetic peak (TFLOP/s); its HBM rate stays in "hbm"
+        tflops = d["flops"] / (d["ms"] / 1e3) / 1e12
+        roof = {"bound": bound,
+                "achieved": achieved if bound == "hbm" else tflops,
+                "peak": peak if bound == "hbm" else fp32_peak,
+                "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                "frac": achieved / peak if bound == "hbm" else tflops / fp32_peak,
+                "hbm": {"achieved_GBps": achieved, "peak_GBps": peak, "frac": achieved / peak},
+                "traffic": tr.get("dram_bytes_per_launch"),
                 "kernel": dom, "launches": d["launches"],
                 "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
                 "avg_launch_ms": d["ms"] / d["launches"],
@@ -461,9 +487,8 @@ def main():
                              f"events around every launch ({ms_iso:.2f} ms/step; the timed region runs "
                              f"{lanes} lanes)"),
                 "flops_per_launch": d["flops"] / d["launches"],
-                "alu": {"achieved_tflops": d["flops"] / (d["ms"] / 1e3) / 1e12, "peak_tflops": fp32_peak,
-                        "frac": (d["flops"] / (d["ms"] / 1e3) / 1e12) / fp32_peak,
-                        "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md section 5)"},
+                "alu": {"achieved_tflops": tflops, "peak_tflops": fp32_peak, "frac": tflops / fp32_peak,
+                        "peak_source": alu_src},
                 "peak_source": peak_src,
                 "traffic_source": tr.get("source"),
                 "traffic_algorithmic_bytes_per_launch": tr.get("algorithmic_bytes_per_launch"),

@@ -1059,9 +1059,11 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
         ++ver[u];
         cslot[u] = cslot[u] + 1 == S ? 0 : cslot[u] + 1;
       }
+    if (HASC && a.c_tile_dep) {            // constants holding output bits (else their offsets stay 0)
 #pragma unroll
-    for (int t = 0; t < kMaxIn - 2; ++t)
-      if (HASC && t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
+      for (int t = 0; t < kMaxIn - 2; ++t)
+        if (t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
+    }
     obase = obase + pbit[r] - pcum[r];
   }
   cp_async_wait<0>();
