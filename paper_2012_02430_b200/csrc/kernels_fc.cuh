@@ -43,8 +43,6 @@ struct FArgs {
   uint64_t omask;                              // (1 << R3) - 1: the o part of a T offset
   int32_t xpf;                                 // 1: prefetch the next tile's X lines into L2 (X holds
                                                // output bits 0..4 at its positions 0..4)
-  int32_t bulk;                                // 1: A / B chunks by cp.async.bulk runs of 2^runl
-  uint32_t runl[2];                            // elements (warp 0 issues, mbarrier per ring slot)
 };
 
 template <int M, int RAB, int RBB, int WB>
@@ -76,26 +74,17 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
     fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], mask_of(t), pv_of(t)) : 0u;
   }
   for (int b = tid; b < NB; b += kThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
-  // piece tables (cp.async: 2^lv elements per piece) or run tables (bulk: 2^runl elements per run):
-  // piece c of input u's chunk -> element offset from the tile's base offset
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const uint32_t pl = f.bulk ? f.runl[u] : a.lv[u];
-    const uint32_t lp = a.nch[u] - pl;
+    const uint32_t lp = a.nch[u] - a.lv[u];
     const uint32_t np = a.nrows[u] << lp;
     for (uint32_t c = tid; c < np; c += kThreads) {
-      const uint32_t ia = (c & ((1u << lp) - 1u)) << pl;
+      const uint32_t ia = (c & ((1u << lp) - 1u)) << a.lv[u];
       uint32_t off = a.rowoff[u][c >> lp];
-      for (uint32_t k = pl; k < a.nch[u]; ++k)
+      for (uint32_t k = a.lv[u]; k < a.nch[u]; ++k)
         if ((ia >> k) & 1u) off += a.posoff[u][k];
       smu[a.sm_dep[u] + c] = off;
     }
-  }
-  __shared__ __align__(8) uint64_t fbar[2][4];   // bulk mode: full barrier per (input, ring slot)
-  if (f.bulk && tid == 0) {
-    for (int u = 0; u < 2; ++u)
-      for (int k = 0; k < a.stages; ++k) mbar_init(&fbar[u][k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int nbu = min(NB - 1, max(0, (int)a.out_rank - TB));
@@ -186,23 +175,8 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
   auto prefetch = [&](int u, uint32_t base, int slot) {
     const float2* src = static_cast<const float2*>(a.in[u]) + base;
     float2* dst = sm + a.sm_in[u][slot];
-    const uint32_t* tab = smu + a.sm_dep[u];
-    if (f.bulk) {                          // warp 0: lane 0 arms the slot's barrier, 32 lanes issue the runs
-      if (tid < 32u) {
-        const uint32_t nr = a.nrows[u] << (a.nch[u] - f.runl[u]);
-        const uint32_t bytes = 8u << f.runl[u];
-        const uint32_t bar = smem_u32(&fbar[u][slot]);
-        if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nr * bytes) : "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the slot's generic reads before the async writes
-        __syncwarp();
-        const uint32_t d0 = smem_u32(dst);
-        for (uint32_t q = tid; q < nr; q += 32)
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d0 + q * bytes),
-                       "l"(src + tab[q]), "r"(bytes), "r"(bar) : "memory");
-      }
-      return;
-    }
     const uint32_t np = a.nrows[u] << (a.nch[u] - a.lv[u]);
+    const uint32_t* tab = smu + a.sm_dep[u];
     if (a.lv[u]) {
       for (uint32_t c = tid; c < np; c += kThreads) cp_async16(dst + (c << 1), src + tab[c]);
     } else {
@@ -279,13 +253,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
         if (t < a.nc) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + curc[t] + a.cgx[t][tid]));
       Cs[tid] = c;
     }
-    if (f.bulk) {                          // this tile's chunk versions landed (parity = version / S)
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const uint32_t bar = smem_u32(&fbar[u][cslot[u]]), par = (uint32_t)(ver[u] / S) & 1u;
-        asm volatile("{\n .reg .pred P;\n FCW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra FCW_%=;\n}" ::"r"(bar), "r"(par) : "memory");
-      }
-    } else if (D <= 1) cp_async_wait<0>(); else if (D == 2) cp_async_wait<1>(); else cp_async_wait<2>();
+    if (D <= 1) cp_async_wait<0>(); else if (D == 2) cp_async_wait<1>(); else cp_async_wait<2>();
     __syncthreads();
     advance_lookahead();
     if (refix) {
@@ -375,11 +343,9 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
         ++ver[u];
         cslot[u] = cslot[u] + 1 == S ? 0 : cslot[u] + 1;
       }
-    if (a.c_tile_dep) {                    // constants holding output bits (else their offsets stay 0)
 #pragma unroll
-      for (int t = 0; t < kMaxIn - 2; ++t)
-        if (t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
-    }
+    for (int t = 0; t < kMaxIn - 2; ++t)
+      if (t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
     obase = obase + pbit[r] - pcum[r];
   }
   cp_async_wait<0>();

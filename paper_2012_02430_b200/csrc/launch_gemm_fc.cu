@@ -224,18 +224,7 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
       ma.pv[s] = in.pv;
       sz[s] = ma.nrows[s] << k;
     }
-    {   // bulk-copy chunks (TNB_FC_BULK=0 off): both chunks made of runs of >= 2 contiguous elements
-      const char* e = std::getenv("TNB_FC_BULK");
-      fa.bulk = (e && e[0] == '0') ? 0 : 1;
-      for (int s = 0; s < 2; ++s) {
-        uint32_t L = 0;
-        while (L < ma.nch[s] && ma.posoff[s][L] == (1u << L)) ++L;
-        fa.runl[s] = L;
-        if (L < 1) fa.bulk = 0;
-      }
-    }
-    const uint32_t pl0 = fa.bulk ? fa.runl[0] : ma.lv[0], pl1 = fa.bulk ? fa.runl[1] : ma.lv[1];
-    const uint32_t dep_u32 = (ma.nrows[0] << (ma.nch[0] - pl0)) + (ma.nrows[1] << (ma.nch[1] - pl1));
+    const uint32_t dep_u32 = (ma.nrows[0] << (ma.nch[0] - ma.lv[0])) + (ma.nrows[1] << (ma.nch[1] - ma.lv[1]));
     const size_t bf_bytes = ((size_t)16 << g.M) << ma.nch[1];
     int S = gemm_stages();
     const size_t budget = WB == 3 ? kFcSmemBudget : kFcSmemBudget / 2;   // 2 or 4 CTAs per SM
@@ -248,7 +237,7 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
     uint32_t u32 = 2 * S * (sz[0] + sz[1]);
     for (int s = 0; s < 2; ++s) {
       ma.sm_dep[s] = u32;
-      u32 += ma.nrows[s] << (ma.nch[s] - (s == 0 ? pl0 : pl1));
+      u32 += ma.nrows[s] << (ma.nch[s] - ma.lv[s]);
     }
     ma.sm_bf_bytes = (u32 * 4 + 15) / 16 * 16;
     const size_t smem = ma.sm_bf_bytes + bf_bytes;
