@@ -76,6 +76,22 @@ __global__ void k_ffma2(int iters, float* sink) {
   if (s == 12345.f) sink[threadIdx.x] = s;
 }
 
+template <int NACC>
+__global__ void k_dfma(int iters, float* sink) {
+  double c[NACC];
+#pragma unroll
+  for (int n = 0; n < NACC; ++n) c[n] = 0.0;
+  const double a = 1.0 + threadIdx.x * 1e-3, b = 0.5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int n = 0; n < NACC; ++n) asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(c[n]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int n = 0; n < NACC; ++n) s += c[n];
+  if (s == 12345.0) sink[threadIdx.x] = (float)s;
+}
+
 template <typename K>
 void run(const char* name, K kern, int warps, int cps, int iters, double macs_per_inst_per_warp, int nacc) {
   float* sink;
@@ -108,6 +124,7 @@ int main() {
     run("mma.sync bf16 m16n8k16 x8", k_bf16<8>, w, 1, it, 16 * 8 * 16, 8);
     run("mma.sync f64 m8n8k4 x8", k_f64<8>, w, 1, it / 4, 8 * 8 * 4, 8);
     run("ffma2 x8", k_ffma2<8>, w, 1, it * 4, 64, 8);
+    run("dfma x8", k_dfma<8>, w, 1, it, 32, 8);
   }
   run("mma.sync tf32 m16n8k8 x8", k_tf32<8>, 8, 2, it, 16 * 8 * 8, 8);
   run("mma.sync tf32 m16n8k8 x8", k_tf32<8>, 16, 2, it, 16 * 8 * 8, 8);
