@@ -181,7 +181,7 @@ tn_status tn_contract(const tn_plan* plan, tn_dtype dtype, const double* gamma, 
  * (tn_workspace_bytes(plan, dtype, L)), slice j of the range runs on lane (j - begin) mod L:
  * lane 0 on `stream`, lane l >= 1 on a library-owned stream in window l, all forked from and
  * joined back into `stream` (results identical to one lane).  Lanes = min(L, TNB_LANES
- * environment variable, default 8; TNB_ONE_LANE=1 forces one). */
+ * environment variable, default 16; TNB_ONE_LANE=1 forces one). */
 tn_status tn_contract_sliced(const tn_plan* plan, tn_dtype dtype, const double* gamma,
                              const double* beta, int32_t p, uint64_t begin, uint64_t end, void* ws,
                              size_t ws_bytes, void* stream, double* partials_dev);

@@ -77,7 +77,7 @@ __device__ __forceinline__ void tf32_split(float v, uint32_t& big, uint32_t& sma
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
                : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
@@ -359,6 +359,22 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
     for (int k = 0; k < NFR; ++k) xs[1 + k] = chunk_off(2, FB0 + k);
   }
 
+  // R chunk index (in floats) of each (batch, row block) fragment set, hoisted out of the tile loop
+  uint32_t iaf[RC][RA];
+#pragma unroll
+  for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+    for (int fa = 0; fa < RA; ++fa) {
+      uint32_t ia = ia_thr;
+#pragma unroll
+      for (int k = 0; k < NFA; ++k)
+        if ((fa >> k) & 1) ia += chunk_off(0, FB0 + k);
+#pragma unroll
+      for (int k = 0; k < NFC; ++k)
+        if ((fc >> k) & 1) ia += chunk_off(0, FB0 + NFA + NFB + k);
+      iaf[fc][fa] = ia * 2u;
+    }
+
   int cslot[3] = {0, 0, 0};
   uint32_t cpar[3] = {0u, 0u, 0u};
   bool qready = false;
@@ -423,14 +439,7 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
       for (int fc = 0; fc < RC; ++fc)
 #pragma unroll
         for (int fa = 0; fa < RA; ++fa) {
-          uint32_t ia = ia_thr;
-#pragma unroll
-          for (int k = 0; k < NFA; ++k)
-            if ((fa >> k) & 1) ia += chunk_off(0, FB0 + k);
-#pragma unroll
-          for (int k = 0; k < NFC; ++k)
-            if ((fc >> k) & 1) ia += chunk_off(0, FB0 + NFA + NFB + k);
-          ia *= 2u;
+          const uint32_t ia = iaf[fc][fa];
           tf32_split(Rraw[rf0 + ia], ab[fc][fa][0], as[fc][fa][0]);
           tf32_split(Rraw[rf0 + ia + ia_r8], ab[fc][fa][1], as[fc][fa][1]);
           tf32_split(Rraw[rf1 + ia], ab[fc][fa][2], as[fc][fa][2]);
