@@ -4,7 +4,7 @@
 
 Per phase-B op (tests/planbuf.py parses the plan buffer):
   t = max(algorithmic bytes / BW, flops / F32) + T_LAUNCH
-with flops = 8 x 2^(R + M) for a fused group (one complex multiply-add per output and summed value;
+(k_gemm_hm groups: HM_BW / HM_FL) with flops = 8 x 2^(R + M) for a fused group (one complex multiply-add per output and summed value;
 a producer -> consumer pair adds its consumer's), BW / F32 the rates the kernels reach on one B200
 (round-2 profiles: ~4.5 TB/s streaming, ~22 TFLOP/s for the SIMT GEMM groups), interpreter runs at
 ~1 us per step.  A plan's time = prefix + 2^k x per-slice time.
@@ -21,6 +21,10 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 BW = 4.5e12
 F32 = 22e12
+# k_gemm_hm (round 2, second session): two-operand groups with M >= 3 and >= 2^22 outputs on the
+# warp-level tensor cores -- C5a's top group 72 us for 335 MB / 2.15 GFLOP (4.6 TB/s, ~30 TFLOP/s)
+HM_BW = 4.6e12
+HM_FL = 30e12
 T_LAUNCH = 4e-6
 T_RUN_STEP = 1e-6
 
@@ -49,7 +53,8 @@ def plan_time(plan):
                 by += 2.0 ** R3 + sum(2.0 ** s3[0].in_[t].rank for t in range(s3[0].n_in)) - 2.0 * 2.0 ** R
                 fl += 8.0 * 2.0 ** (R3 + len(s3))
                 i += 1
-            t = max(by * 8 / BW, fl / F32) + T_LAUNCH
+            hm = op.type == planbuf.OP_GROUP and len(st) >= 3 and R >= 22
+            t = (max(by * 8 / HM_BW, fl / HM_FL) if hm else max(by * 8 / BW, fl / F32)) + T_LAUNCH
         if op.phase == 0:
             t_pre += t
         else:
