@@ -61,6 +61,7 @@ struct HArgs {
   uint32_t sm_run[3];                  // dynamic smem byte offset of the run table (element offset of run q)
   uint32_t sm_q;                       // dynamic smem byte offset of the Q fragments
   int32_t p0, p1;                      // register slots holding output bits 0 and 1
+  int32_t dbg;                         // TNB_HM_DBG (diagnostics only, wrong results): 1 skip the MMAs, 2 skip the consumer math
   int32_t stages[3];                   // ring slots per stream (2..4)
   const void* cin[kMaxIn];             // constant inputs: no output bit (C[x] = prod_t cin[t][cgx[t][x]])
   uint32_t cgx[kMaxIn][1 << kMaxGroup];
@@ -428,11 +429,12 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
     const float* Rraw = reinterpret_cast<const float*>(dsm + a.sm_in[0][cslot[0]]) + qe;
     float acc[NF][4];
 #pragma unroll
-    for (int f = 0; f < NF; ++f)
+    for (int fi = 0; fi < NF; ++fi)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[f][k] = 0.f;
+      for (int k = 0; k < 4; ++k) acc[fi][k] = 0.f;
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
+      if (a.dbg & 1) break;
       const uint32_t rf0 = rowf[4 * s + (tig >> 1)], rf1 = rowf[4 * s + 2 + (tig >> 1)];
       uint32_t ab[RC][RA][4], as[RC][RA][4];
 #pragma unroll
@@ -458,11 +460,11 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
           for (int fb = 0; fb < RB; ++fb)
 #pragma unroll
             for (int fa = 0; fa < RA; ++fa) {
-              const int f = fa + RA * (fb + RB * fc);
+              const int fi = fa + RA * (fb + RB * fc);
               const float4 q = qv[fc][fb];
-              if (pass == 0) mma_tf32(acc[f], as[fc][fa], __float_as_uint(q.x), __float_as_uint(q.y));
-              else if (pass == 1) mma_tf32(acc[f], ab[fc][fa], __float_as_uint(q.z), __float_as_uint(q.w));
-              else mma_tf32(acc[f], ab[fc][fa], __float_as_uint(q.x), __float_as_uint(q.y));
+              if (pass == 0) mma_tf32(acc[fi], as[fc][fa], __float_as_uint(q.x), __float_as_uint(q.y));
+              else if (pass == 1) mma_tf32(acc[fi], ab[fc][fa], __float_as_uint(q.z), __float_as_uint(q.w));
+              else mma_tf32(acc[fi], ab[fc][fa], __float_as_uint(q.x), __float_as_uint(q.y));
             }
     }
     // chunk versions for the next tile; release the slots this warp is done with
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
       if (++cslot[2] == a.stages[2]) { cslot[2] = 0; cpar[2] ^= 1u; }
       const float2 c3 = C3s[y];
 #pragma unroll
-      for (int reg = 0; reg < 2 * NF; ++reg) {
+      for (int reg = 0; reg < 2 * NF && !(a.dbg & 2); ++reg) {
         const float xx0 = c3.x * xr[reg][0] - c3.y * xr[reg][1], xx1 = c3.x * xr[reg][1] + c3.y * xr[reg][0];
         const float t0r = acc[reg >> 1][2 * (reg & 1)], t0i = acc[reg >> 1][2 * (reg & 1) + 1];
         oacc[reg >> 1][2 * (reg & 1)] += xx0 * t0r - xx1 * t0i;

@@ -272,6 +272,10 @@ bool plan_hm(const GDesc& g, uint64_t allowed, const int* yfirst, int ny, const 
   if (np != R - TB) return false;
   ha.out = g.out;
   ha.out_rank = R;
+  {
+    const char* e = std::getenv("TNB_HM_DBG");
+    ha.dbg = e ? std::atoi(e) : 0;
+  }
   const int cps = std::max(1, std::min(4, (int)(kHmSmemPerSm / smem)));
   if (env_flag("TNB_GEMM_DEBUG")) {
     std::fprintf(stderr, "k_gemm_hm R=%d M=%d frag(a,b,c)=(%d,%d,%d) p=(%d,%d) nch=(%u,%u,%u) runl=(%u,%u,%u) rows=(%u,%u) S=(%d,%d,%d) smem=%zu cps=%d nc=%d outbits=",
