@@ -10,8 +10,8 @@
 //   R'[m][2x+e] = (Re, Im)_e of R[m][x],
 //   Q'[2x][2j] = Re q, Q'[2x][2j+1] = Im q, Q'[2x+1][2j] = -Im q, Q'[2x+1][2j+1] = Re q  (q = C[x] Q[x][j]),
 // so the MMA's (c0, c1) are (Re, Im) of one complex output.  Every operand value v is split as
-// big = cvt.rna.tf32(v), small = v - big; D += Rs Qb + Rb Qs + Rb Qb (the dropped Rs Qs term is
-// ~2^-22 relative; measured 7e-7 against 7e-4 for one TF32 product, profiles/r01/tc/NOTES.md).
+// big = v truncated to TF32, small = v - big; D += Rs Qb + Rb Qs + Rb Qb (the dropped Rs Qs term is
+// ~2^-20 relative; 3xTF32 measured 7e-7 against 7e-4 for one TF32 product, profiles/r01/tc/NOTES.md).
 //
 // Why mma.sync and not tcgen05 here: an MMA row of R is a set of R-only output bits whose elements
 // are scattered over R's bit order (SURVEY F5 layouts), so each thread gathers its fragment values
@@ -70,9 +70,11 @@ struct HArgs {
   uint8_t perm[64];                    // logical tile-index bit b -> output bit (traversal order)
 };
 
+// v = big + small with big = v truncated to TF32 (the low 13 mantissa bits cleared: one LOP3; the
+// cvt.rna.tf32 rounding form is a ~5-instruction sequence on sm_100a) and small = v - big exactly;
+// the MMA then truncates small to TF32 as well, so big + small carries ~21 bits of v
 __device__ __forceinline__ void tf32_split(float v, uint32_t& big, uint32_t& small) {
-  uint32_t b;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v));
+  const uint32_t b = __float_as_uint(v) & 0xFFFFE000u;
   big = b;
   small = __float_as_uint(v - __uint_as_float(b));
 }
@@ -360,6 +362,13 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
     for (int k = 0; k < NFR; ++k) xs[1 + k] = chunk_off(2, FB0 + k);
   }
 
+  // R chunk row offsets (in floats) of this lane's x values per k-step (x = 4s + tig/2 and + 2)
+  uint32_t rfr[KS][2];
+#pragma unroll
+  for (int s = 0; s < KS; ++s) {
+    rfr[s][0] = ((uint32_t)a.row[0][4 * s + (tig >> 1)] << a.nch[0]) * 2u;
+    rfr[s][1] = ((uint32_t)a.row[0][4 * s + 2 + (tig >> 1)] << a.nch[0]) * 2u;
+  }
   // R chunk index (in floats) of each (batch, row block) fragment set, hoisted out of the tile loop
   uint32_t iaf[RC][RA];
 #pragma unroll
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
       if (a.dbg & 1) break;
-      const uint32_t rf0 = rowf[4 * s + (tig >> 1)], rf1 = rowf[4 * s + 2 + (tig >> 1)];
+      const uint32_t rf0 = rfr[s][0], rf1 = rfr[s][1];
       uint32_t ab[RC][RA][4], as[RC][RA][4];
 #pragma unroll
       for (int fc = 0; fc < RC; ++fc)
