@@ -61,6 +61,7 @@ struct HArgs {
   uint32_t sm_run[3];                  // dynamic smem byte offset of the run table (element offset of run q)
   uint32_t sm_q;                       // dynamic smem byte offset of the Q fragments
   int32_t p0, p1;                      // register slots holding output bits 0 and 1
+  uint32_t rpad;                       // floats of padding after every R chunk row (shared-memory banks)
   int32_t dbg;                         // TNB_HM_DBG (diagnostics only, wrong results): 1 skip the MMAs, 2 skip the consumer math
   int32_t stages[3];                   // ring slots per stream (2..4)
   const void* cin[kMaxIn];             // constant inputs: no output bit (C[x] = prod_t cin[t][cgx[t][x]])
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
   }
   for (int b = tid; b < NB; b += kThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
   if (tid < (uint32_t)K) {
-    rowf[tid] = ((uint32_t)a.row[0][tid] << a.nch[0]) * 2u;
+    rowf[tid] = ((uint32_t)a.row[0][tid] << a.nch[0]) * 2u + (uint32_t)a.row[0][tid] * a.rpad;
     float2 c = make_float2(1.f, 0.f);
     for (int t = 0; t < a.nc; ++t) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + a.cgx[t][tid]));
     Cs[tid] = c;
@@ -293,7 +294,9 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
         const float2* src = static_cast<const float2*>(a.in[u]) + base;
         const uint32_t dst = smem_u32(dsm + a.sm_in[u][slot]);
         const uint32_t* tab = reinterpret_cast<const uint32_t*>(dsm + a.sm_run[u]);
-        for (uint32_t q = lane; q < nr; q += 32) hm_bulk(dst + q * bytes, src + tab[q], bytes, bar);
+        // R rows are padded by rpad floats (run q of row q >> (nch - runl))
+        const uint32_t pad_b = u == 0 ? a.rpad * 4u : 0u, lpr = a.nch[u] - a.runl[u];
+        for (uint32_t q = lane; q < nr; q += 32) hm_bulk(dst + q * bytes + (q >> lpr) * pad_b, src + tab[q], bytes, bar);
       };
       issue(0, cur[0]);
       issue(1, cur[1]);
@@ -366,8 +369,9 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
   uint32_t rfr[KS][2];
 #pragma unroll
   for (int s = 0; s < KS; ++s) {
-    rfr[s][0] = ((uint32_t)a.row[0][4 * s + (tig >> 1)] << a.nch[0]) * 2u;
-    rfr[s][1] = ((uint32_t)a.row[0][4 * s + 2 + (tig >> 1)] << a.nch[0]) * 2u;
+    const uint32_t r0 = a.row[0][4 * s + (tig >> 1)], r1 = a.row[0][4 * s + 2 + (tig >> 1)];
+    rfr[s][0] = (r0 << a.nch[0]) * 2u + r0 * a.rpad;
+    rfr[s][1] = (r1 << a.nch[0]) * 2u + r1 * a.rpad;
   }
   // R chunk index (in floats) of each (batch, row block) fragment set, hoisted out of the tile loop
   uint32_t iaf[RC][RA];

@@ -230,6 +230,11 @@ bool plan_hm(const GDesc& g, uint64_t allowed, const int* yfirst, int ny, const 
     ha.mask[s] = in.out_mask;
     ha.pv[s] = in.pv;
     sz[s] = ha.nrows[s] << k;
+    if (s == 0) {   // R rows 16 floats apart in the banks when the row stride is a multiple of 32 floats
+      const char* e = std::getenv("TNB_HM_RPAD");
+      ha.rpad = (e && e[0] == '0') ? 0u : (((2u << k) % 32u) == 0u ? 16u : 0u);
+      sz[s] += ha.nrows[s] * ha.rpad / 2u;
+    }
     nruns[s] = ha.nrows[s] << (k - L);
   }
   if (xop) {   // X quads: output bits 0, 1 at X chunk positions 0, 1
