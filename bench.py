@@ -99,10 +99,16 @@ MMA_SYNC_TF32_TFLOPS = 276.8
 TENSOR_FAMILIES = {"k_gemm_hm", "k_fc_hm"}
 
 
-def alu_peak_tflops(kernel: str):
+# FP64 FMA throughput measured on this pool's B200 (DFMA 18.1 TMAC/s, profiles/r02/hm/mma_rate.txt)
+FP64_TFLOPS = 36.2
+
+
+def alu_peak_tflops(kernel: str, c128: bool = False):
     """(peak, source) of a kernel family's arithmetic: FP32 FFMA for the SIMT kernels; for the
     mma.sync 3xTF32 kernels the measured tf32 rate / 3 (three products per complex-as-real MAC set),
     i.e. the FP32-equivalent rate of the flops bench counts (8 per complex multiply-add)."""
+    if c128:
+        return FP64_TFLOPS, "measured DFMA 18.1 TMAC/s (FP64 arithmetic of the c128 path), profiles/r02/hm/mma_rate.txt"
     if kernel in TENSOR_FAMILIES:
         return MMA_SYNC_TF32_TFLOPS / 3.0, ("measured mma.sync tf32 276.8 TFLOP/s / 3 (3xTF32), "
                                            "profiles/r02/hm/mma_rate.txt")
@@ -464,7 +470,7 @@ def main():
         d = fam[dom]
         # arithmetic peak of the family: FP32 FFMA for the SIMT kernels, the measured mma.sync tf32
         # rate / 3 (3xTF32 products) for the warp-level tensor-core kernels
-        fp32_peak, alu_src = alu_peak_tflops(dom)
+        fp32_peak, alu_src = alu_peak_tflops(dom, dtype == T.TN_C128)
         achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
         t_hbm = d["bytes"] / (peak * 1e9)
         t_alu = d["flops"] / (fp32_peak * 1e12)

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtnb200.so")
 OBJ = os.path.join(CSRC, "build")
-SOURCES = ["runtime.cu", "planner.cpp", "launch_gemm.cu", "launch_gemm_hm.cu", "launch_gemm_tc.cu", "launch_gemm_fc.cu", "launch_fc_tc.cu", "launch_pair.cu", "launch_bucket.cu",
+SOURCES = ["runtime.cu", "planner.cpp", "launch_gemm.cu", "launch_gemm_hm.cu", "launch_gemm_hm64.cu", "launch_gemm_tc.cu", "launch_gemm_fc.cu", "launch_fc_tc.cu", "launch_pair.cu", "launch_bucket.cu",
            "launch_group_c64.cu", "launch_group_c128.cu"]
 HEADERS = ["kernels.cuh", "kernels_tc.cuh", "kernels_hm.cuh", "kernels_fc.cuh", "kernels_fctc.cuh", "launch.cuh", "launch_group.inl", "plan_format.h", "planner.h",
            os.path.join("..", "..", "include", "tn_b200.h")]

@@ -545,3 +545,260 @@ __global__ void __launch_bounds__((32 << WB) + 32, FC ? 2 : 3) k_gemm_hm(const H
 }
 
 }  // namespace tnb
+
+namespace tnb {
+
+// ---------------------------------------------------------------- complex128: k_gemm_hm64
+// The same two-operand merge group for c128 on the FP64 tensor path: mma.sync.m8n8k4.f64 (DMMA),
+// one product, no split (DMMA and DFMA both measured ~18 TMAC/s on B200, profiles/r02/hm/mma_rate.txt;
+// what DMMA buys is 256 MACs per warp instruction instead of 32, for a kernel family bound by its
+// instruction stream).  Fragments (lane = 4 g + tig): A'[g][tig] with x = 2s + tig/2, e = tig & 1;
+// B'[k = tig][n = g] (complex column g / 2, f = g & 1); C[g][2 tig], C[g][2 tig + 1] = (Re, Im) of
+// complex column tig.  Tile-local bits: 0, 1 tig (Q-only), 2, 3, 4 g (R-only), then WB warp bits,
+// then the fragment bits (register slots 0 .. 2: NFA R-only, NFB Q-only, NFC shared); output bit 0
+// is register slot P0, so two complex values = one 32-byte sector leave in one 256-bit store.
+// Ring, producer warp and traversal as k_gemm_hm (HArgs; element = double2, run bytes 16 << runl).
+__device__ __forceinline__ void mma_f64(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void st_v4d_cs(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+template <int P0, int NF>
+__device__ __forceinline__ void hm64_store(double* ob, const double (&acc)[NF][2], const uint32_t (&so)[3]) {
+  constexpr int NR = NF == 8 ? 3 : (NF == 4 ? 2 : 1);
+#pragma unroll
+  for (int q = 0; q < NF; ++q) {
+    if (q & (1 << P0)) continue;
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k)
+      if ((q >> k) & 1) o += so[k];
+    const int q1 = q | (1 << P0);
+    st_v4d_cs(ob + 2 * (size_t)o, acc[q][0], acc[q][1], acc[q1][0], acc[q1][1]);
+  }
+}
+
+template <int M, int NFA, int NFB, int NFC, int WB>
+__global__ void __launch_bounds__((32 << WB) + 32, 2) k_gemm_hm64(const HArgs a) {
+  constexpr int NW = 1 << WB;
+  constexpr int kThreads = 32 * NW + 32;
+  constexpr int K = 1 << M;
+  constexpr int KS = K / 2;                // k-steps of 4 real values (2 complex x)
+  constexpr int RA = 1 << NFA, RB = 1 << NFB, RC = 1 << NFC;
+  constexpr int NFR = NFA + NFB + NFC;
+  constexpr int NF = 1 << NFR;
+  constexpr int TB = 5 + WB + NFR;
+  constexpr int NB = 64 - TB;
+  static_assert(M >= 1 && M <= kMaxGroup && NFR == 3, "k_gemm_hm64: 1 <= M <= 5, 3 fragment bits");
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+  const uint32_t g = lane >> 2, tig = lane & 3u;
+  const uint64_t n_tiles = 1ull << (a.out_rank - TB);
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ uint32_t fbit[2][NB];
+  __shared__ uint32_t fcum[2][NB + 1];
+  __shared__ uint64_t pbit[NB], pcum[NB + 1];
+  __shared__ double2 Cs[K];
+  __shared__ __align__(8) uint64_t bars[2][2][4];
+  const int nperm = a.out_rank - TB;
+  for (int i = tid; i < 2 * NB; i += kThreads) {
+    const int t = i / NB, b = i % NB;
+    fbit[t][b] = b < nperm ? (uint32_t)fmap(1ull << a.perm[b], a.mask[t], a.pv[t]) : 0u;
+  }
+  for (int b = tid; b < NB; b += kThreads) pbit[b] = b < nperm ? 1ull << a.perm[b] : 0ull;
+  if (tid < (uint32_t)K) {
+    double2 c = make_double2(1.0, 0.0);
+    for (int t = 0; t < a.nc; ++t) c = cmul(c, __ldg(static_cast<const double2*>(a.cin[t]) + a.cgx[t][tid]));
+    Cs[tid] = c;
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t lp = a.nch[u] - a.runl[u];
+    const uint32_t nr = a.nrows[u] << lp;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm + a.sm_run[u]);
+    for (uint32_t q = tid; q < nr; q += kThreads) {
+      const uint32_t w = (q & ((1u << lp) - 1u)) << a.runl[u];
+      uint32_t off = a.rowoff[u][q >> lp];
+      for (uint32_t k = a.runl[u]; k < a.nch[u]; ++k)
+        if ((w >> k) & 1u) off += a.posoff[u][k];
+      tab[q] = off;
+    }
+  }
+  if (tid == 0) {
+    for (int u = 0; u < 2; ++u)
+      for (int s = 0; s < a.stages[u]; ++s) {
+        mbar_init(&bars[0][u][s], 1);
+        mbar_init(&bars[1][u][s], NW);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nbu = min(NB - 1, max(0, nperm));
+  if (tid < 2u) {
+    uint32_t c = 0;
+    fcum[tid][0] = 0;
+    for (int b = 0; b < nbu; ++b) { c += fbit[tid][b]; fcum[tid][b + 1] = c; }
+  }
+  if (tid == 3u) {
+    uint64_t c = 0;
+    pcum[0] = 0;
+    for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
+  }
+  __syncthreads();
+  const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+  uint64_t obase = 0;
+  for (int b = 0; b < nperm && (t0 >> b); ++b)
+    if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
+  const uint32_t bar_full = smem_u32(&bars[0][0][0]);
+  const uint32_t bar_empty = smem_u32(&bars[1][0][0]);
+
+  if (wid == (uint32_t)NW) {                // producer warp (as k_gemm_hm)
+    if (t0 < t1) {
+      uint32_t cur[2];
+      int ver[2] = {0, 0};
+      for (int u = 0; u < 2; ++u) cur[u] = (uint32_t)fmap(obase, a.mask[u], a.pv[u]);
+      auto issue = [&](int u) {
+        const int S = a.stages[u];
+        const int v = ver[u], slot = v % S;
+        if (v >= S) hm_wait(bar_empty + (uint32_t)(u * 4 + slot) * 8u, (uint32_t)((v / S) - 1) & 1u);
+        const uint32_t nr = a.nrows[u] << (a.nch[u] - a.runl[u]);
+        const uint32_t bytes = 16u << a.runl[u];
+        const uint32_t bar = bar_full + (uint32_t)(u * 4 + slot) * 8u;
+        if (lane == 0) hm_expect_tx(bar, nr * bytes);
+        __syncwarp();
+        const double2* src = static_cast<const double2*>(a.in[u]) + cur[u];
+        const uint32_t dst = smem_u32(dsm + a.sm_in[u][slot]);
+        const uint32_t* tab = reinterpret_cast<const uint32_t*>(dsm + a.sm_run[u]);
+        for (uint32_t q = lane; q < nr; q += 32) hm_bulk(dst + q * bytes, src + tab[q], bytes, bar);
+      };
+      issue(0);
+      issue(1);
+      for (uint64_t tile = t0; tile + 1 < t1; ++tile) {
+        const int r = __ffsll((long long)~tile) - 1;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (fbit[u][r] != fcum[u][r]) {
+            cur[u] = cur[u] + fbit[u][r] - fcum[u][r];
+            ++ver[u];
+            issue(u);
+          }
+      }
+    }
+    return;
+  }
+
+  auto chunk_off = [&](int u, int k) -> uint32_t { return a.chbit[u][k] >= 0 ? 1u << a.chbit[u][k] : 0u; };
+  auto obit = [&](int k) -> uint32_t { return 1u << a.outbit[k]; };
+  constexpr int FB0 = 5 + WB;
+  uint32_t othr = 0, ia_thr = 0, ib_w = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if ((tig >> k) & 1u) othr += obit(k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if ((g >> k) & 1u) { othr += obit(2 + k); ia_thr += chunk_off(0, 2 + k); }
+#pragma unroll
+  for (int k = 0; k < WB; ++k)
+    if ((wid >> k) & 1u) { othr += obit(5 + k); ia_thr += chunk_off(0, 5 + k); ib_w += chunk_off(1, 5 + k); }
+  uint32_t so[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) so[k] = obit(FB0 + k);
+  const uint32_t ib_lane = ib_w + (((g >> 1) & 1u) ? chunk_off(1, 0) : 0u) + (((g >> 2) & 1u) ? chunk_off(1, 1) : 0u);
+  const uint32_t qf = g & 1u, qe = tig & 1u;
+  double* qfrag = reinterpret_cast<double*>(dsm + a.sm_q) + (size_t)wid * RB * RC * KS * 32 + lane;
+  uint32_t rfr[KS];                        // R chunk row offset (in doubles) of x = 2s + tig / 2
+#pragma unroll
+  for (int s = 0; s < KS; ++s) rfr[s] = ((uint32_t)a.row[0][2 * s + (tig >> 1)] << a.nch[0]) * 2u;
+  uint32_t iaf[RC][RA];
+#pragma unroll
+  for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+    for (int fa = 0; fa < RA; ++fa) {
+      uint32_t ia = ia_thr;
+#pragma unroll
+      for (int k = 0; k < NFA; ++k)
+        if ((fa >> k) & 1) ia += chunk_off(0, FB0 + k);
+#pragma unroll
+      for (int k = 0; k < NFC; ++k)
+        if ((fc >> k) & 1) ia += chunk_off(0, FB0 + NFA + NFB + k);
+      iaf[fc][fa] = ia * 2u + qe;
+    }
+  double* out = static_cast<double*>(a.out);
+  int cslot[2] = {0, 0};
+  uint32_t cpar[2] = {0u, 0u};
+  bool qready = false;
+  for (uint64_t tile = t0; tile < t1; ++tile) {
+    const int r = __ffsll((long long)~tile) - 1;
+    if (!qready) {
+      hm_wait(bar_full + (uint32_t)(4 + cslot[1]) * 8u, cpar[1]);
+      const double2* Qraw = reinterpret_cast<const double2*>(dsm + a.sm_in[1][cslot[1]]);
+#pragma unroll
+      for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+        for (int fb = 0; fb < RB; ++fb) {
+          uint32_t ib = ib_lane;
+#pragma unroll
+          for (int k = 0; k < NFB; ++k)
+            if ((fb >> k) & 1) ib += chunk_off(1, FB0 + NFA + k);
+#pragma unroll
+          for (int k = 0; k < NFC; ++k)
+            if ((fc >> k) & 1) ib += chunk_off(1, FB0 + NFA + NFB + k);
+#pragma unroll
+          for (int s = 0; s < KS; ++s) {
+            const int x = 2 * s + (int)(tig >> 1);
+            const double2 q = cmul(Qraw[((uint32_t)a.row[1][x] << a.nch[1]) + ib], Cs[x]);
+            qfrag[((fc * RB + fb) * KS + s) * 32] = qe == qf ? q.x : (qe ? -q.y : q.y);
+          }
+        }
+      __syncwarp();
+      if (lane == 0) hm_arrive(bar_empty + (uint32_t)(4 + cslot[1]) * 8u);
+      qready = true;
+    }
+    hm_wait(bar_full + (uint32_t)cslot[0] * 8u, cpar[0]);
+    const double* Rraw = reinterpret_cast<const double*>(dsm + a.sm_in[0][cslot[0]]);
+    double acc[NF][2];
+#pragma unroll
+    for (int fi = 0; fi < NF; ++fi) { acc[fi][0] = 0.0; acc[fi][1] = 0.0; }
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      double av[RC][RA], qv[RC][RB];
+#pragma unroll
+      for (int fc = 0; fc < RC; ++fc) {
+#pragma unroll
+        for (int fa = 0; fa < RA; ++fa) av[fc][fa] = Rraw[rfr[s] + iaf[fc][fa]];
+#pragma unroll
+        for (int fb = 0; fb < RB; ++fb) qv[fc][fb] = qfrag[((fc * RB + fb) * KS + s) * 32];
+      }
+#pragma unroll
+      for (int fc = 0; fc < RC; ++fc)
+#pragma unroll
+        for (int fb = 0; fb < RB; ++fb)
+#pragma unroll
+          for (int fa = 0; fa < RA; ++fa) mma_f64(acc[fa + RA * (fb + RB * fc)], av[fc][fa], qv[fc][fb]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (fbit[u][r] != fcum[u][r]) {
+        if (u == 0) {
+          __syncwarp();
+          if (lane == 0) hm_arrive(bar_empty + (uint32_t)cslot[0] * 8u);
+        } else {
+          qready = false;
+        }
+        if (++cslot[u] == a.stages[u]) { cslot[u] = 0; cpar[u] ^= 1u; }
+      }
+    double* ob = out + 2 * (obase + othr);
+    switch (a.p0) {
+      case 0: hm64_store<0, NF>(ob, acc, so); break;
+      case 1: hm64_store<1, NF>(ob, acc, so); break;
+      case 2: hm64_store<2, NF>(ob, acc, so); break;
+      default: break;
+    }
+    obase = obase + pbit[r] - pcum[r];
+  }
+}
+
+}  // namespace tnb

@@ -96,6 +96,10 @@ inline bool env_flag(const char* name) {
   const char* v = std::getenv(name);
   return v && v[0] == '1';
 }
+inline bool env_flag0(const char* name) {   // set to "0"
+  const char* v = std::getenv(name);
+  return v && v[0] == '0';
+}
 inline int gemm_stages() {   // TNB_GEMM_STAGES=2..4 (default 3)
   static const int s = [] {
     const char* v = std::getenv("TNB_GEMM_STAGES");
@@ -155,6 +159,8 @@ bool try_launch_gemm_tc(const GDesc& g, cudaStream_t st);
 // the same GEMM groups on mma.sync tf32 (k_gemm_hm, c64, 3xTF32); false when the shape does not qualify
 bool try_launch_gemm_hm(const GDesc& g, cudaStream_t st);
 bool gemm_hm_enabled();                                                          // TNB_GEMM_HM=0 off
+// c128 groups on mma.sync f64 (k_gemm_hm64); false when the shape does not qualify
+bool try_launch_gemm_hm64(const GDesc& g, cudaStream_t st);
 // producer group g on mma.sync tf32 consumed by g3 in registers (k_fc_hm); false when it does not qualify
 bool try_launch_fc_hm(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
 bool fc_hm_enabled();                                                            // TNB_FC_HM=0 off

@@ -59,6 +59,10 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   // the top group; smaller or M = 2 groups are bound by its per-tile pipeline, profiles/r02/hm/)
   if (std::is_same<T, float2>::value && gemm_hm_enabled() && g.M >= 3 && g.out_rank >= 22 && try_launch_gemm_hm(g, st))
     return true;
+  // c128: k_gemm_hm64 (DMMA) for groups of >= 2^20 outputs (TNB_GEMM_HM64=0 off)
+  if (std::is_same<T, double2>::value && gemm_hm_enabled() && !env_flag0("TNB_GEMM_HM64") && g.out_rank >= 20 &&
+      try_launch_gemm_hm64(g, st))
+    return true;
   // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
   const int wb0 = gemm_wb(), wb1 = 5 - wb0;
   return try_launch_gemm_impl<T>(g, st, wb0) || try_launch_gemm_impl<T>(g, st, wb1);

@@ -397,3 +397,4 @@ bool try_launch_fc_hm(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
 }
 
 }  // namespace tnb
+

@@ -1307,10 +1307,11 @@ extern "C" tn_status tn_eliminate_group(tn_dtype dtype, int32_t M, int32_t n_in,
        : kernel == 3 ? try_launch_group<float2>(g, st)
        : (try_launch_gemm<float2>(g, st) || try_launch_pair<float2>(g, st) || try_launch_group<float2>(g, st));
   } else {
-    ok = kernel == 1 ? try_launch_gemm<double2>(g, st)
+    ok = kernel == 1 ? try_launch_gemm_simt<double2>(g, st)
+       : kernel == 5 ? try_launch_gemm_hm64(g, st)
        : kernel == 2 ? try_launch_pair<double2>(g, st)
        : kernel == 3 ? try_launch_group<double2>(g, st)
-       : (try_launch_pair<double2>(g, st) || try_launch_group<double2>(g, st));
+       : (try_launch_gemm<double2>(g, st) || try_launch_pair<double2>(g, st) || try_launch_group<double2>(g, st));
   }
   if (!ok) return fail(TN_E_INVAL, "tn_eliminate_group: no kernel instantiation for this shape");
   CU(cudaGetLastError());

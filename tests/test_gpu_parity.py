@@ -313,6 +313,34 @@ def test_gemm_hm_vs_oracle(case):
     assert err < TOL[T.TN_C64] * 0.1, err
 
 
+HM64_CASES = HM_CASES + [
+    (18, 1, "abcaacaabbcacbaaca", None, None),      # M = 1: one k-step (K = 2 complex)
+    (19, 2, "bacbaacaabcacbcabaa", None, None),     # output bit 0 held by Q only
+]
+
+
+@pytest.mark.parametrize("case", range(len(HM64_CASES)))
+def test_gemm_hm64_vs_oracle(case):
+    """k_gemm_hm64 (complex128 merge groups on mma.sync m8n8k4 f64: one FP64 product, no split) vs the
+    oracle at the complex128 tolerance; the HM shapes plus M = 1 and a Q-held output bit 0."""
+    out_rank, M, cls_s, xa, xb = HM64_CASES[case]
+    rng = np.random.default_rng(7200 + case)
+    cls = list(cls_s)
+    assert len(cls) == out_rank
+    masks, xms, shapes = _gemm_group(rng, out_rank, M, cls, xa, xb)
+    arrays = [rng.uniform(-1, 1, 2 ** r) + 1j * rng.uniform(-1, 1, 2 ** r) for r in shapes]
+    dev = [torch.tensor(a, dtype=torch.complex128, device="cuda") for a in arrays]
+    out = torch.full((2 ** out_rank,), float("nan"), dtype=torch.complex128, device="cuda")
+    B.tn_eliminate_group(T.TN_C128, M, [d.data_ptr() for d in dev], masks, xms, out.data_ptr(), out_rank,
+                         5, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    ref = _oracle_group(arrays, masks, xms, M, out_rank)
+    assert np.all(np.isfinite(got)), "output element not written"
+    err = np.max(np.abs(got - ref)) / (np.max(np.abs(ref)) + 1e-30)
+    assert err < TOL[T.TN_C128] * 0.1, err
+
+
 def test_gemm_hm_declines_tile_dependent_constants():
     """A constant factor holding an output bit would force the Q fragments to be rebuilt every
     tile: k_gemm_hm declines (the library's choice then takes k_gemm)."""
