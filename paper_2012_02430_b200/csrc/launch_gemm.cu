@@ -51,6 +51,11 @@ inline int gemm_min_m() {   // TNB_GEMM_MIN_M: groups summing fewer indices go t
   return v;
 }
 
+inline int hm64_min_r() {
+  const char* e = std::getenv("TNB_HM64_MIN_R");
+  return e ? std::atoi(e) : 20;
+}
+
 template <typename T>
 bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   if (g.M < gemm_min_m()) return false;
@@ -59,8 +64,8 @@ bool try_launch_gemm(const GDesc& g, cudaStream_t st) {
   // the top group; smaller or M = 2 groups are bound by its per-tile pipeline, profiles/r02/hm/)
   if (std::is_same<T, float2>::value && gemm_hm_enabled() && g.M >= 3 && g.out_rank >= 22 && try_launch_gemm_hm(g, st))
     return true;
-  // c128: k_gemm_hm64 (DMMA) for groups of >= 2^20 outputs (TNB_GEMM_HM64=0 off)
-  if (std::is_same<T, double2>::value && gemm_hm_enabled() && !env_flag0("TNB_GEMM_HM64") && g.out_rank >= 20 &&
+  // c128: k_gemm_hm64 (DMMA) for groups of >= 2^TNB_HM64_MIN_R outputs (default 20; TNB_GEMM_HM64=0 off)
+  if (std::is_same<T, double2>::value && gemm_hm_enabled() && !env_flag0("TNB_GEMM_HM64") && g.out_rank >= hm64_min_r() &&
       try_launch_gemm_hm64(g, st))
     return true;
   // the preferred CTA size (gemm_wb()) first, the other one when its shared-memory budget is too small
