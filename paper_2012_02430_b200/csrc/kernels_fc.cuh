@@ -43,6 +43,8 @@ struct FArgs {
   uint64_t omask;                              // (1 << R3) - 1: the o part of a T offset
   int32_t xpf;                                 // 1: prefetch the next tile's X lines into L2 (X holds
                                                // output bits 0..4 at its positions 0..4)
+  uint32_t* sem;                               // split consumer blocks: one zeroed counter per CTA
+                                               // boundary (nullptr: whole blocks per CTA)
 };
 
 template <int M, int RAB, int RBB, int WB>
@@ -98,12 +100,22 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
     pcum[0] = 0;
     for (int b = 0; b < nbu; ++b) { c += pbit[b]; pcum[b + 1] = c; }
   }
-  // whole groups of 2^M3 tiles per CTA (a consumer output block is finished inside one CTA)
-  const uint64_t n_groups = n_tiles >> f.M3;
-  const uint64_t gper = (n_groups + gridDim.x - 1) / gridDim.x;
-  const uint64_t t0 = ((uint64_t)blockIdx.x * gper) << f.M3;
-  const uint64_t t1e = (((uint64_t)blockIdx.x + 1) * gper) << f.M3;
-  const uint64_t t1 = t1e < n_tiles ? t1e : n_tiles;
+  uint64_t t0, t1;
+  if (f.sem) {
+    // balanced contiguous tile ranges (floor partition; >= 2^M3 tiles each, the host keeps grid <=
+    // the number of blocks): a consumer output block (2^M3 consecutive tiles) spans at most two
+    // CTAs, whose two partial sums meet through sem[boundary] (see the flush below)
+    t0 = (uint64_t)blockIdx.x * n_tiles / gridDim.x;
+    t1 = ((uint64_t)blockIdx.x + 1) * n_tiles / gridDim.x;
+  } else {
+    // whole groups of 2^M3 tiles per CTA (a consumer output block is finished inside one CTA)
+    const uint64_t n_groups = n_tiles >> f.M3;
+    const uint64_t gper = (n_groups + gridDim.x - 1) / gridDim.x;
+    t0 = ((uint64_t)blockIdx.x * gper) << f.M3;
+    const uint64_t t1e = (((uint64_t)blockIdx.x + 1) * gper) << f.M3;
+    t1 = t1e < n_tiles ? t1e : n_tiles;
+  }
+  __shared__ uint32_t s_arrive;
   uint64_t obase = 0;
   for (int b = 0; b < nperm && (t0 >> b); ++b)
     if ((t0 >> b) & 1) obase |= 1ull << a.perm[b];
@@ -219,7 +231,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
   for (uint64_t tile = t0; tile < t1; ++tile) {
     const int r = __ffsll((long long)~tile) - 1;
     const uint32_t y = (uint32_t)tile & ymask;
-    if (y == 0u) {                         // a new consumer output block
+    if (y == 0u || tile == t0) {           // a new consumer output block (or this CTA's part of one)
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
@@ -330,12 +342,46 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
         asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(oacc[i][j]) : "l"(f2_pack(tv.x, tv.x)), "l"(f2_pack(xx.x, xx.y)));
         asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(oacc[i][j]) : "l"(f2_pack(-tv.y, tv.y)), "l"(f2_pack(xx.y, xx.x)));
       }
-    if (y == ymask) {                      // last y of the block: the consumer output is final
+    if (y == ymask || tile + 1 == t1) {    // last y of the block (or of this CTA's part of it)
       float2* ot = out3 + (obase & f.omask) + othr;
+      if (tile - y >= t0 && y == ymask) {  // the whole block ran here: the consumer output is final
 #pragma unroll
-      for (int i = 0; i < RA; ++i)
+        for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
+          for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
+      } else {
+        // a block split between this CTA and its neighbour: out = P_first + P_second, the first
+        // arriving CTA stores its partial and publishes it, the second adds its own (float
+        // addition commutes, so the bits do not depend on the arrival order)
+        uint32_t* sem = f.sem + (tile - y < t0 ? blockIdx.x : blockIdx.x + 1);
+        __syncthreads();
+        if (tid == 0) s_arrive = atomicAdd(sem, 1u);
+        __syncthreads();
+        if (s_arrive == 0u) {
+#pragma unroll
+          for (int i = 0; i < RA; ++i)
+#pragma unroll
+            for (int j = 0; j < RB; ++j) __stcg(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) atomicAdd(sem, 1u);   // published (2 arrivals + 1 publish = 3)
+        } else {
+          if (tid == 0) {
+            while (atomicAdd(sem, 0u) != 3u) __nanosleep(64);
+            *sem = 0u;                        // zero again for the next launch (stream-ordered)
+          }
+          __syncthreads();
+          __threadfence();
+#pragma unroll
+          for (int i = 0; i < RA; ++i)
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+              const float2 p = __ldcg(ot + ora[i] + orb[j]);
+              const float2 q = f2_unpack(oacc[i][j]);
+              __stcs(ot + ora[i] + orb[j], make_float2(p.x + q.x, p.y + q.y));
+            }
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u)

@@ -166,7 +166,11 @@ bool try_launch_fc_hm(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st)
 bool fc_hm_enabled();                                                            // TNB_FC_HM=0 off
 bool gemm_tc_enabled();                                                          // TNB_GEMM_TC=1
 // producer group g (GEMM-shaped) computed tile by tile and consumed by group g3 (its input tin)
-template <typename T> bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
+// sem: kFcSemPerOp zeroed counters owned by this launch site (k_gemm_fc's split consumer blocks;
+// nullptr: whole blocks per CTA)
+constexpr int kFcSemPerOp = 1024;
+template <typename T> bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st,
+                                              uint32_t* sem = nullptr);
 // the same pair with the producer GEMM on tcgen05 (k_fc_tc, c64); false when the shape does not qualify
 bool try_launch_fc_tc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st);
 bool fc_tc_enabled();                                                            // TNB_FC_TC=0/1

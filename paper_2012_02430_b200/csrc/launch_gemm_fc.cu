@@ -60,18 +60,32 @@ inline int fc_wb() {   // TNB_FC_WB = 2 (4-warp CTAs, 4 per SM) or 3 (8-warp CTA
   } while (0)
 
 template <typename T>
-bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, int WB);
+bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, int WB, uint32_t* sem);
 
-template <typename T>
-bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st) {
-  const int wb0 = fc_wb();
-  return try_launch_gemm_fc_wb<T>(g, g3, tin, st, wb0) || try_launch_gemm_fc_wb<T>(g, g3, tin, st, 5 - wb0);
+inline bool fc_split() {   // TNB_FC_SPLIT=1: consumer blocks split between neighbouring CTAs (balanced
+                           // per-SM load; C5a: the launch 209 vs 222 us alone, but the step with 16
+                           // slice lanes 98.0 vs 100.5 /s -- the lanes fill the idle slots), off;
+                           // read per launch (the parity test runs both in one process)
+  const char* e = std::getenv("TNB_FC_SPLIT");
+  return e && e[0] == '1';
+}
+
+inline unsigned fc_cps() {   // TNB_FC_CPS: k_gemm_fc CTAs per SM in the grid (default: as many as fit)
+  static const unsigned v = [] { const char* e = std::getenv("TNB_FC_CPS"); return e ? (unsigned)std::atoi(e) : 0u; }();
+  return v;
 }
 
 template <typename T>
-bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, int WB) {
+bool try_launch_gemm_fc(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, uint32_t* sem) {
+  const int wb0 = fc_wb();
+  if (!fc_split()) sem = nullptr;
+  return try_launch_gemm_fc_wb<T>(g, g3, tin, st, wb0, sem) || try_launch_gemm_fc_wb<T>(g, g3, tin, st, 5 - wb0, sem);
+}
+
+template <typename T>
+bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_t st, int WB, uint32_t* sem) {
   if constexpr (!std::is_same<T, float2>::value) {
-    (void)g; (void)g3; (void)tin; (void)st; (void)WB;
+    (void)g; (void)g3; (void)tin; (void)st; (void)WB; (void)sem;
     return false;
   } else {
     if (gemm_disabled() || g.M < 1 || g.M > kMaxGroup || g.n < 2) FC_DECLINE("producer M / inputs");
@@ -297,7 +311,10 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
       return e ? (uint64_t)std::atoll(e) : 0ull;
     }();
     if (groups < min_groups) FC_DECLINE("too few consumer blocks");
-    const unsigned grid = (unsigned)std::min<uint64_t>(groups, (uint64_t)num_sms() * (WB == 3 ? 2 : 4));
+    const unsigned grid = (unsigned)std::min<uint64_t>(groups, (uint64_t)num_sms() * (fc_cps() ? fc_cps() : (WB == 3 ? 2 : 4)));
+    // balanced tile ranges with consumer blocks split between neighbouring CTAs (C5a: 512 blocks on
+    // 296 CTAs -- whole blocks left 40 CTAs idle and 108 SMs with 4 blocks against 3.46 on average)
+    fa.sem = (sem && grid >= 2 && grid < (unsigned)kFcSemPerOp && (groups % grid) != 0) ? sem : nullptr;
     switch (g.M) {
       case 1: return WB == 3 ? dispatch_fc<1, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<1, 2>(ma, fa, nra, nrb, grid, smem, st);
       case 2: return WB == 3 ? dispatch_fc<2, 3>(ma, fa, nra, nrb, grid, smem, st) : dispatch_fc<2, 2>(ma, fa, nra, nrb, grid, smem, st);
@@ -309,9 +326,9 @@ bool try_launch_gemm_fc_wb(const GDesc& g, const GDesc& g3, int tin, cudaStream_
   }
 }
 
-template bool try_launch_gemm_fc<float2>(const GDesc&, const GDesc&, int, cudaStream_t);
-template bool try_launch_gemm_fc_wb<float2>(const GDesc&, const GDesc&, int, cudaStream_t, int);
-template bool try_launch_gemm_fc_wb<double2>(const GDesc&, const GDesc&, int, cudaStream_t, int);
-template bool try_launch_gemm_fc<double2>(const GDesc&, const GDesc&, int, cudaStream_t);
+template bool try_launch_gemm_fc<float2>(const GDesc&, const GDesc&, int, cudaStream_t, uint32_t*);
+template bool try_launch_gemm_fc_wb<float2>(const GDesc&, const GDesc&, int, cudaStream_t, int, uint32_t*);
+template bool try_launch_gemm_fc_wb<double2>(const GDesc&, const GDesc&, int, cudaStream_t, int, uint32_t*);
+template bool try_launch_gemm_fc<double2>(const GDesc&, const GDesc&, int, cudaStream_t, uint32_t*);
 
 }  // namespace tnb

@@ -63,6 +63,7 @@ struct DevTables {
   LeafRec* leaves = nullptr;
   ScalarRec* scalars = nullptr;
   ProgramRec* progs = nullptr;
+  uint32_t* fc_sem = nullptr;   // k_gemm_fc split-block counters: [lane][feed op][kFcSemPerOp], zeroed
   cudaStream_t side[kMaxLanes - 1] = {};   // slice lanes 1.. (tn_contract_sliced, one window each)
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes - 1] = {};
   // graphs are captured and replayed on a library stream ordered after / before the caller's (the
@@ -94,6 +95,8 @@ struct tn_plan {
   uint64_t all_launches = 0;
   uint64_t graph_launches = 0;   // cudaGraphLaunch calls (each replays a captured slice range)
   bool batchable = false;   // every per-slice op is an interpreter run -> slices can run batched
+  std::vector<int32_t> feed_slot;   // per op: index among the OP_GROUP_FEED ops (their fc_sem regions)
+  int32_t n_feed = 0;
   std::vector<int32_t> waveA;   // per op: wave of independent prefix ops (-1: phase B), see prefix_waves
   ~tn_plan() {
     for (auto& kv : dev) {
@@ -102,6 +105,7 @@ struct tn_plan {
       cudaFree(kv.second.leaves);
       cudaFree(kv.second.scalars);
       cudaFree(kv.second.progs);
+      cudaFree(kv.second.fc_sem);
       for (int l = 0; l < kMaxLanes - 1; ++l) {
         if (kv.second.side[l]) cudaStreamDestroy(kv.second.side[l]);
         if (kv.second.ev_join[l]) cudaEventDestroy(kv.second.ev_join[l]);
@@ -542,6 +546,15 @@ tn_status ensure_dev(tn_plan* pl, DevTables** out) {
     CU(up((void**)&t.leaves, pl->leaves.data(), pl->leaves.size() * sizeof(LeafRec)));
     CU(up((void**)&t.scalars, pl->scalars.data(), pl->scalars.size() * sizeof(ScalarRec)));
     CU(up((void**)&t.progs, pl->progs.data(), pl->progs.size() * sizeof(ProgramRec)));
+    pl->feed_slot.assign(pl->ops.size(), 0);
+    pl->n_feed = 0;
+    for (size_t oi = 0; oi < pl->ops.size(); ++oi)
+      if (pl->ops[oi].type == OP_GROUP_FEED) pl->feed_slot[oi] = pl->n_feed++;
+    {
+      const size_t sem_bytes = (size_t)kMaxLanes * std::max(pl->n_feed, 1) * kFcSemPerOp * sizeof(uint32_t);
+      CU(cudaMalloc((void**)&t.fc_sem, sem_bytes));
+      CU(cudaMemset(t.fc_sem, 0, sem_bytes));
+    }
     for (int l = 0; l < kMaxLanes - 1; ++l) {
       CU(cudaStreamCreateWithFlags(&t.side[l], cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&t.ev_join[l], cudaEventDisableTiming));
@@ -714,7 +727,7 @@ bool group_desc(const tn_plan* pl, const OpRec& op, T* ws, uint64_t j, uint64_t 
 
 template <typename T>
 tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, uint64_t j, uint64_t rel,
-                  cudaStream_t st) {
+                  cudaStream_t st, int lane = 0) {
   for (int oi = op_b; oi < op_e; ++oi) {
     const OpRec& op = pl->ops[oi];
     if (op.type == OP_BIG) {
@@ -778,7 +791,9 @@ tn_status run_ops(tn_plan* pl, const DevTables& dt, int op_b, int op_e, T* ws, u
             ps.pr.flops = 8.0 * (std::ldexp(1.0, g.out_rank + g.M) + std::ldexp(1.0, g3.out_rank + g3.M));
             const bool fused = (std::is_same<T, float2>::value && fc_tc_enabled() && try_launch_fc_tc(g, g3, tin, st)) ||
                                (std::is_same<T, float2>::value && fc_hm_enabled() && try_launch_fc_hm(g, g3, tin, st)) ||
-                               try_launch_gemm_fc<T>(g, g3, tin, st);
+                               try_launch_gemm_fc<T>(g, g3, tin, st,
+                                                     dt.fc_sem + ((size_t)lane * std::max(pl->n_feed, 1) + pl->feed_slot[oi]) *
+                                                                     kFcSemPerOp);
             ps.cancel = !fused;
             if (fused) {
               ++oi;
@@ -1054,7 +1069,7 @@ tn_status sliced_body(tn_plan* pl, DevTables* dt, uint64_t begin, uint64_t end, 
     const uint64_t lane = L >= 2 ? (j - begin) % L : 0;
     cudaStream_t sj = lane ? dt->side[lane - 1] : st;
     const uint64_t rel = lane ? window_rel_host(lane, base_bytes / es, pl->h.arena_elems) : 0ull;
-    if ((s = run_ops<T>(pl, *dt, pr.opB_begin, pr.opB_end, ws, j, rel, sj)) != TN_OK) return s;
+    if ((s = run_ops<T>(pl, *dt, pr.opB_begin, pr.opB_end, ws, j, rel, sj, (int)lane)) != TN_OK) return s;
     {
       const uint32_t A = 1u << pl->h.n_open;
       k_finalize<T><<<(A + 127) / 128, 128, 0, sj>>>(dt->scalars, pr.scal_begin, pr.scal_end, ws, j, pr.log2_scale,

@@ -399,7 +399,9 @@ def test_fused_groups_vs_oracle(dtype, n, p, k, orderer):
 
 
 FUSED_PAIR = {"k_gemm_fc", "k_fc_tc", "k_fc_hm"}   # the kernels of an OP_GROUP_FEED pair (SIMT / tcgen05 / mma.sync)
-FC_ENV = {"tc": {"TNB_FC_TC": "1"}, "simt": {"TNB_FC_TC": "0", "TNB_FC_HM": "0"}, "hm": {"TNB_FC_TC": "0", "TNB_FC_HM": "1"}}
+FC_ENV = {"tc": {"TNB_FC_TC": "1"}, "simt": {"TNB_FC_TC": "0", "TNB_FC_HM": "0", "TNB_FC_SPLIT": "0"},
+          "hm": {"TNB_FC_TC": "0", "TNB_FC_HM": "1"},
+          "split": {"TNB_FC_TC": "0", "TNB_FC_HM": "0", "TNB_FC_SPLIT": "1"}}
 
 
 @pytest.mark.parametrize("kernel", ["tc", "simt", "hm"])
@@ -408,7 +410,7 @@ FC_ENV = {"tc": {"TNB_FC_TC": "1"}, "simt": {"TNB_FC_TC": "0", "TNB_FC_HM": "0"}
 def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused, kernel, monkeypatch):
     """OP_GROUP_FEED: a GEMM-shaped group whose output is a full input of the next group runs as ONE
     launch (the intermediate is never written) -- k_fc_tc (tcgen05, TNB_FC_TC=1), k_fc_hm (mma.sync,
-    the default) or k_gemm_fc (FP32 SIMT) when the shape qualifies; the contraction still matches the oracle
+    TNB_FC_HM=1) or k_gemm_fc (FP32 SIMT, the default) when the shape qualifies; the contraction still matches the oracle
     (c64 tolerance), and the fused launch is the one that ran (profile records).  Pairs whose
     consumer output has fewer bits than a k_gemm_fc tile (fused=False) run as the two groups."""
     for key, val in FC_ENV[kernel].items():
@@ -431,11 +433,12 @@ def test_feed_pairs_run_fused_and_match_oracle(n, p, k, fused, kernel, monkeypat
     assert rel(got, ref) < TOL[T.TN_C64]
 
 
-@pytest.mark.parametrize("fast", ["tc", "hm"])
+@pytest.mark.parametrize("fast", ["tc", "hm", "split"])
 def test_fc_fast_kernels_run_on_c5a_and_match_simt_per_slice(fast, monkeypatch):
     """C5a's producer -> consumer pair (R = 26 -> 21, the bench's largest launch) runs on k_fc_tc
-    (tcgen05) / k_fc_hm (mma.sync, the default); every per-slice partial agrees with the FP32 SIMT
-    k_gemm_fc within the c64 tolerance."""
+    (tcgen05) / k_fc_hm (mma.sync) / k_gemm_fc with consumer blocks split between neighbouring CTAs
+    (TNB_FC_SPLIT=1: 512 blocks on 296 CTAs, so the split path really runs); every per-slice partial
+    agrees with the default FP32 SIMT k_gemm_fc within the c64 tolerance."""
     plan, g, ga, be, meta = _bench_plan()
     n = plan.n_slices
     parts = {}
@@ -449,7 +452,7 @@ def test_fc_fast_kernels_run_on_c5a_and_match_simt_per_slice(fast, monkeypatch):
         ran = {r["kernel"] for r in plan.profile_records()}
         plan.profile(False)
         plan.profile_read()
-        assert {"tc": "k_fc_tc", "hm": "k_fc_hm", "simt": "k_gemm_fc"}[kern] in ran, sorted(ran)
+        assert {"tc": "k_fc_tc", "hm": "k_fc_hm", "simt": "k_gemm_fc", "split": "k_gemm_fc"}[kern] in ran, sorted(ran)
         h = part.cpu().tolist()
         parts[kern] = [complex(h[2 * j], h[2 * j + 1]) for j in range(n)]
     scale = max(abs(v) for v in parts["simt"])
