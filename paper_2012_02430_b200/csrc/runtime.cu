@@ -555,17 +555,8 @@ tn_status ensure_dev(tn_plan* pl, DevTables** out) {
       CU(cudaMalloc((void**)&t.fc_sem, sem_bytes));
       CU(cudaMemset(t.fc_sem, 0, sem_bytes));
     }
-    // TNB_LANE_PRIO (experiment): 1 = side lanes' priorities graded from the greatest down, 2 = odd
-    // lanes at the greatest priority (lanes then drift apart instead of running in lockstep)
-    const char* lp = std::getenv("TNB_LANE_PRIO");
-    const int prio_mode = lp ? std::atoi(lp) : 0;
-    int prio_lo = 0, prio_hi = 0;
-    CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     for (int l = 0; l < kMaxLanes - 1; ++l) {
-      int pr = prio_lo;
-      if (prio_mode == 1) pr = prio_hi + (l * (prio_lo - prio_hi + 1)) / (kMaxLanes - 1);
-      if (prio_mode == 2) pr = (l & 1) ? prio_lo : prio_hi;   // side[l] is lane l + 1
-      CU(cudaStreamCreateWithPriority(&t.side[l], cudaStreamNonBlocking, pr));
+      CU(cudaStreamCreateWithFlags(&t.side[l], cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&t.ev_join[l], cudaEventDisableTiming));
     }
     CU(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
