@@ -25,6 +25,16 @@
 #define FC_XV_AT 2   // consumer loads at x = FC_XV_AT * K / 2 (0: before the GEMM, 2: after it; 0 and 1 spill at 4x4)
 #endif
 
+#ifndef FC_U1
+#define FC_U1 1      // keep the chunk-load and B' rebuild loops rolled: 4,144 vs 6,480 SASS instructions, fewer
+                     // instruction-fetch stalls (launch 212 vs 221 us, C5a 101.8 vs 101.1 /s; `profiles/r02/session4/`)
+#endif
+#if FC_U1
+#define FC_LOOP_PRAGMA _Pragma("unroll 1")
+#else
+#define FC_LOOP_PRAGMA
+#endif
+
 namespace tnb {
 
 constexpr int kFcMaxV = 1;   // consumer inputs (besides T) that hold output bits
@@ -190,8 +200,10 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
     const uint32_t np = a.nrows[u] << (a.nch[u] - a.lv[u]);
     const uint32_t* tab = smu + a.sm_dep[u];
     if (a.lv[u]) {
+FC_LOOP_PRAGMA
       for (uint32_t c = tid; c < np; c += kThreads) cp_async16(dst + (c << 1), src + tab[c]);
     } else {
+FC_LOOP_PRAGMA
       for (uint32_t c = tid; c < np; c += kThreads) cp_async8(dst + c, src + tab[c]);
     }
   };
@@ -270,6 +282,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? FC_OCC : 2 * FC_OCC)) k_g
     advance_lookahead();
     if (refix) {
       const float2* sBraw = sm + a.sm_in[1][cslot[1]];
+FC_LOOP_PRAGMA
       for (uint32_t e = tid; e < (uint32_t)K * nB; e += kThreads) {
         const uint32_t x = e >> a.nch[1], idx = e & (nB - 1u);
         float2 b = sBraw[((uint32_t)a.row[1][x] << a.nch[1]) + idx];
