@@ -22,6 +22,16 @@
 
 #include "plan_format.h"
 
+#ifndef GEMM_U1
+#define GEMM_U1 1    // k_gemm's chunk-load and B' rebuild loops kept rolled (as FC_U1): about half the SASS,
+                     // C5a 101.8 vs 101.0 /s, C4b 105.4 vs 103.0 /s (`profiles/r02/session4/gemm_u1/`)
+#endif
+#if GEMM_U1
+#define GEMM_LOOP_PRAGMA _Pragma("unroll 1")
+#else
+#define GEMM_LOOP_PRAGMA
+#endif
+
 namespace tnb {
 
 // ------------------------------------------------------------------ complex helpers
@@ -959,8 +969,10 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
     const uint32_t np = a.nrows[u] << (a.nch[u] - a.lv[u]);
     const uint32_t* tab = smu + a.sm_dep[u];
     if (a.lv[u]) {
+GEMM_LOOP_PRAGMA
       for (uint32_t c = tid; c < np; c += kGemmThreads) cp_async16(dst + (c << 1), src + tab[c]);
     } else {
+GEMM_LOOP_PRAGMA
       for (uint32_t c = tid; c < np; c += kGemmThreads) cp_async8(dst + c, src + tab[c]);
     }
   };
@@ -1014,6 +1026,7 @@ __global__ void __launch_bounds__(32 << WB, (WB == 3 ? 2 : 4)) k_gemm(const MArg
     // then two FFMA2 on operands read straight from shared memory (no register shuffles)
     if (refix) {
       const float2* sBraw = sm + a.sm_in[1][cslot[1]];
+GEMM_LOOP_PRAGMA
       for (uint32_t e = tid; e < (uint32_t)K * nB; e += kGemmThreads) {
         const uint32_t x = e >> a.nch[1], idx = e & (nB - 1u);
         float2 b = sBraw[((uint32_t)a.row[1][x] << a.nch[1]) + idx];

@@ -236,11 +236,84 @@ FC_LOOP_PRAGMA
   const uint32_t ymask = (1u << f.M3) - 1u;
 
   uint64_t oacc[RA][RB];                   // consumer accumulators (packed complex)
+  uint64_t acc[RA][RB];                    // the tile's T block
+  float2 xv[kFcMaxV][RA][RB];              // consumer factors of the tile (T's partner values)
+  float2 c3 = make_float2(0.f, 0.f);
   uint32_t vcur[kFcMaxV];
 #pragma unroll
   for (int v = 0; v < kFcMaxV; ++v) vcur[v] = 0u;
   int fixed_ver = -1;
+  // consumer: oacc += C3_y X(o, y) T[o, y]
+  auto consume = [&]() {
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+      for (int j = 0; j < RB; ++j) {
+        float2 xx = c3;
+#pragma unroll
+        for (int v = 0; v < kFcMaxV; ++v)
+          if (v < f.nv) xx = cmul(xx, xv[v][i][j]);
+        const float2 tv = f2_unpack(acc[i][j]);
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(oacc[i][j]) : "l"(f2_pack(tv.x, tv.x)), "l"(f2_pack(xx.x, xx.y)));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(oacc[i][j]) : "l"(f2_pack(-tv.y, tv.y)), "l"(f2_pack(xx.y, xx.x)));
+      }
+  };
+  // store the consumer block that tile tl (summed value yy, o part ob) ends
+  auto flush = [&](uint64_t tl, uint32_t yy, uint32_t ob) {
+    float2* ot = out3 + ob + othr;
+    if (tl - yy >= t0 && yy == ymask) {    // the whole block ran here: the consumer output is final
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
+    } else {
+      // a block split between this CTA and its neighbour: out = P_first + P_second, the first
+      // arriving CTA stores its partial and publishes it, the second adds its own (float
+      // addition commutes, so the bits do not depend on the arrival order)
+      uint32_t* sem = f.sem + (tl - yy < t0 ? blockIdx.x : blockIdx.x + 1);
+      __syncthreads();
+      if (tid == 0) s_arrive = atomicAdd(sem, 1u);
+      __syncthreads();
+      if (s_arrive == 0u) {
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < RB; ++j) __stcg(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) atomicAdd(sem, 1u);   // published (2 arrivals + 1 publish = 3)
+      } else {
+        if (tid == 0) {
+          while (atomicAdd(sem, 0u) != 3u) __nanosleep(64);
+          *sem = 0u;                        // zero again for the next launch (stream-ordered)
+        }
+        __syncthreads();
+        __threadfence();
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < RB; ++j) {
+            const float2 p = __ldcg(ot + ora[i] + orb[j]);
+            const float2 q = f2_unpack(oacc[i][j]);
+            __stcs(ot + ora[i] + orb[j], make_float2(p.x + q.x, p.y + q.y));
+          }
+      }
+    }
+  };
+  // (Software-pipelining the consumer step -- tile t's X loads consumed after the barrier and chunk
+  // issue of tile t + 1 -- was measured slower: 128 registers with spills, 225-227 vs 209.5 us.)
   for (uint64_t tile = t0; tile < t1; ++tile) {
+    const bool refix = ver[1] != fixed_ver || a.c_tile_dep;
+    if (refix && tid < (uint32_t)K) {
+      float2 c = make_float2(1.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kMaxIn - 2; ++t)
+        if (t < a.nc) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + curc[t] + a.cgx[t][tid]));
+      Cs[tid] = c;
+    }
+    if (D <= 1) cp_async_wait<0>(); else if (D == 2) cp_async_wait<1>(); else cp_async_wait<2>();
+    __syncthreads();
+    advance_lookahead();
     const int r = __ffsll((long long)~tile) - 1;
     const uint32_t y = (uint32_t)tile & ymask;
     if (y == 0u || tile == t0) {           // a new consumer output block (or this CTA's part of one)
@@ -252,7 +325,7 @@ FC_LOOP_PRAGMA
 #pragma unroll
       for (int v = 0; v < kFcMaxV; ++v) vcur[v] = v < f.nv ? (uint32_t)fmap(obo, f.vmask[v], f.vpv[v]) : 0u;
     }
-    const float2 c3 = C3s[y];
+    c3 = C3s[y];
     if (pf_lane && y < ymask)              // the next tile (same block, y + 1): its X lines into L2
       asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const float2*>(f.vin[0]) + vcur[0] + pfo + f.vgx[0][y + 1]));
 #if FC_PREFETCH
@@ -269,17 +342,6 @@ FC_LOOP_PRAGMA
             asm volatile("prefetch.global.L1 [%0];" ::"l"(src + va[v][i] + vb[v][j]));
       }
 #endif
-    const bool refix = ver[1] != fixed_ver || a.c_tile_dep;
-    if (refix && tid < (uint32_t)K) {
-      float2 c = make_float2(1.f, 0.f);
-#pragma unroll
-      for (int t = 0; t < kMaxIn - 2; ++t)
-        if (t < a.nc) c = cmul(c, __ldg(static_cast<const float2*>(a.cin[t]) + curc[t] + a.cgx[t][tid]));
-      Cs[tid] = c;
-    }
-    if (D <= 1) cp_async_wait<0>(); else if (D == 2) cp_async_wait<1>(); else cp_async_wait<2>();
-    __syncthreads();
-    advance_lookahead();
     if (refix) {
       const float2* sBraw = sm + a.sm_in[1][cslot[1]];
 FC_LOOP_PRAGMA
@@ -294,14 +356,12 @@ FC_LOOP_PRAGMA
     }
     const float2* sA = sm + a.sm_in[0][cslot[0]] + iathr;
     const float4* sB = bf + ibthr;
-    uint64_t acc[RA][RB];
 #pragma unroll
     for (int i = 0; i < RA; ++i)
 #pragma unroll
       for (int j = 0; j < RB; ++j) acc[i][j] = 0ull;
-    // consumer factors of this tile (T's partner values), issued half-way through the GEMM so
-    // the second half covers their latency without holding the registers for the whole tile
-    float2 xv[kFcMaxV][RA][RB];
+    // the X loads are issued inside the GEMM (4 x 2 blocks: at its start) or after it (4 x 4:
+    // earlier spills)
 #pragma unroll
     for (int x = 0; x < K; ++x) {
       if (x == (XV * K) / 2) {
@@ -342,69 +402,20 @@ FC_LOOP_PRAGMA
             for (int j = 0; j < RB; ++j) xv[v][i][j] = __ldg(src + va[v][i] + vb[v][j]);
         }
     }
-    // consumer: oacc += C3_y X(o, y) T[o, y]
-#pragma unroll
-    for (int i = 0; i < RA; ++i)
-#pragma unroll
-      for (int j = 0; j < RB; ++j) {
-        float2 xx = c3;
-#pragma unroll
-        for (int v = 0; v < kFcMaxV; ++v)
-          if (v < f.nv) xx = cmul(xx, xv[v][i][j]);
-        const float2 tv = f2_unpack(acc[i][j]);
-        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(oacc[i][j]) : "l"(f2_pack(tv.x, tv.x)), "l"(f2_pack(xx.x, xx.y)));
-        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(oacc[i][j]) : "l"(f2_pack(-tv.y, tv.y)), "l"(f2_pack(xx.y, xx.x)));
-      }
-    if (y == ymask || tile + 1 == t1) {    // last y of the block (or of this CTA's part of it)
-      float2* ot = out3 + (obase & f.omask) + othr;
-      if (tile - y >= t0 && y == ymask) {  // the whole block ran here: the consumer output is final
-#pragma unroll
-        for (int i = 0; i < RA; ++i)
-#pragma unroll
-          for (int j = 0; j < RB; ++j) __stcs(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
-      } else {
-        // a block split between this CTA and its neighbour: out = P_first + P_second, the first
-        // arriving CTA stores its partial and publishes it, the second adds its own (float
-        // addition commutes, so the bits do not depend on the arrival order)
-        uint32_t* sem = f.sem + (tile - y < t0 ? blockIdx.x : blockIdx.x + 1);
-        __syncthreads();
-        if (tid == 0) s_arrive = atomicAdd(sem, 1u);
-        __syncthreads();
-        if (s_arrive == 0u) {
-#pragma unroll
-          for (int i = 0; i < RA; ++i)
-#pragma unroll
-            for (int j = 0; j < RB; ++j) __stcg(ot + ora[i] + orb[j], f2_unpack(oacc[i][j]));
-          __threadfence();
-          __syncthreads();
-          if (tid == 0) atomicAdd(sem, 1u);   // published (2 arrivals + 1 publish = 3)
-        } else {
-          if (tid == 0) {
-            while (atomicAdd(sem, 0u) != 3u) __nanosleep(64);
-            *sem = 0u;                        // zero again for the next launch (stream-ordered)
-          }
-          __syncthreads();
-          __threadfence();
-#pragma unroll
-          for (int i = 0; i < RA; ++i)
-#pragma unroll
-            for (int j = 0; j < RB; ++j) {
-              const float2 p = __ldcg(ot + ora[i] + orb[j]);
-              const float2 q = f2_unpack(oacc[i][j]);
-              __stcs(ot + ora[i] + orb[j], make_float2(p.x + q.x, p.y + q.y));
-            }
-        }
-      }
-    }
+    consume();
+    if (y == ymask || tile + 1 == t1)      // last y of the block (or of this CTA's part of it)
+      flush(tile, y, (uint32_t)(obase & f.omask));
 #pragma unroll
     for (int u = 0; u < 2; ++u)
       if (fbit[u][r] != fcum[u][r]) {
         ++ver[u];
         cslot[u] = cslot[u] + 1 == S ? 0 : cslot[u] + 1;
       }
+    if (a.c_tile_dep) {                    // constants holding output bits (else their offsets stay 0)
 #pragma unroll
-    for (int t = 0; t < kMaxIn - 2; ++t)
-      if (t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
+      for (int t = 0; t < kMaxIn - 2; ++t)
+        if (t < a.nc) curc[t] = curc[t] + fbit[2 + t][r] - fcum[2 + t][r];
+    }
     obase = obase + pbit[r] - pcum[r];
   }
   cp_async_wait<0>();
