@@ -19,7 +19,8 @@
 #define FC_OCC 2
 #endif
 #ifndef FC_PREFETCH
-#define FC_PREFETCH 0   // prefetch.global.L1 of the consumer factors: measured no gain (0.228 ms either way)
+#define FC_PREFETCH 0   // prefetch.global.L1 of the consumer factors: no gain in round 1 (0.228 ms either way),
+                        // slower in the final state (224.4 vs 209.7 us, C5a 99.0 vs 102.8 /s; session4/fc_prefetch)
 #endif
 #ifndef FC_XV_AT
 #define FC_XV_AT 2   // consumer loads at x = FC_XV_AT * K / 2 (0: before the GEMM, 2: after it; 0 and 1 spill at 4x4)
